@@ -1,0 +1,154 @@
+/*
+ * hap_b200.h — C ABI of the B200 executor for HAP-synthesized programs.
+ *
+ * Plain pointers, sizes and a CUDA stream handle (cudaStream_t passed as
+ * void*); no torch or C++ types cross this boundary.  Every call is
+ * asynchronous on `stream` and returns a hap_status; hap_last_error() gives
+ * the message of the last failure on the calling thread.
+ *
+ * The entry points replace the per-instruction work of the reference
+ * interpreter (pkg/src/shardplan/interpreter.py), which executes a
+ * distributed program on m simulated devices with numpy.  The reference
+ * citation is given on each declaration; the reference-side binding a
+ * maintainer would add is in INTEGRATION.md.
+ *
+ * Layout conventions: tensors are dense row-major.  A rank-r tensor sliced
+ * along axis d is viewed as [outer, extent, inner] with
+ * outer = prod(shape[:d]) and inner = prod(shape[d+1:]).  `sm_cap` bounds the
+ * number of SMs a kernel may occupy (0 = whole GPU); it is how per-rank
+ * heterogeneity is emulated on a homogeneous box.
+ */
+#ifndef HAP_B200_H
+#define HAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HAP_OK = 0,
+  HAP_ERR_ARG = 1,
+  HAP_ERR_CUDA = 2,
+  HAP_ERR_NCCL = 3,
+  HAP_ERR_UNSUPPORTED = 4
+} hap_status;
+
+typedef enum { HAP_F32 = 0, HAP_BF16 = 1 } hap_dtype;
+
+/* ElemwiseUnary tags (graph_ir.py UNARY_TAGS) and ElemwiseBinary tags. */
+typedef enum { HAP_EXP = 0, HAP_NEG = 1, HAP_RELU = 2, HAP_SIGMOID = 3, HAP_TANH = 4 } hap_unary_tag;
+typedef enum { HAP_ADD = 0, HAP_MUL = 1 } hap_binary_tag;
+
+/* GEMM engine selection reported by hap_matmul_engine(). */
+typedef enum { HAP_GEMM_TCGEN05 = 0, HAP_GEMM_SIMT = 1 } hap_gemm_engine;
+
+const char* hap_last_error(void);
+int hap_abi_version(void);
+/* SM count of the current device (148 on B200); -1 without a device. */
+int hap_sm_count(void);
+
+/* ---- compute instructions ------------------------------------------------ */
+
+/* matmul — interpreter.py:139-140 (`a @ b` per device) and its adjoints.
+ * C[M,N] (+)= op(A)[M,K] . op(B)[K,N], op(X) = X or X^T (trans flag, X then
+ * stored transposed).  bf16 inputs run on tcgen05 tensor cores (TMA-fed,
+ * TMEM accumulator, fp32 accumulate) when strides are 16-byte aligned;
+ * other shapes and fp32 inputs run a CUDA-core kernel.  Inputs A and B share
+ * `in_dtype`; `accumulate` adds into C. */
+hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
+                      int transB, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                      hap_dtype in_dtype, hap_dtype out_dtype, int accumulate, int sm_cap,
+                      void* stream);
+/* Which engine hap_matmul would use for these arguments (no launch). */
+int hap_matmul_engine(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
+                      int transB, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype);
+
+/* elemwise_unary — interpreter.py:141-143. y = f(x) over n elements. */
+hap_status hap_unary(int tag, const void* x, hap_dtype x_dtype, void* y, hap_dtype y_dtype,
+                     int64_t n, int sm_cap, void* stream);
+/* Adjoint of elemwise_unary: dx (+)= dy * f'(x), using x (relu) or y = f(x). */
+hap_status hap_unary_grad(int tag, const void* x, const void* y, hap_dtype xy_dtype,
+                          const void* dy, hap_dtype dy_dtype, void* dx, hap_dtype dx_dtype,
+                          int64_t n, int accumulate, int sm_cap, void* stream);
+
+/* elemwise_binary — interpreter.py:144-148. out = a (+|*) b. */
+hap_status hap_binary(int tag, const void* a, const void* b, hap_dtype in_dtype, void* out,
+                      hap_dtype out_dtype, int64_t n, int sm_cap, void* stream);
+/* Adjoint of mul: da (+)= dy*b and db (+)= dy*a in one pass (da/db may be
+ * NULL to skip; when a==b and da==db the two contributions are summed). */
+hap_status hap_mul_grad(const void* a, const void* b, hap_dtype in_dtype, const void* dy,
+                        hap_dtype dy_dtype, void* da, void* db, hap_dtype d_dtype, int64_t n,
+                        int accumulate, int sm_cap, void* stream);
+
+/* reduce — interpreter.py:149-150 (np.sum over `dims`).  x has `rank` dims
+ * given by `shape`; bit d of dims_mask selects axis d.  y is fp32 or bf16 in
+ * the shape with the reduced axes removed; accumulation is fp32. */
+hap_status hap_reduce(const void* x, hap_dtype x_dtype, const int64_t* shape, int rank,
+                      uint32_t dims_mask, void* y, hap_dtype y_dtype, int accumulate, int sm_cap,
+                      void* stream);
+/* Adjoint of reduce: dx[shape] (+)= broadcast of dy over the reduced axes. */
+hap_status hap_unreduce(const void* dy, hap_dtype dy_dtype, const int64_t* shape, int rank,
+                        uint32_t dims_mask, void* dx, hap_dtype dx_dtype, int accumulate,
+                        int sm_cap, void* stream);
+
+/* ---- data movement ------------------------------------------------------- */
+
+/* Block copy along one axis — the slicing convention of slice_by_sizes
+ * (interpreter.py:81-91) and *_shard sources (interpreter.py:135-138):
+ * dst[o, dst_off + i, :] (+)= src[o, src_off + i, :] for i < count, with both
+ * tensors viewed as [outer, extent, inner].  Converts dtype on the fly. */
+hap_status hap_copy_block(const void* src, hap_dtype src_dtype, int64_t src_extent,
+                          int64_t src_off, void* dst, hap_dtype dst_dtype, int64_t dst_extent,
+                          int64_t dst_off, int64_t outer, int64_t count, int64_t inner,
+                          int accumulate, int sm_cap, void* stream);
+/* y (+)= alpha * x with dtype conversion (identity, adds, casts, scaling). */
+hap_status hap_axpy(float alpha, const void* x, hap_dtype x_dtype, void* y, hap_dtype y_dtype,
+                    int64_t n, int accumulate, int sm_cap, void* stream);
+hap_status hap_fill(void* y, hap_dtype y_dtype, float value, int64_t n, void* stream);
+
+/* SGD step on an fp32 master copy with a bf16/fp32 working copy:
+ * master -= lr * grad; weight = (dtype) master. */
+hap_status hap_sgd(float* master, const float* grad, void* weight, hap_dtype w_dtype, float lr,
+                   int64_t n, int sm_cap, void* stream);
+
+/* ---- collectives (NCCL over NVLink / NVSwitch) ---------------------------
+ * One communicator per process (rank = device index of the program).  The
+ * 128-byte unique id is created on rank 0 and broadcast by the host. */
+int hap_nccl_version(void);
+hap_status hap_comm_unique_id(uint8_t* out128);
+hap_status hap_comm_init(void** comm, const uint8_t* id128, int nranks, int rank);
+hap_status hap_comm_destroy(void* comm);
+
+/* all_reduce — interpreter.py:74-78 (sum, replicated to every rank). */
+hap_status hap_all_reduce(void* comm, const void* send, void* recv, int64_t count,
+                          hap_dtype dtype, void* stream);
+/* all_gather along the outer-most blocked axis — interpreter.py:69-71 with
+ * uneven shards.  Rank j contributes counts[j] elements; the result is the
+ * rank-ordered concatenation written to recv (total = sum(counts)).
+ * padded != 0 uses one ncclAllGather over max(counts)-padded chunks
+ * (`scratch` must hold nranks*max(counts) elements) — the padded-gather cost
+ * model (cost_model.py:218); padded == 0 uses grouped send/recv. */
+hap_status hap_all_gather_v(void* comm, const void* send, void* recv, const int64_t* counts,
+                            hap_dtype dtype, int padded, void* scratch, void* stream);
+/* grouped_broadcast — cost_model.py:210 semantics: nranks broadcasts of the
+ * actual (unpadded) shards; result identical to hap_all_gather_v. */
+hap_status hap_grouped_broadcast(void* comm, const void* send, void* recv, const int64_t* counts,
+                                 hap_dtype dtype, void* stream);
+/* reduce_scatter — interpreter.py:94-96: sum over ranks then keep this
+ * rank's counts[rank]-element chunk of the rank-ordered layout of `send`.
+ * `scratch` must hold nranks*max(counts) elements (padded layout). */
+hap_status hap_reduce_scatter_v(void* comm, const void* send, void* recv, const int64_t* counts,
+                                hap_dtype dtype, void* scratch, void* stream);
+/* all_to_all — interpreter.py:99-101: send chunk k (send_counts[k] elements,
+ * rank-ordered in `send`) to rank k; receive recv_counts[k] from rank k into
+ * rank-ordered `recv`. */
+hap_status hap_all_to_all_v(void* comm, const void* send, const int64_t* send_counts, void* recv,
+                            const int64_t* recv_counts, hap_dtype dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HAP_B200_H */

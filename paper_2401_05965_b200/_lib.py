@@ -1,0 +1,105 @@
+"""ctypes binding of the C ABI in include/hap_b200.h (libhap_b200.so).
+
+This is the only door to the GPU kernels.  There is no fallback: if the
+library is missing or does not export a declared symbol, loading raises
+:class:`LibraryError` and the executor refuses to run.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+from ctypes import c_float, c_int, c_int64, c_uint32, c_void_p, POINTER
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhap_b200.so")
+HEADER = os.path.join(os.path.dirname(PKG), "include", "hap_b200.h")
+
+F32, BF16 = 0, 1
+UNARY_TAGS = {"exp": 0, "neg": 1, "relu": 2, "sigmoid": 3, "tanh": 4}
+BINARY_TAGS = {"add": 0, "mul": 1}
+GEMM_TCGEN05, GEMM_SIMT = 0, 1
+
+_P = c_void_p
+_I64P = POINTER(c_int64)
+
+# name -> (restype, argtypes); must cover every function include/hap_b200.h declares.
+SIGNATURES = {
+    "hap_last_error": (ctypes.c_char_p, []),
+    "hap_abi_version": (c_int, []),
+    "hap_sm_count": (c_int, []),
+    "hap_matmul": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, _P, c_int64, c_int64, c_int64,
+                           c_int64, c_int, c_int, c_int, c_int, _P]),
+    "hap_matmul_engine": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, c_int64, c_int64, c_int64,
+                                  c_int]),
+    "hap_unary": (c_int, [c_int, _P, c_int, _P, c_int, c_int64, c_int, _P]),
+    "hap_unary_grad": (c_int, [c_int, _P, _P, c_int, _P, c_int, _P, c_int, c_int64, c_int, c_int, _P]),
+    "hap_binary": (c_int, [c_int, _P, _P, c_int, _P, c_int, c_int64, c_int, _P]),
+    "hap_mul_grad": (c_int, [_P, _P, c_int, _P, c_int, _P, _P, c_int, c_int64, c_int, c_int, _P]),
+    "hap_reduce": (c_int, [_P, c_int, _I64P, c_int, c_uint32, _P, c_int, c_int, c_int, _P]),
+    "hap_unreduce": (c_int, [_P, c_int, _I64P, c_int, c_uint32, _P, c_int, c_int, c_int, _P]),
+    "hap_copy_block": (c_int, [_P, c_int, c_int64, c_int64, _P, c_int, c_int64, c_int64, c_int64,
+                               c_int64, c_int64, c_int, c_int, _P]),
+    "hap_axpy": (c_int, [c_float, _P, c_int, _P, c_int, c_int64, c_int, c_int, _P]),
+    "hap_fill": (c_int, [_P, c_int, c_float, c_int64, _P]),
+    "hap_sgd": (c_int, [_P, _P, _P, c_int, c_float, c_int64, c_int, _P]),
+    "hap_nccl_version": (c_int, []),
+    "hap_comm_unique_id": (c_int, [ctypes.c_char_p]),
+    "hap_comm_init": (c_int, [POINTER(c_void_p), ctypes.c_char_p, c_int, c_int]),
+    "hap_comm_destroy": (c_int, [_P]),
+    "hap_all_reduce": (c_int, [_P, _P, _P, c_int64, c_int, _P]),
+    "hap_all_gather_v": (c_int, [_P, _P, _P, _I64P, c_int, c_int, _P, _P]),
+    "hap_grouped_broadcast": (c_int, [_P, _P, _P, _I64P, c_int, _P]),
+    "hap_reduce_scatter_v": (c_int, [_P, _P, _P, _I64P, c_int, _P, _P]),
+    "hap_all_to_all_v": (c_int, [_P, _P, _I64P, _P, _I64P, c_int, _P]),
+}
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+class HapError(RuntimeError):
+    pass
+
+
+def declared_symbols(header: str = HEADER) -> list[str]:
+    """Function names declared in include/hap_b200.h."""
+    with open(header, encoding="utf-8") as fh:
+        text = fh.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hap_[a-z0-9_]+)\s*\(", text)))
+
+
+_LIB = None
+
+
+def lib():
+    """Load (once) and return the bound library; raises LibraryError."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise LibraryError(f"{LIB_PATH} is missing: run `python -m paper_2401_05965_b200.build` "
+                           "(the executor has no CPU fallback)")
+    handle = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        try:
+            fn = getattr(handle, name)
+        except AttributeError:
+            raise LibraryError(f"{LIB_PATH} does not export {name}") from None
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = handle
+    return handle
+
+
+def check(status: int, what: str = "") -> None:
+    if status != 0:
+        msg = lib().hap_last_error().decode(errors="replace")
+        raise HapError(f"{what or 'hap call'} failed (status {status}): {msg}")
+
+
+def i64_array(values) -> ctypes.Array:
+    return (c_int64 * len(values))(*[int(v) for v in values])

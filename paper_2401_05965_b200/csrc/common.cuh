@@ -1,0 +1,80 @@
+// Shared helpers for the HAP B200 executor kernels (sm_100a only).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hap_b200.h"
+
+namespace hap {
+
+// Last error message (thread-local) surfaced through hap_last_error().
+void set_error(const std::string& msg);
+
+#define HAP_CUDA_TRY(expr)                                                       \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::hap::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+      return HAP_ERR_CUDA;                                                       \
+    }                                                                            \
+  } while (0)
+
+#define HAP_CHECK_ARG(cond, msg)                                                 \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      ::hap::set_error(msg);                                                     \
+      return HAP_ERR_ARG;                                                        \
+    }                                                                            \
+  } while (0)
+
+inline hap_status launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return HAP_ERR_CUDA;
+  }
+  return HAP_OK;
+}
+
+// SM count of the current device (cached per device).
+int sm_count();
+
+// Grid size for a capped, persistent launch: at most `sm_cap` CTAs (one per
+// SM when each CTA is sized to fill an SM), never more than `work_blocks`.
+inline int capped_grid(int64_t work_blocks, int sm_cap) {
+  int cap = sm_cap > 0 ? sm_cap : sm_count();
+  if (cap > sm_count()) cap = sm_count();
+  int64_t g = work_blocks < cap ? work_blocks : cap;
+  return g < 1 ? 1 : static_cast<int>(g);
+}
+
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+inline size_t dtype_size(hap_dtype t) { return t == HAP_BF16 ? 2 : 4; }
+
+}  // namespace hap
+
+// Dispatch a (input dtype, output dtype) pair to a templated body.
+#define HAP_DISPATCH_IO(IN, OUT, ...)                                            \
+  [&]() -> hap_status {                                                          \
+    if ((IN) == HAP_BF16 && (OUT) == HAP_BF16) {                                 \
+      using Tin = __nv_bfloat16; using Tout = __nv_bfloat16; return __VA_ARGS__(); \
+    } else if ((IN) == HAP_BF16 && (OUT) == HAP_F32) {                           \
+      using Tin = __nv_bfloat16; using Tout = float; return __VA_ARGS__();       \
+    } else if ((IN) == HAP_F32 && (OUT) == HAP_BF16) {                           \
+      using Tin = float; using Tout = __nv_bfloat16; return __VA_ARGS__();       \
+    } else {                                                                     \
+      using Tin = float; using Tout = float; return __VA_ARGS__();               \
+    }                                                                            \
+  }()

@@ -1,0 +1,364 @@
+// Elementwise instructions and their adjoints, plus the data-movement and
+// optimizer kernels of the executor.  All are HBM-bound: 16-byte vector
+// accesses when the pointers allow it, fp32 math, persistent grid capped at
+// `sm_cap` CTAs of 1024 threads (one CTA per SM), grid-stride loops.
+//
+//   elemwise_unary   reference interpreter.py:141-143
+//   elemwise_binary  reference interpreter.py:144-148
+//   identity         reference interpreter.py:151-152 (a copy / axpy)
+//   *_shard slicing  reference interpreter.py:81-91, 135-138 (copy_block)
+#include "common.cuh"
+
+namespace hap {
+namespace {
+
+constexpr int kBlock = 1024;
+
+__device__ __forceinline__ float unary_fwd(int tag, float x) {
+  switch (tag) {
+    case HAP_EXP: return __expf(x);
+    case HAP_NEG: return -x;
+    case HAP_RELU: return fmaxf(x, 0.f);
+    case HAP_SIGMOID: return 1.f / (1.f + __expf(-x));
+    default: return tanhf(x);
+  }
+}
+
+// d/dx f at x, given y = f(x).
+__device__ __forceinline__ float unary_deriv(int tag, float x, float y) {
+  switch (tag) {
+    case HAP_EXP: return y;
+    case HAP_NEG: return -1.f;
+    case HAP_RELU: return x > 0.f ? 1.f : 0.f;
+    case HAP_SIGMOID: return y * (1.f - y);
+    default: return 1.f - y * y;
+  }
+}
+
+// Vector of 8 elements loaded/stored as one 16-byte (bf16) or two 16-byte (fp32) accesses.
+template <typename T> struct Vec8;
+template <> struct Vec8<__nv_bfloat16> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
+    uint4 raw = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void store(__nv_bfloat16* p, const float (&v)[8]) {
+    uint4 raw;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = raw;
+  }
+};
+template <> struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[8]) {
+    float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+inline int grid_for(int64_t n, int sm_cap) {
+  return capped_grid((n + 8LL * kBlock - 1) / (8LL * kBlock), sm_cap);
+}
+
+// ---------------------------------------------------------------- unary
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kBlock) unary_kernel(int tag, const Tin* __restrict__ x,
+                                                       Tout* __restrict__ y, int64_t n, int vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vec) {
+    const int64_t nv = n / 8;
+    for (int64_t i = tid; i < nv; i += stride) {
+      float v[8];
+      Vec8<Tin>::load(x + 8 * i, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = unary_fwd(tag, v[j]);
+      Vec8<Tout>::store(y + 8 * i, v);
+    }
+    for (int64_t i = nv * 8 + tid; i < n; i += stride) y[i] = from_f32<Tout>(unary_fwd(tag, to_f32(x[i])));
+  } else {
+    for (int64_t i = tid; i < n; i += stride) y[i] = from_f32<Tout>(unary_fwd(tag, to_f32(x[i])));
+  }
+}
+
+template <typename Txy, typename Tdy, typename Tdx>
+__global__ void __launch_bounds__(kBlock)
+    unary_grad_kernel(int tag, const Txy* __restrict__ x, const Txy* __restrict__ y,
+                      const Tdy* __restrict__ dy, Tdx* dx, int64_t n, int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float xv = x ? to_f32(x[i]) : 0.f;
+    const float yv = y ? to_f32(y[i]) : 0.f;
+    float g = to_f32(dy[i]) * unary_deriv(tag, xv, yv);
+    if (accumulate) g += to_f32(dx[i]);
+    dx[i] = from_f32<Tdx>(g);
+  }
+}
+
+// ---------------------------------------------------------------- binary
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kBlock) binary_kernel(int tag, const Tin* __restrict__ a,
+                                                        const Tin* __restrict__ b,
+                                                        Tout* __restrict__ out, int64_t n, int vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t start = 0;
+  if (vec) {
+    const int64_t nv = n / 8;
+    for (int64_t i = tid; i < nv; i += stride) {
+      float va[8], vb[8];
+      Vec8<Tin>::load(a + 8 * i, va);
+      Vec8<Tin>::load(b + 8 * i, vb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) va[j] = tag == HAP_ADD ? va[j] + vb[j] : va[j] * vb[j];
+      Vec8<Tout>::store(out + 8 * i, va);
+    }
+    start = nv * 8;
+  }
+  for (int64_t i = start + tid; i < n; i += stride) {
+    const float u = to_f32(a[i]), v = to_f32(b[i]);
+    out[i] = from_f32<Tout>(tag == HAP_ADD ? u + v : u * v);
+  }
+}
+
+template <typename Tin, typename Tdy, typename Td>
+__global__ void __launch_bounds__(kBlock)
+    mul_grad_kernel(const Tin* __restrict__ a, const Tin* __restrict__ b, const Tdy* __restrict__ dy,
+                    Td* da, Td* db, int64_t n, int accumulate) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool same = da == db;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float g = to_f32(dy[i]);
+    const float ga = g * to_f32(b[i]), gb = g * to_f32(a[i]);
+    if (same && da) {
+      float v = ga + gb;
+      if (accumulate) v += to_f32(da[i]);
+      da[i] = from_f32<Td>(v);
+    } else {
+      if (da) da[i] = from_f32<Td>(accumulate ? to_f32(da[i]) + ga : ga);
+      if (db) db[i] = from_f32<Td>(accumulate ? to_f32(db[i]) + gb : gb);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- movement
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kBlock)
+    axpy_kernel(float alpha, const Tin* __restrict__ x, Tout* y, int64_t n, int accumulate, int vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t start = 0;
+  if (vec) {
+    const int64_t nv = n / 8;
+    for (int64_t i = tid; i < nv; i += stride) {
+      float v[8];
+      Vec8<Tin>::load(x + 8 * i, v);
+      if (accumulate) {
+        float o[8];
+        Vec8<Tout>::load(y + 8 * i, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = o[j] + alpha * v[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] *= alpha;
+      }
+      Vec8<Tout>::store(y + 8 * i, v);
+    }
+    start = nv * 8;
+  }
+  for (int64_t i = start + tid; i < n; i += stride) {
+    float v = alpha * to_f32(x[i]);
+    if (accumulate) v += to_f32(y[i]);
+    y[i] = from_f32<Tout>(v);
+  }
+}
+
+// dst[o, dst_off + i, k] (+)= src[o, src_off + i, k]
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kBlock)
+    copy_block_kernel(const Tin* __restrict__ src, int64_t src_extent, int64_t src_off, Tout* dst,
+                      int64_t dst_extent, int64_t dst_off, int64_t outer, int64_t count,
+                      int64_t inner, int accumulate) {
+  const int64_t per_outer = count * inner;
+  const int64_t total = outer * per_outer;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t o = e / per_outer;
+    const int64_t r = e - o * per_outer;
+    const int64_t s = (o * src_extent + src_off) * inner + r;
+    const int64_t d = (o * dst_extent + dst_off) * inner + r;
+    float v = to_f32(src[s]);
+    if (accumulate) v += to_f32(dst[d]);
+    dst[d] = from_f32<Tout>(v);
+  }
+}
+
+template <typename T>
+__global__ void fill_kernel(T* y, float value, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = from_f32<T>(value);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+    sgd_kernel(float* __restrict__ master, const float* __restrict__ grad, T* __restrict__ w,
+               float lr, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = master[i] - lr * grad[i];
+    master[i] = v;
+    w[i] = from_f32<T>(v);
+  }
+}
+
+template <typename T>
+using cptr = const T*;
+
+}  // namespace
+}  // namespace hap
+
+using namespace hap;
+
+#define HAP_STREAM cudaStream_t stream = static_cast<cudaStream_t>(stream_)
+
+extern "C" hap_status hap_unary(int tag, const void* x, hap_dtype xd, void* y, hap_dtype yd,
+                                int64_t n, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  HAP_CHECK_ARG(tag >= HAP_EXP && tag <= HAP_TANH, "hap_unary: bad tag");
+  if (n <= 0) return HAP_OK;
+  const int vec = aligned16(x) && aligned16(y);
+  return HAP_DISPATCH_IO(xd, yd, [&] {
+    unary_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        tag, static_cast<const Tin*>(x), static_cast<Tout*>(y), n, vec);
+    return launch_status("unary_kernel");
+  });
+}
+
+extern "C" hap_status hap_unary_grad(int tag, const void* x, const void* y, hap_dtype xyd,
+                                     const void* dy, hap_dtype dyd, void* dx, hap_dtype dxd,
+                                     int64_t n, int accumulate, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  HAP_CHECK_ARG(tag >= HAP_EXP && tag <= HAP_TANH, "hap_unary_grad: bad tag");
+  if (n <= 0) return HAP_OK;
+  HAP_CHECK_ARG(tag == HAP_NEG || (tag == HAP_RELU ? x != nullptr : y != nullptr),
+                "hap_unary_grad: missing saved activation");
+  return HAP_DISPATCH_IO(xyd, dxd, [&] {
+    if (dyd == HAP_BF16)
+      unary_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+          tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
+          static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(dx), n, accumulate);
+    else
+      unary_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+          tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
+          static_cast<const float*>(dy), static_cast<Tout*>(dx), n, accumulate);
+    return launch_status("unary_grad_kernel");
+  });
+}
+
+extern "C" hap_status hap_binary(int tag, const void* a, const void* b, hap_dtype ind, void* out,
+                                 hap_dtype outd, int64_t n, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  HAP_CHECK_ARG(tag == HAP_ADD || tag == HAP_MUL, "hap_binary: bad tag");
+  if (n <= 0) return HAP_OK;
+  const int vec = aligned16(a) && aligned16(b) && aligned16(out);
+  return HAP_DISPATCH_IO(ind, outd, [&] {
+    binary_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        tag, static_cast<const Tin*>(a), static_cast<const Tin*>(b), static_cast<Tout*>(out), n, vec);
+    return launch_status("binary_kernel");
+  });
+}
+
+extern "C" hap_status hap_mul_grad(const void* a, const void* b, hap_dtype ind, const void* dy,
+                                   hap_dtype dyd, void* da, void* db, hap_dtype dd, int64_t n,
+                                   int accumulate, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  return HAP_DISPATCH_IO(ind, dd, [&] {
+    if (dyd == HAP_BF16)
+      mul_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+          static_cast<const Tin*>(a), static_cast<const Tin*>(b),
+          static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(da), static_cast<Tout*>(db), n,
+          accumulate);
+    else
+      mul_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+          static_cast<const Tin*>(a), static_cast<const Tin*>(b), static_cast<const float*>(dy),
+          static_cast<Tout*>(da), static_cast<Tout*>(db), n, accumulate);
+    return launch_status("mul_grad_kernel");
+  });
+}
+
+extern "C" hap_status hap_axpy(float alpha, const void* x, hap_dtype xd, void* y, hap_dtype yd,
+                               int64_t n, int accumulate, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  const int vec = aligned16(x) && aligned16(y);
+  return HAP_DISPATCH_IO(xd, yd, [&] {
+    axpy_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        alpha, static_cast<const Tin*>(x), static_cast<Tout*>(y), n, accumulate, vec);
+    return launch_status("axpy_kernel");
+  });
+}
+
+extern "C" hap_status hap_copy_block(const void* src, hap_dtype sd, int64_t src_extent,
+                                     int64_t src_off, void* dst, hap_dtype dd, int64_t dst_extent,
+                                     int64_t dst_off, int64_t outer, int64_t count, int64_t inner,
+                                     int accumulate, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  HAP_CHECK_ARG(src_off >= 0 && dst_off >= 0 && src_off + count <= src_extent &&
+                    dst_off + count <= dst_extent,
+                "hap_copy_block: block out of range");
+  const int64_t total = outer * count * inner;
+  if (total <= 0) return HAP_OK;
+  // Contiguous same-dtype blocks (the row shards of a leading axis) are one memcpy.
+  if (outer == 1 && sd == dd && !accumulate) {
+    const size_t es = dtype_size(sd);
+    HAP_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + dst_off * inner * es,
+                                 static_cast<const char*>(src) + src_off * inner * es,
+                                 count * inner * es, cudaMemcpyDeviceToDevice, stream));
+    return HAP_OK;
+  }
+  return HAP_DISPATCH_IO(sd, dd, [&] {
+    copy_block_kernel<Tin, Tout><<<grid_for(total, sm_cap), kBlock, 0, stream>>>(
+        static_cast<const Tin*>(src), src_extent, src_off, static_cast<Tout*>(dst), dst_extent,
+        dst_off, outer, count, inner, accumulate);
+    return launch_status("copy_block_kernel");
+  });
+}
+
+extern "C" hap_status hap_fill(void* y, hap_dtype yd, float value, int64_t n, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  const int grid = capped_grid((n + 1023) / 1024, 0);
+  if (yd == HAP_BF16)
+    fill_kernel<__nv_bfloat16><<<grid, 1024, 0, stream>>>(static_cast<__nv_bfloat16*>(y), value, n);
+  else
+    fill_kernel<float><<<grid, 1024, 0, stream>>>(static_cast<float*>(y), value, n);
+  return launch_status("fill_kernel");
+}
+
+extern "C" hap_status hap_sgd(float* master, const float* grad, void* w, hap_dtype wd, float lr,
+                              int64_t n, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  if (wd == HAP_BF16)
+    sgd_kernel<__nv_bfloat16><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        master, grad, static_cast<__nv_bfloat16*>(w), lr, n);
+  else
+    sgd_kernel<float><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(master, grad,
+                                                                  static_cast<float*>(w), lr, n);
+  return launch_status("sgd_kernel");
+}

@@ -1,0 +1,559 @@
+// Ratio-sharded GEMM for the `matmul` instruction and its adjoints.
+//
+// Forward   C = A . B        (reference interpreter.py:139-140, per device)
+// Adjoints dA = dC . B^T,  dB = A^T . dC   (executor backward pass)
+//
+// tcgen05 path (bf16 in, fp32 accumulate in TMEM, bf16/fp32 out):
+//   * persistent, warp-specialised CTA (256 threads, one CTA per SM):
+//       warp 0  TMA producer (one elected lane)
+//       warp 1  MMA issuer   (one elected lane, tcgen05.mma.cta_group::1)
+//       warp 2  TMEM allocator
+//       warps 4-7 epilogue   (tcgen05.ld -> registers -> global)
+//   * tile 128 x BN x 64, BN in {128, 256}; smem ring of 6 / 4 stages fed by
+//     TMA with 128B swizzle; double-buffered TMEM accumulator so the epilogue
+//     of tile i overlaps the MMAs of tile i+1;
+//   * every operand orientation the adjoints need is handled by the UMMA
+//     descriptor's major-ness (K-major or MN-major) — no transposes in HBM;
+//   * grid = min(tiles, sm_cap): the per-rank SM cap that emulates a slower
+//     device bounds the SMs the kernel can occupy.
+// SIMT path: fp32 inputs, or strides TMA cannot describe (row pitch not a
+// multiple of 16 bytes) — small corpus shapes and zero-size shards.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace hap {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int UMMA_K = 16;
+constexpr int kThreads = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kBarrierBytes = 256;
+  static constexpr int kSmem = kStages * kStageBytes + kBarrierBytes + 1024;
+};
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128B swizzle, sm_100 version field.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor: bf16 x bf16 -> fp32, M x N, operand major-ness.
+__host__ __device__ constexpr uint32_t idesc(int m, int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+template <typename OutT>
+__device__ __forceinline__ void store_row_chunk(OutT* dst, const uint32_t (&r)[32], int valid,
+                                                bool vec, int accumulate) {
+  if constexpr (std::is_same<OutT, float>::value) {
+    if (vec && valid == 32) {
+      float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 v = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                               __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        if (accumulate) {
+          float4 o = d4[i];
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        d4[i] = v;
+      }
+    } else {
+      for (int i = 0; i < valid; ++i) {
+        float v = __uint_as_float(r[i]);
+        dst[i] = accumulate ? dst[i] + v : v;
+      }
+    }
+  } else {
+    if (vec && valid == 32) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[8 * i + j]);
+        if (accumulate) {
+          uint4 o = d4[i];
+          const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 of = __bfloat1622float2(ob[j]);
+            f[2 * j] += of.x;
+            f[2 * j + 1] += of.y;
+          }
+        }
+        uint4 v;
+        __nv_bfloat162* vb = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vb[j] = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+        d4[i] = v;
+      }
+    } else {
+      for (int i = 0; i < valid; ++i) {
+        float v = __uint_as_float(r[i]);
+        if (accumulate) v += __bfloat162float(dst[i]);
+        dst[i] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+template <int BN, bool kAMN, bool kBMN, typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   OutT* __restrict__ C, int64_t ldc, int M, int N, int K, int accumulate,
+                   int vec_ok) {
+  using G = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::kStages * G::kStageBytes);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = smem_u32(bars + G::kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
+  const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < G::kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(G::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % m_tiles) * BM;
+        const int n0 = (t / m_tiles) * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_expect_tx(fb, G::kStageBytes);
+          const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
+          const uint32_t sb = sa + G::kABytes;
+          const int k0 = kb * BK;
+          if (kAMN) {
+            tma_load_2d(sa, &tmA, fb, m0, k0);
+            tma_load_2d(sa + BK * 128, &tmA, fb, m0 + 64, k0);
+          } else {
+            tma_load_2d(sa, &tmA, fb, k0, m0);
+          }
+          if (kBMN) {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * BK * 128, &tmB, fb, n0 + 64 * c, k0);
+          } else {
+            tma_load_2d(sb, &tmB, fb, k0, n0);
+          }
+          if (++stage == G::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t kIdesc = idesc(BM, BN, kAMN, kBMN);
+      // K-major: rows of 128B, 8-row atoms 1024B apart (SBO), LBO unused (16B).
+      // MN-major: K-rows of 128B, 8-row groups 1024B apart (SBO); successive
+      // 64-element MN chunks BK*128 bytes apart (LBO).
+      constexpr uint32_t kALbo = kAMN ? BK * 128 : 16;
+      constexpr uint32_t kBLbo = kBMN ? BK * 128 : 16;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
+          const uint32_t sb = sa + G::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint32_t aoff = kAMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
+            const uint32_t boff = kBMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
+            tc_mma(d_tmem, sdesc(sa + aoff, kALbo, 1024), sdesc(sb + boff, kBLbo, 1024), kIdesc,
+                   (kb | kk) != 0);
+          }
+          tc_commit(empty0 + 8 * stage);
+          if (++stage == G::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = (t % m_tiles) * BM;
+      const int n0 = (t / m_tiles) * BN;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const int row = m0 + quarter * 32 + lane;
+      OutT* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
+        const int col0 = n0 + c * 32;
+        const int valid = N - col0 < 32 ? N - col0 : 32;
+        if (row < M && valid > 0) store_row_chunk<OutT>(crow + col0, r, valid, vec_ok, accumulate);
+      }
+      tc_fence_before();
+      mbar_arrive(tempty0 + 8 * acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(G::kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows of
+// pitch `ld` elements, box {64, box_outer}, 128B swizzle, zero OOB fill.
+bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld,
+              int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool kAMN, bool kBMN, typename OutT>
+hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M,
+                  int N, int K, int accumulate, int vec_ok, int sm_cap, cudaStream_t stream) {
+  using G = Cfg<BN>;
+  auto kern = gemm_tc_kernel<BN, kAMN, kBMN, OutT>;
+  static bool configured = false;
+  if (!configured) {
+    HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    configured = true;
+  }
+  const int64_t tiles = static_cast<int64_t>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = capped_grid(tiles, sm_cap);
+  kern<<<grid, kThreads, G::kSmem, stream>>>(ma, mb, static_cast<OutT*>(C), ldc, M, N, K,
+                                              accumulate, vec_ok);
+  return launch_status("gemm_tc_kernel");
+}
+
+template <int BN, typename OutT>
+hap_status dispatch_major(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
+                          void* C, int64_t ldc, int M, int N, int K, int acc, int vec, int cap,
+                          cudaStream_t s) {
+  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
+  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
+  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
+  return launch<BN, true, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ SIMT path
+namespace simt {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const Tin* __restrict__ A, int64_t lda,
+                                                        int transA, const Tin* __restrict__ B,
+                                                        int64_t ldb, int transB,
+                                                        Tout* __restrict__ C, int64_t ldc,
+                                                        int64_t M, int64_t N, int64_t K,
+                                                        int accumulate) {
+  __shared__ float As[TK][TM + 1];
+  __shared__ float Bs[TK][TN + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t tiles_n = (N + TN - 1) / TN;
+  const int64_t tiles = ((M + TM - 1) / TM) * tiles_n;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t m0 = (t / tiles_n) * TM, n0 = (t % tiles_n) * TN;
+    float acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < K; k0 += TK) {
+      for (int i = threadIdx.x; i < TK * TM; i += 256) {
+        const int kk = transA ? i / TM : i % TK;
+        const int mm = transA ? i % TM : i / TK;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        float v = 0.f;
+        if (gm < M && gk < K) v = to_f32(transA ? A[gk * lda + gm] : A[gm * lda + gk]);
+        As[kk][mm] = v;
+      }
+      for (int i = threadIdx.x; i < TK * TN; i += 256) {
+        const int kk = transB ? i % TK : i / TN;
+        const int nn = transB ? i / TK : i % TN;
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        float v = 0.f;
+        if (gn < N && gk < K) v = to_f32(transB ? B[gn * ldb + gk] : B[gk * ldb + gn]);
+        Bs[kk][nn] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t gm = m0 + ty * 4 + i;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t gn = n0 + tx * 4 + j;
+        if (gn >= N) continue;
+        float v = acc[i][j];
+        if (accumulate) v += to_f32(C[gm * ldc + gn]);
+        C[gm * ldc + gn] = from_f32<Tout>(v);
+      }
+    }
+  }
+}
+
+}  // namespace simt
+
+namespace {
+
+bool tc_eligible(const void* A, int64_t lda, int transA, const void* B, int64_t ldb, int transB,
+                 int64_t M, int64_t N, int64_t K, hap_dtype in_dtype) {
+  if (in_dtype != HAP_BF16) return false;
+  if (M <= 0 || N <= 0 || K <= 0) return false;
+  if (M > (1LL << 31) - 1 || N > (1LL << 31) - 1 || K > (1LL << 31) - 1) return false;
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) return false;
+  if ((lda % 8) || (ldb % 8)) return false;
+  // TMA needs the contiguous extent to cover at least one 16-byte chunk.
+  const int64_t a_inner = transA ? M : K, b_inner = transB ? K : N;
+  if (a_inner < 8 || b_inner < 8) return false;
+  (void)transB;
+  return tc::encode_fn() != nullptr;
+}
+
+template <typename Tin, typename Tout>
+hap_status simt_launch(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
+                       int transB, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                       int accumulate, int sm_cap, cudaStream_t stream) {
+  const int64_t tiles = ((M + simt::TM - 1) / simt::TM) * ((N + simt::TN - 1) / simt::TN);
+  const int grid = capped_grid(tiles, sm_cap > 0 ? sm_cap * 4 : sm_count() * 4);
+  simt::gemm_simt_kernel<Tin, Tout><<<grid, 256, 0, stream>>>(
+      static_cast<const Tin*>(A), lda, transA, static_cast<const Tin*>(B), ldb, transB,
+      static_cast<Tout*>(C), ldc, M, N, K, accumulate);
+  return launch_status("gemm_simt_kernel");
+}
+
+}  // namespace
+}  // namespace hap
+
+using namespace hap;
+
+extern "C" int hap_matmul_engine(const void* A, int64_t lda, int transA, const void* B,
+                                 int64_t ldb, int transB, int64_t M, int64_t N, int64_t K,
+                                 hap_dtype in_dtype) {
+  return tc_eligible(A, lda, transA, B, ldb, transB, M, N, K, in_dtype) ? HAP_GEMM_TCGEN05
+                                                                         : HAP_GEMM_SIMT;
+}
+
+extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B,
+                                 int64_t ldb, int transB, void* C, int64_t ldc, int64_t M,
+                                 int64_t N, int64_t K, hap_dtype in_dtype, hap_dtype out_dtype,
+                                 int accumulate, int sm_cap, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  HAP_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "hap_matmul: negative extent");
+  if (M == 0 || N == 0) return HAP_OK;  // zero-size shard: nothing to compute
+  HAP_CHECK_ARG(C != nullptr, "hap_matmul: null output");
+  if (K == 0) {
+    if (accumulate) return HAP_OK;
+    // C = 0 for an empty contraction (a zero-extent shard on the K axis).
+    const size_t osz = dtype_size(out_dtype);
+    HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * osz, 0, N * osz, M, stream));
+    return HAP_OK;
+  }
+  HAP_CHECK_ARG(A != nullptr && B != nullptr, "hap_matmul: null operand");
+  if (tc_eligible(A, lda, transA, B, ldb, transB, M, N, K, in_dtype)) {
+    const int BN = N > 128 ? 256 : 128;
+    CUtensorMap ma, mb;
+    bool ok = transA ? tc::make_map(&ma, A, M, K, lda, tc::BK)
+                     : tc::make_map(&ma, A, K, M, lda, tc::BM);
+    ok = ok && (transB ? tc::make_map(&mb, B, K, N, ldb, BN) : tc::make_map(&mb, B, N, K, ldb, tc::BK));
+    HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout");
+    const bool amn = transA != 0, bmn = transB == 0;
+    const size_t osz = dtype_size(out_dtype);
+    const int vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * osz) % 16 == 0);
+    const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+    if (out_dtype == HAP_BF16) {
+      return BN == 256
+                 ? tc::dispatch_major<256, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                                                          accumulate, vec, sm_cap, stream)
+                 : tc::dispatch_major<128, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                                                          accumulate, vec, sm_cap, stream);
+    }
+    return BN == 256 ? tc::dispatch_major<256, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                                                      accumulate, vec, sm_cap, stream)
+                     : tc::dispatch_major<128, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                                                      accumulate, vec, sm_cap, stream);
+  }
+  return HAP_DISPATCH_IO(in_dtype, out_dtype, [&] {
+    return simt_launch<Tin, Tout>(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, accumulate,
+                                  sm_cap, stream);
+  });
+}

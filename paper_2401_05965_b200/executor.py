@@ -1,0 +1,933 @@
+"""B200 executor for HAP-synthesized distributed programs.
+
+Drop-in for the reference interpreter's run path (pkg/src/shardplan/
+interpreter.py: ``run_distributed`` :217, ``execute_instruction`` :118,
+``check_equivalence`` :264): it takes the same program, device count and
+shard table, but every instruction runs as hand-written sm_100a CUDA through
+the C ABI (include/hap_b200.h) — tcgen05 GEMMs, vectorised elementwise and
+reduction kernels, NCCL collectives over NVLink — and it also runs the
+training step the reference cannot: the adjoint program (backward), the
+parameter-gradient synchronisation (all-reduce or sufficient-factor
+broadcasting, chosen by the cost model) and an SGD update.
+
+Device groups:
+  * ``NcclGroup`` — one process per GPU, rank j executes device j of the
+    program; collectives are NCCL calls on the compute stream.
+  * ``LocalGroup`` — all m program devices on one GPU in lock step, the
+    reference interpreter's own execution model; collectives become local
+    copy / sum kernels.  Used for parity tests of m-device programs on a
+    single GPU.
+
+The compile step turns the program into a flat list of C-ABI launches with
+every pointer and size resolved, so a step is a loop of ctypes calls — or a
+single CUDA-graph replay.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BF16, F32, check
+from .program import (ALL_GATHER, ALL_REDUCE, IDENTITY, DistributedProgram, Instruction,
+                      form_of_dist_id)
+from .sharding import offsets
+
+SOURCE_KINDS = ("placeholder", "placeholder_shard", "parameter", "parameter_shard")
+_TORCH = {F32: torch.float32, BF16: torch.bfloat16}
+
+
+class ExecutionError(RuntimeError):
+    """A program that cannot execute (unsound plan, missing binding or shard
+    sizes) — same contract as the reference's interpreter.ExecutionError."""
+
+
+# ---------------------------------------------------------------------------- buffers
+
+@dataclass
+class Buf:
+    tensor: torch.Tensor
+    dtype: int
+    shape: tuple
+
+    @property
+    def ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+    @property
+    def numel(self) -> int:
+        return int(math.prod(self.shape))
+
+
+def _view(shape: tuple, axis: int) -> tuple[int, int, int]:
+    """(outer, extent, inner) of ``shape`` around ``axis``."""
+    return (int(math.prod(shape[:axis])), int(shape[axis]), int(math.prod(shape[axis + 1:])))
+
+
+# ---------------------------------------------------------------------------- groups
+
+class LocalGroup:
+    """All m program devices emulated on the current GPU (lock step)."""
+
+    def __init__(self, m: int):
+        self.m = m
+        self.rank = 0
+        self.local_ranks = list(range(m))
+        self.comm = None
+
+    def close(self):
+        pass
+
+
+class NcclGroup:
+    """One program device per process; collectives over NCCL (C ABI)."""
+
+    def __init__(self, rank: int, m: int, comm_handle):
+        self.m = m
+        self.rank = rank
+        self.local_ranks = [rank]
+        self.comm = comm_handle
+
+    @classmethod
+    def from_torch_distributed(cls) -> "NcclGroup":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(_lib.lib().hap_comm_unique_id(uid), "hap_comm_unique_id")
+        obj = [bytes(uid.raw) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        handle = ctypes.c_void_p()
+        check(_lib.lib().hap_comm_init(ctypes.byref(handle), obj[0], world, rank), "hap_comm_init")
+        return cls(rank, world, handle)
+
+    def close(self):
+        if self.comm is not None:
+            check(_lib.lib().hap_comm_destroy(self.comm), "hap_comm_destroy")
+            self.comm = None
+
+
+# ---------------------------------------------------------------------------- config
+
+@dataclass
+class ExecConfig:
+    dtype: str = "bf16"               # working precision of activations ("bf16" | "fp32")
+    sm_caps: list | None = None       # per program-device SM cap (heterogeneity emulation)
+    lr: float = 0.0                   # SGD learning rate of train_step
+    grad_sync: str = "auto"           # "auto" (cost model) | "all_reduce" | "sfb"
+    gather: str = "auto"              # all_gather impl: "auto" | "padded" | "p2p"
+    input_grads: bool = False         # also differentiate w.r.t. placeholders
+    cluster: object = None            # ClusterSpec for the cost-model choices
+    ratios: tuple | None = None       # ratio row the plan was made with (cost model)
+
+
+@dataclass
+class Op:
+    fn: object
+    args: tuple
+    what: str
+    kernel: bool = True               # launches one of our kernels (vs NCCL / memcpy)
+
+
+# ---------------------------------------------------------------------------- executor
+
+class Executor:
+    """Compiled executor of one distributed program on this process's devices."""
+
+    def __init__(self, program: DistributedProgram, m: int, shard_table: dict,
+                 source_shapes: dict, group=None, config: ExecConfig | None = None,
+                 device: torch.device | None = None):
+        self.lib = _lib.lib()
+        self.program = program
+        self.m = m
+        self.table = {(k[0], int(k[1])): list(v) for k, v in shard_table.items()}
+        self.source_shapes = {k: tuple(v) for k, v in source_shapes.items()}
+        self.group = group or LocalGroup(m)
+        if self.group.m != m:
+            raise ExecutionError(f"device group has {self.group.m} devices, program needs {m}")
+        self.cfg = config or ExecConfig()
+        self.wdt = BF16 if self.cfg.dtype == "bf16" else F32
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.Stream(self.device)
+        self.caps = list(self.cfg.sm_caps) if self.cfg.sm_caps else [0] * m
+        self.ops_fwd: list[Op] = []
+        self.ops_bwd: list[Op] = []
+        self._ops = self.ops_fwd
+        self.bufs: dict[tuple[str, int], Buf] = {}
+        self.grads: dict[tuple[str, int], Buf] = {}
+        self.masters: dict[tuple[str, int], Buf] = {}
+        self.shapes: dict[str, list[tuple]] = {}
+        self.dtypes: dict[str, int] = {}
+        self.sync_choice: dict[str, str] = {}
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.source_dids = {i.output for i in program.instrs if i.kind in SOURCE_KINDS}
+        self._check_program()
+        self._infer()
+        self._allocate()
+        self._compile_forward()
+        self._compile_backward()
+
+    # ------------------------------------------------------------------ analysis
+    def _sizes(self, ref: str, axis: int) -> list[int]:
+        try:
+            sizes = self.table[(ref, axis)]
+        except KeyError:
+            raise ExecutionError(f"shard table lacks sizes for tensor {ref!r} axis {axis}") from None
+        if len(sizes) != self.m:
+            raise ExecutionError(f"shard table entry for {ref!r} axis {axis} has {len(sizes)} "
+                                 f"entries for {self.m} devices")
+        return sizes
+
+    def _check_program(self):
+        if not self.program.instrs:
+            raise ExecutionError("cannot run an empty program")
+        seen = set()
+        for ins in self.program.instrs:
+            for d in ins.operands:
+                if d not in seen:
+                    raise ExecutionError(f"instruction {ins.canonical()} reads unrealized tensor {d!r}")
+            if ins.kind in SOURCE_KINDS and ins.ref not in self.source_shapes:
+                raise ExecutionError(f"no binding for source tensor {ins.ref!r}")
+            seen.add(ins.output)
+
+    def _infer(self):
+        """Per-device shapes and dtypes of every distributed tensor."""
+        m = self.m
+        for ins in self.program.instrs:
+            k = ins.kind
+            ops = [self.shapes[d] for d in ins.operands]
+            dts = [self.dtypes[d] for d in ins.operands]
+            if k in ("placeholder", "parameter"):
+                full = self.source_shapes[ins.ref]
+                out = [full] * m
+                dt = self.wdt
+            elif k in ("placeholder_shard", "parameter_shard"):
+                full = self.source_shapes[ins.ref]
+                if not 0 <= ins.axis < len(full):
+                    raise ExecutionError(f"shape mismatch executing {ins.canonical()}: axis {ins.axis}")
+                sizes = self._sizes(ins.ref, ins.axis)
+                if sum(sizes) != full[ins.axis]:
+                    raise ExecutionError(f"shard sizes {sizes} do not cover extent {full[ins.axis]}")
+                out = [tuple(s if a == ins.axis else e for a, e in enumerate(full)) for s in sizes]
+                dt = self.wdt
+            elif k == "matmul":
+                out = []
+                for a, b in zip(*ops):
+                    if len(a) != 2 or len(b) != 2 or a[1] != b[0]:
+                        raise ExecutionError(f"shape mismatch executing {ins.canonical()}: {a} x {b}")
+                    out.append((a[0], b[1]))
+                dt = self.wdt
+            elif k in ("elemwise_unary", "identity"):
+                out = list(ops[0])
+                dt = dts[0]
+            elif k == "elemwise_binary":
+                for a, b in zip(*ops):
+                    if a != b:
+                        raise ExecutionError(f"shape mismatch executing {ins.canonical()}: {a} vs {b}")
+                out = list(ops[0])
+                dt = F32 if F32 in dts else self.wdt
+            elif k == "reduce":
+                out = [tuple(e for a, e in enumerate(s) if a not in ins.dims) for s in ops[0]]
+                dt = F32
+            elif k == "all_reduce":
+                if len(set(ops[0])) != 1:
+                    raise ExecutionError(f"shape mismatch executing {ins.canonical()}")
+                out = list(ops[0])
+                dt = dts[0]
+            elif k in ("all_gather", "grouped_broadcast"):
+                s0 = ops[0][0]
+                ext = sum(s[ins.axis] for s in ops[0])
+                out = [tuple(ext if a == ins.axis else e for a, e in enumerate(s0))] * m
+                dt = dts[0]
+            elif k == "reduce_scatter":
+                sizes = self._sizes(ins.ref, ins.axis)
+                s0 = ops[0][0]
+                if sum(sizes) != s0[ins.axis]:
+                    raise ExecutionError(f"shard sizes {sizes} do not cover extent {s0[ins.axis]}")
+                out = [tuple(sz if a == ins.axis else e for a, e in enumerate(s0)) for sz in sizes]
+                dt = dts[0]
+            elif k == "all_to_all":
+                sizes = self._sizes(ins.ref, ins.axis2)
+                s0 = ops[0][0]
+                ext1 = sum(s[ins.axis] for s in ops[0])
+                if sum(sizes) != s0[ins.axis2]:
+                    raise ExecutionError(f"shard sizes {sizes} do not cover extent {s0[ins.axis2]}")
+                out = [tuple(ext1 if a == ins.axis else (sz if a == ins.axis2 else e)
+                             for a, e in enumerate(s0)) for sz in sizes]
+                dt = dts[0]
+            else:
+                raise ExecutionError(f"unsupported instruction kind {k!r}")
+            self.shapes[ins.output] = out
+            self.dtypes[ins.output] = dt
+        # Which tensors need gradients: anything downstream of a parameter
+        # (and of placeholders when input gradients are requested).
+        self.req: dict[str, bool] = {}
+        for ins in self.program.instrs:
+            if ins.kind in SOURCE_KINDS:
+                self.req[ins.output] = ins.kind.startswith("parameter") or self.cfg.input_grads
+            else:
+                self.req[ins.output] = any(self.req[d] for d in ins.operands)
+
+    def _new(self, shape, dtype) -> Buf:
+        t = torch.empty(max(1, int(math.prod(shape))), dtype=_TORCH[dtype], device=self.device)
+        return Buf(t, dtype, tuple(shape))
+
+    def _allocate(self):
+        for did, shapes in self.shapes.items():
+            for r in self.group.local_ranks:
+                self.bufs[(did, r)] = self._new(shapes[r], self.dtypes[did])
+        for ins in self.program.instrs:
+            if ins.kind.startswith("parameter"):
+                for r in self.group.local_ranks:
+                    self.masters[(ins.output, r)] = self._new(self.shapes[ins.output][r], F32)
+        self.loss_buf = {r: self._new((), F32) for r in self.group.local_ranks}
+
+    # ------------------------------------------------------------------ emission
+    def _emit(self, name: str, *args, kernel: bool = True, what: str = ""):
+        fn = getattr(self.lib, name)
+        self._ops.append(Op(fn, args, what or name, kernel))
+
+    def _sptr(self):
+        return self.stream.cuda_stream
+
+    def _copy(self, src: Buf, dst: Buf, cap: int, accumulate: int = 0, alpha: float = 1.0):
+        n = src.numel if src.shape else 1
+        if dst.numel != n and dst.shape:
+            raise ExecutionError(f"copy of {src.shape} into {dst.shape}")
+        self._emit("hap_axpy", alpha, src.ptr, src.dtype, dst.ptr, dst.dtype, n, accumulate, cap,
+                   self._sptr())
+
+    def _block(self, src: Buf, src_view, src_off, dst: Buf, dst_view, dst_off, count, cap,
+               accumulate=0):
+        so, se, si = src_view
+        do, de, di = dst_view
+        if so != do or si != di:
+            raise ExecutionError(f"block copy views disagree: {src_view} vs {dst_view}")
+        self._emit("hap_copy_block", src.ptr, src.dtype, se, src_off, dst.ptr, dst.dtype, de, dst_off,
+                   so, count, si, accumulate, cap, self._sptr())
+
+    def _as(self, buf: Buf, dtype: int, cap: int) -> Buf:
+        """Buffer holding ``buf`` in ``dtype`` (a conversion op when needed)."""
+        if buf.dtype == dtype:
+            return buf
+        out = self._new(buf.shape, dtype)
+        self._copy(buf, out, cap)
+        return out
+
+    def _gemm(self, a: Buf, trans_a: bool, b: Buf, trans_b: bool, c: Buf, cap: int, accumulate: int):
+        am, ak = (a.shape[1], a.shape[0]) if trans_a else a.shape
+        bk, bn = (b.shape[1], b.shape[0]) if trans_b else b.shape
+        if ak != bk or tuple(c.shape) != (am, bn):
+            raise ExecutionError(f"gemm shape mismatch {a.shape}{'T' if trans_a else ''} x "
+                                 f"{b.shape}{'T' if trans_b else ''} -> {c.shape}")
+        in_dt = BF16 if (a.dtype == BF16 and b.dtype == BF16) else F32
+        a = self._as(a, in_dt, cap)
+        b = self._as(b, in_dt, cap)
+        self._emit("hap_matmul", a.ptr, a.shape[1], int(trans_a), b.ptr, b.shape[1], int(trans_b),
+                   c.ptr, c.shape[1], am, bn, ak, in_dt, c.dtype, accumulate, cap, self._sptr())
+
+    # ------------------------------------------------------------------ collectives
+    # Every collective maps per-device source buffers to per-device outputs with
+    # the reference's semantics (interpreter.py:69-101) and an `accumulate`
+    # flag so adjoints can add into gradient buffers.
+
+    def _coll_all_reduce(self, src: dict, dst: dict, accumulate: int):
+        g = self.group
+        if isinstance(g, LocalGroup):
+            tmp = self._new(src[0].shape, src[0].dtype if src[0].dtype == F32 else F32)
+            for j in range(self.m):
+                self._copy(src[j], tmp, self.caps[j], accumulate=int(j > 0))
+            for j in range(self.m):
+                self._copy(tmp, dst[j], self.caps[j], accumulate=accumulate)
+            return
+        r = g.rank
+        s = src[r]
+        target = dst[r] if (not accumulate and dst[r].dtype == s.dtype) else self._new(s.shape, s.dtype)
+        self._emit("hap_all_reduce", g.comm, s.ptr, target.ptr, s.numel if s.shape else 1, s.dtype,
+                   self._sptr(), kernel=False)
+        if target is not dst[r]:
+            self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
+
+    def _coll_all_gather(self, src: dict, src_shapes: list, dst: dict, axis: int, accumulate: int,
+                         kind: str):
+        """Shards along ``axis`` (all devices' shapes ``src_shapes``) -> full
+        tensor on every device."""
+        g = self.group
+        sizes = [s[axis] for s in src_shapes]
+        offs = offsets(sizes)
+        full_shape = dst[g.local_ranks[0]].shape
+        if isinstance(g, LocalGroup):
+            for j in range(self.m):
+                for k in range(self.m):
+                    self._block(src[k], _view(src[k].shape, axis), 0, dst[j], _view(full_shape, axis),
+                                offs[k], sizes[k], self.caps[j], accumulate)
+            return
+        r = g.rank
+        outer, _, inner = _view(full_shape, axis)
+        counts = [sz * outer * inner for sz in sizes]
+        s = src[r]
+        direct = outer == 1 and not accumulate and dst[r].dtype == s.dtype
+        target = dst[r] if direct else self._new((sum(counts),), s.dtype)
+        carr = _lib.i64_array(counts)
+        self._keep(carr)
+        if kind == "grouped_broadcast":
+            self._emit("hap_grouped_broadcast", g.comm, s.ptr, target.ptr, carr, s.dtype,
+                       self._sptr(), kernel=False)
+        else:
+            padded = self.cfg.gather in ("auto", "padded")
+            scratch = self._new((self.m * max(counts),), s.dtype) if padded else None
+            self._emit("hap_all_gather_v", g.comm, s.ptr, target.ptr, carr, s.dtype, int(padded),
+                       scratch.ptr if scratch else None, self._sptr(), kernel=False)
+        if not direct:
+            # rank-ordered chunks [outer, size_k, inner] -> full [outer, E, inner]
+            coff = offsets(counts)
+            for k in range(self.m):
+                if sizes[k] == 0:
+                    continue
+                chunk = Buf(target.tensor[coff[k]:coff[k + 1]] if target.tensor.numel() > 1 else target.tensor,
+                            target.dtype, (outer, sizes[k], inner))
+                self._block(chunk, (outer, sizes[k], inner), 0, dst[r], (outer, full_shape[axis], inner),
+                            offs[k], sizes[k], self.caps[r], accumulate)
+
+    def _coll_reduce_scatter(self, src: dict, dst: dict, axis: int, sizes: list, accumulate: int):
+        """Partial full tensors -> summed shard ``rank`` along ``axis``."""
+        g = self.group
+        full_shape = src[g.local_ranks[0]].shape
+        offs = offsets(sizes)
+        outer, ext, inner = _view(full_shape, axis)
+        if isinstance(g, LocalGroup):
+            tmp = self._new(full_shape, F32)
+            for k in range(self.m):
+                self._copy(src[k], tmp, self.caps[k], accumulate=int(k > 0))
+            for j in range(self.m):
+                self._block(tmp, (outer, ext, inner), offs[j], dst[j], (outer, sizes[j], inner), 0,
+                            sizes[j], self.caps[j], accumulate)
+            return
+        r = g.rank
+        s = src[r]
+        counts = [sz * outer * inner for sz in sizes]
+        if outer == 1:
+            send = s
+        else:  # pack rank-ordered chunks
+            send = self._new((sum(counts),), s.dtype)
+            coff = offsets(counts)
+            for k in range(self.m):
+                if sizes[k]:
+                    chunk = Buf(send.tensor[coff[k]:coff[k + 1]], s.dtype, (outer, sizes[k], inner))
+                    self._block(s, (outer, ext, inner), offs[k], chunk, (outer, sizes[k], inner), 0,
+                                sizes[k], self.caps[r])
+        direct = not accumulate and dst[r].dtype == s.dtype
+        target = dst[r] if direct else self._new(dst[r].shape, s.dtype)
+        scratch = self._new((self.m * max(max(counts), 1),), s.dtype)
+        carr = _lib.i64_array(counts)
+        self._keep(carr)
+        self._emit("hap_reduce_scatter_v", g.comm, send.ptr, target.ptr, carr, s.dtype, scratch.ptr,
+                   self._sptr(), kernel=False)
+        if not direct:
+            self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
+
+    def _coll_all_to_all(self, src: dict, src_shapes: list, dst: dict, d1: int, d2: int, sizes2: list,
+                         accumulate: int):
+        """Shards along d1 (all devices' shapes ``src_shapes``) -> shards along d2."""
+        g = self.group
+        sizes1 = [s[d1] for s in src_shapes]
+        off1, off2 = offsets(sizes1), offsets(sizes2)
+        if isinstance(g, LocalGroup):
+            for j in range(self.m):
+                for k in range(self.m):
+                    # block of src_k (rows off1[k] of the full tensor along d1)
+                    # restricted to device j's range along d2.
+                    piece_shape = tuple(sizes2[j] if a == d2 else e for a, e in enumerate(src_shapes[k]))
+                    piece = self._new(piece_shape, src[k].dtype)
+                    self._block(src[k], _view(src_shapes[k], d2), off2[j], piece, _view(piece_shape, d2), 0,
+                                sizes2[j], self.caps[j])
+                    self._block(piece, _view(piece_shape, d1), 0, dst[j], _view(dst[j].shape, d1), off1[k],
+                                sizes1[k], self.caps[j], accumulate)
+            return
+        r = g.rank
+        s = src[r]
+        send_shapes = [tuple(sizes2[k] if a == d2 else e for a, e in enumerate(s.shape)) for k in range(self.m)]
+        send_counts = [int(math.prod(sh)) for sh in send_shapes]
+        send = self._new((max(1, sum(send_counts)),), s.dtype)
+        soff = offsets(send_counts)
+        for k in range(self.m):
+            if send_counts[k]:
+                chunk = Buf(send.tensor[soff[k]:soff[k + 1]], s.dtype, send_shapes[k])
+                self._block(s, _view(s.shape, d2), off2[k], chunk, _view(send_shapes[k], d2), 0, sizes2[k],
+                            self.caps[r])
+        recv_shapes = [tuple(sizes1[k] if a == d1 else e for a, e in enumerate(dst[r].shape)) for k in range(self.m)]
+        recv_counts = [int(math.prod(sh)) for sh in recv_shapes]
+        recv = self._new((max(1, sum(recv_counts)),), s.dtype)
+        sarr, rarr = _lib.i64_array(send_counts), _lib.i64_array(recv_counts)
+        self._keep(sarr)
+        self._keep(rarr)
+        self._emit("hap_all_to_all_v", g.comm, send.ptr, sarr, recv.ptr, rarr, s.dtype, self._sptr(),
+                   kernel=False)
+        roff = offsets(recv_counts)
+        for k in range(self.m):
+            if recv_counts[k]:
+                chunk = Buf(recv.tensor[roff[k]:roff[k + 1]], s.dtype, recv_shapes[k])
+                self._block(chunk, _view(recv_shapes[k], d1), 0, dst[r], _view(dst[r].shape, d1), off1[k],
+                            sizes1[k], self.caps[r], accumulate)
+
+    def _keep(self, obj):
+        self.__dict__.setdefault("_keepalive", []).append(obj)
+
+    # ------------------------------------------------------------------ forward
+    def _compile_forward(self):
+        self._ops = self.ops_fwd
+        for ins in self.program.instrs:
+            self._forward_instr(ins)
+        self._loss_closure()
+
+    def _forward_instr(self, ins: Instruction):
+        k = ins.kind
+        if k in SOURCE_KINDS:
+            return  # bound by load()/feed()
+        L = self.group.local_ranks
+        out = {r: self.bufs[(ins.output, r)] for r in L}
+        src = [{r: self.bufs[(d, r)] for r in L} for d in ins.operands]
+        if k == "matmul":
+            for r in L:
+                self._gemm(src[0][r], False, src[1][r], False, out[r], self.caps[r], 0)
+        elif k == "elemwise_unary":
+            for r in L:
+                self._emit("hap_unary", _lib.UNARY_TAGS[ins.tag], src[0][r].ptr, src[0][r].dtype,
+                           out[r].ptr, out[r].dtype, out[r].numel, self.caps[r], self._sptr())
+        elif k == "elemwise_binary":
+            for r in L:
+                a, b = src[0][r], src[1][r]
+                in_dt = BF16 if a.dtype == BF16 and b.dtype == BF16 else F32
+                a, b = self._as(a, in_dt, self.caps[r]), self._as(b, in_dt, self.caps[r])
+                self._emit("hap_binary", _lib.BINARY_TAGS[ins.tag], a.ptr, b.ptr, in_dt, out[r].ptr,
+                           out[r].dtype, out[r].numel, self.caps[r], self._sptr())
+        elif k == "identity":
+            for r in L:
+                self._copy(src[0][r], out[r], self.caps[r])
+        elif k == "reduce":
+            for r in L:
+                x = src[0][r]
+                self._reduce(x, ins.dims, out[r], self.caps[r], 0)
+        elif k == "all_reduce":
+            self._coll_all_reduce(src[0], out, 0)
+        elif k in ("all_gather", "grouped_broadcast"):
+            self._coll_all_gather(src[0], self.shapes[ins.operands[0]], out, ins.axis, 0, k)
+        elif k == "reduce_scatter":
+            self._coll_reduce_scatter(src[0], out, ins.axis, self._sizes(ins.ref, ins.axis), 0)
+        elif k == "all_to_all":
+            self._coll_all_to_all(src[0], self.shapes[ins.operands[0]], out, ins.axis, ins.axis2,
+                                  self._sizes(ins.ref, ins.axis2), 0)
+        else:
+            raise ExecutionError(f"unsupported instruction kind {k!r}")
+
+    def _reduce(self, x: Buf, dims, y: Buf, cap: int, accumulate: int):
+        mask = 0
+        for d in dims:
+            mask |= 1 << d
+        shape = _lib.i64_array(x.shape) if x.shape else _lib.i64_array([1])
+        self._keep(shape)
+        if y.dtype != F32:
+            raise ExecutionError("reduce outputs are fp32")
+        self._emit("hap_reduce", x.ptr, x.dtype, shape, len(x.shape), mask, y.ptr, y.dtype, accumulate,
+                   cap, self._sptr())
+
+    def _loss_closure(self):
+        """interpreter.py:193 — full form if realised, else all-reduce the partial."""
+        L = self.group.local_ranks
+        loss = self.program.loss
+        if f"{loss}@full" in self.shapes:
+            for r in L:
+                self._copy(self.bufs[(f"{loss}@full", r)], self.loss_buf[r], self.caps[r])
+        elif f"{loss}@partial" in self.shapes:
+            self._coll_all_reduce({r: self.bufs[(f"{loss}@partial", r)] for r in L}, self.loss_buf, 0)
+        else:
+            raise ExecutionError(f"program realizes no property of the loss tensor {loss!r}")
+
+    # ------------------------------------------------------------------ backward
+    def _grad(self, did: str, r: int) -> Buf:
+        key = (did, r)
+        if key not in self.grads:
+            fwd = self.bufs[key]
+            dt = F32 if (fwd.dtype == F32 or did in self.source_dids) else fwd.dtype
+            self.grads[key] = self._new(fwd.shape, dt)
+        return self.grads[key]
+
+    def _compile_backward(self):
+        self._ops = self.ops_bwd
+        L = self.group.local_ranks
+        loss = self.program.loss
+        written: set[str] = set()   # grads that already hold a contribution
+
+        def contrib(did: str) -> int:
+            """accumulate flag for the next contribution to grad(did)."""
+            acc = int(did in written)
+            written.add(did)
+            return acc
+
+        if f"{loss}@full" in self.shapes:
+            seed_did, seed_val = f"{loss}@full", 1.0 / self.m
+        else:
+            seed_did, seed_val = f"{loss}@partial", 1.0
+        if not self.req.get(seed_did, False):
+            self._finish_update(written)
+            return
+        for r in L:
+            gb = self._grad(seed_did, r)
+            self._emit("hap_fill", gb.ptr, gb.dtype, seed_val, max(1, gb.numel), self._sptr())
+        written.add(seed_did)
+
+        self._plan_sfb()
+        for ins in reversed(self.program.instrs):
+            if ins.output not in written or ins.kind in SOURCE_KINDS:
+                continue
+            need = [self.req[d] for d in ins.operands]
+            if not any(need):
+                continue
+            self._adjoint(ins, need, contrib)
+        self._finish_update(written)
+
+    def _adjoint(self, ins: Instruction, need: list, contrib):
+        L = self.group.local_ranks
+        k = ins.kind
+        dy = {r: self.grads[(ins.output, r)] for r in L}
+        x = [{r: self.bufs[(d, r)] for r in L} for d in ins.operands]
+        ops = ins.operands
+        if k == "matmul":
+            if need[0]:
+                acc = contrib(ops[0])
+                for r in L:     # dA = dC . B^T
+                    self._gemm(dy[r], False, x[1][r], True, self._grad(ops[0], r), self.caps[r], acc)
+            if need[1]:
+                if ops[1] in self.sfb:
+                    self._sfb_weight_grad(ins, contrib)
+                else:
+                    acc = contrib(ops[1])
+                    for r in L:     # dB = A^T . dC
+                        self._gemm(x[0][r], True, dy[r], False, self._grad(ops[1], r), self.caps[r], acc)
+        elif k == "elemwise_unary":
+            acc = contrib(ops[0])
+            tag = _lib.UNARY_TAGS[ins.tag]
+            for r in L:
+                xb, yb = x[0][r], self.bufs[(ins.output, r)]
+                if xb.dtype != yb.dtype:
+                    xb = self._as(xb, yb.dtype, self.caps[r])
+                g = self._grad(ops[0], r)
+                self._emit("hap_unary_grad", tag, xb.ptr, yb.ptr, yb.dtype, dy[r].ptr, dy[r].dtype,
+                           g.ptr, g.dtype, g.numel, acc, self.caps[r], self._sptr())
+        elif k == "identity":
+            acc = contrib(ops[0])
+            for r in L:
+                self._copy(dy[r], self._grad(ops[0], r), self.caps[r], accumulate=acc)
+        elif k == "elemwise_binary":
+            if ins.tag == "add":
+                for i in (0, 1):
+                    if need[i]:
+                        acc = contrib(ops[i])
+                        for r in L:
+                            self._copy(dy[r], self._grad(ops[i], r), self.caps[r], accumulate=acc)
+            else:
+                same = ops[0] == ops[1]
+                if same:
+                    acc = contrib(ops[0])
+                    for r in L:
+                        a = x[0][r]
+                        g = self._grad(ops[0], r)
+                        self._emit("hap_mul_grad", a.ptr, a.ptr, a.dtype, dy[r].ptr, dy[r].dtype, g.ptr,
+                                   g.ptr, g.dtype, g.numel, acc, self.caps[r], self._sptr())
+                else:
+                    for i in (0, 1):
+                        if not need[i]:
+                            continue
+                        acc = contrib(ops[i])
+                        for r in L:
+                            other = x[1 - i][r]
+                            g = self._grad(ops[i], r)
+                            # d(a*b)/da = b : mul_grad with only the `da` output
+                            self._emit("hap_mul_grad", other.ptr, other.ptr, other.dtype, dy[r].ptr,
+                                       dy[r].dtype, g.ptr, None, g.dtype, g.numel, acc, self.caps[r],
+                                       self._sptr())
+        elif k == "reduce":
+            acc = contrib(ops[0])
+            mask = 0
+            for d in ins.dims:
+                mask |= 1 << d
+            for r in L:
+                xs = x[0][r].shape
+                shape = _lib.i64_array(xs) if xs else _lib.i64_array([1])
+                self._keep(shape)
+                g = self._grad(ops[0], r)
+                self._emit("hap_unreduce", dy[r].ptr, dy[r].dtype, shape, len(xs), mask, g.ptr, g.dtype,
+                           acc, self.caps[r], self._sptr())
+        elif k == "all_reduce":          # AR -> Id : adjoint is all-reduce
+            acc = contrib(ops[0])
+            self._coll_all_reduce(dy, {r: self._grad(ops[0], r) for r in L}, acc)
+        elif k in ("all_gather", "grouped_broadcast"):   # AG(d) -> Id : reduce-scatter
+            acc = contrib(ops[0])
+            self._coll_reduce_scatter(dy, {r: self._grad(ops[0], r) for r in L}, ins.axis,
+                                      self._sizes(ins.ref, ins.axis), acc)
+        elif k == "reduce_scatter":      # AR -> AG(d) : all-gather
+            acc = contrib(ops[0])
+            for r in L:
+                self._grad(ops[0], r)
+            self._coll_all_gather(dy, self.shapes[ins.output], {r: self.grads[(ops[0], r)] for r in L},
+                                  ins.axis, acc, "all_gather")
+        elif k == "all_to_all":          # AG(d1) -> AG(d2) : all-to-all back
+            acc = contrib(ops[0])
+            for r in L:
+                self._grad(ops[0], r)
+            self._coll_all_to_all(dy, self.shapes[ins.output], {r: self.grads[(ops[0], r)] for r in L},
+                                  ins.axis2, ins.axis, self._sizes(ins.ref, ins.axis), acc)
+        else:
+            raise ExecutionError(f"unsupported instruction kind {k!r}")
+
+    # ------------------------------------------------------------------ gradient sync
+    def _plan_sfb(self):
+        """Pick sufficient-factor broadcasting for replicated parameters whose
+        every use is a row-sharded matmul (x@shard0 . w@full -> y@shard0):
+        gather the factors x and dy and rebuild dW = x^T dy on every device,
+        instead of all-reducing the partial dW — whichever the cost model
+        prices lower (HAP's SFB rule; cost_model.comm_time)."""
+        self.sfb: dict[str, list[Instruction]] = {}
+        self.sfb_done: set[str] = set()
+        if self.m == 1 or self.cfg.grad_sync == "all_reduce":
+            return
+        uses: dict[str, list[Instruction]] = {}
+        for ins in self.program.instrs:
+            for d in ins.operands:
+                uses.setdefault(d, []).append(ins)
+        for ins in self.program.instrs:
+            if ins.kind != "parameter" or not self.req.get(ins.output):
+                continue
+            us = uses.get(ins.output, [])
+            ok = bool(us) and all(u.kind == "matmul" and u.operands[1] == ins.output and u.operands[0] != ins.output
+                                  and form_of_dist_id(u.operands[0]).kind == ALL_GATHER
+                                  and form_of_dist_id(u.operands[0]).axis == 0
+                                  and form_of_dist_id(u.output).kind == ALL_GATHER for u in us)
+            if not ok:
+                continue
+            choice = self.cfg.grad_sync if self.cfg.grad_sync != "auto" else self._price_sync(ins, us)
+            self.sync_choice[ins.ref] = choice
+            if choice == "sfb":
+                self.sfb[ins.output] = us
+
+    def _price_sync(self, pins: Instruction, uses: list) -> str:
+        from .cost_model import ClusterSpec, comm_time
+
+        spec = self.cfg.cluster
+        if spec is None:
+            return "all_reduce"
+        if not isinstance(spec, ClusterSpec):
+            spec = ClusterSpec.from_dict(spec)
+        row = self.cfg.ratios or tuple(d.flops_per_second / spec.total_rate for d in spec.devices)
+        rates = [d.flops_per_second for d in spec.devices]
+        kdim, ndim = self.source_shapes[pins.ref]
+        ar = Instruction("all_reduce", pins.ref, elements=kdim * ndim)
+        t_ar = comm_time(ar, row, spec)
+        t_sfb = 0.0
+        for u in uses:
+            rows = sum(s[0] for s in self.shapes[u.operands[0]])
+            flops = 2 * rows * kdim * ndim
+            gx = Instruction("all_gather", u.operands[0].split("@")[0], elements=rows * kdim)
+            gy = Instruction("all_gather", u.ref, elements=rows * ndim)
+            t_sfb += comm_time(gx, row, spec) + comm_time(gy, row, spec)
+            # SFB replicates the weight-gradient GEMM at full batch on every device;
+            # all-reduce keeps it sharded.
+            t_sfb += max(flops / rt for rt in rates)
+            t_ar += max(flops * b / rt for b, rt in zip(row, rates))
+        return "sfb" if t_sfb < t_ar else "all_reduce"
+
+    def _sfb_weight_grad(self, ins: Instruction, contrib):
+        """dW = gather(x)^T . gather(dy), replicated (Id form) on every device."""
+        L = self.group.local_ranks
+        w = ins.operands[1]
+        xdid, ydid = ins.operands[0], ins.output
+        xfull = {r: self._new((sum(s[0] for s in self.shapes[xdid]),) + self.shapes[xdid][0][1:],
+                              self.bufs[(xdid, r)].dtype) for r in L}
+        yfull = {r: self._new((sum(s[0] for s in self.shapes[ydid]),) + self.shapes[ydid][0][1:],
+                              self.grads[(ydid, r)].dtype) for r in L}
+        self._coll_all_gather({r: self.bufs[(xdid, r)] for r in L}, self.shapes[xdid], xfull, 0, 0,
+                              "all_gather")
+        self._coll_all_gather({r: self.grads[(ydid, r)] for r in L}, self.shapes[ydid], yfull, 0, 0,
+                              "all_gather")
+        acc = contrib(w)
+        self.sfb_done.add(w)
+        for r in L:
+            self._gemm(xfull[r], True, yfull[r], False, self._grad(w, r), self.caps[r], acc)
+
+    def _finish_update(self, written: set):
+        """Turn per-device parameter gradients into true gradients and apply SGD.
+
+        Replicated (@full) parameter gradients are partial sums: all-reduced,
+        unless SFB already produced them replicated.  Sharded gradients are
+        already the device's slice of the true gradient."""
+        L = self.group.local_ranks
+        sfb_done = self.sfb_done
+        self.param_grads: dict[tuple[str, int], Buf] = {}
+        forms: dict[str, list[Instruction]] = {}
+        for ins in self.program.instrs:
+            if ins.kind.startswith("parameter") or (self.cfg.input_grads and ins.kind.startswith("placeholder")):
+                forms.setdefault(ins.ref, []).append(ins)
+        for ref, fs in forms.items():
+            live = [f for f in fs if f.output in written]
+            if not live:
+                continue
+            if len(fs) == 1:
+                f = fs[0]
+                g = {r: self.grads[(f.output, r)] for r in L}
+                if f.kind in ("parameter", "placeholder") and f.output not in sfb_done and self.m > 1:
+                    self._coll_all_reduce(g, g, 0)
+                for r in L:
+                    self.param_grads[(f.output, r)] = g[r]
+            else:
+                # A parameter realised in several forms: assemble the full
+                # gradient (partial form), all-reduce it, hand each form its part.
+                full_shape = self.source_shapes[ref]
+                fullg = {r: self._new(full_shape, F32) for r in L}
+                first = True
+                for f in live:
+                    for r in L:
+                        g = self.grads[(f.output, r)]
+                        if f.kind.endswith("_shard"):
+                            sizes = self._sizes(ref, f.axis)
+                            o = offsets(sizes)[r]
+                            if first:
+                                self._emit("hap_fill", fullg[r].ptr, F32, 0.0, fullg[r].numel, self._sptr())
+                            self._block(g, _view(g.shape, f.axis), 0, fullg[r], _view(full_shape, f.axis), o,
+                                        g.shape[f.axis], self.caps[r], 1)
+                        else:
+                            scale = 1.0 / self.m if f.output in sfb_done else 1.0
+                            self._copy(g, fullg[r], self.caps[r], accumulate=int(not first), alpha=scale)
+                    first = False
+                if self.m > 1:
+                    self._coll_all_reduce(fullg, fullg, 0)
+                for f in fs:
+                    for r in L:
+                        if f.kind.endswith("_shard"):
+                            sizes = self._sizes(ref, f.axis)
+                            part = self._new(self.shapes[f.output][r], F32)
+                            self._block(fullg[r], _view(full_shape, f.axis), offsets(sizes)[r], part,
+                                        _view(part.shape, f.axis), 0, sizes[r], self.caps[r])
+                            self.param_grads[(f.output, r)] = part
+                        else:
+                            self.param_grads[(f.output, r)] = fullg[r]
+        self._ops = self.ops_upd = []
+        if self.cfg.lr:
+            for (did, r), g in self.param_grads.items():
+                if (did, r) not in self.masters:
+                    continue
+                mst, wb = self.masters[(did, r)], self.bufs[(did, r)]
+                self._emit("hap_sgd", mst.ptr, g.ptr, wb.ptr, wb.dtype, float(self.cfg.lr), mst.numel,
+                           self.caps[r], self._sptr())
+
+    # ------------------------------------------------------------------ binding
+    def load(self, inputs: dict):
+        """Bind every source (interpreter.py:132-138): float64 host arrays ->
+        device working copies (+ fp32 masters for parameters), sliced per the
+        shard table."""
+        self.stream.synchronize()
+        for ins in self.program.instrs:
+            if ins.kind not in SOURCE_KINDS:
+                continue
+            try:
+                value = np.asarray(inputs[ins.ref], dtype=np.float64)
+            except KeyError:
+                raise ExecutionError(f"no binding for source tensor {ins.ref!r}") from None
+            if tuple(value.shape) != self.source_shapes[ins.ref]:
+                raise ExecutionError(f"binding for {ins.ref!r} has shape {value.shape}, "
+                                     f"want {self.source_shapes[ins.ref]}")
+            full = torch.from_numpy(np.ascontiguousarray(value, dtype=np.float32))
+            for r in self.group.local_ranks:
+                if ins.kind.endswith("_shard"):
+                    sizes = self._sizes(ins.ref, ins.axis)
+                    o = offsets(sizes)
+                    part = full.narrow(ins.axis, o[r], sizes[r]).contiguous()
+                else:
+                    part = full
+                buf = self.bufs[(ins.output, r)]
+                buf.tensor[:part.numel()].copy_(part.reshape(-1).to(self.device), non_blocking=False)
+                if (ins.output, r) in self.masters:
+                    self.masters[(ins.output, r)].tensor[:part.numel()].copy_(part.reshape(-1).to(self.device))
+
+    def source_buffers(self, ref: str) -> dict[int, tuple[Instruction, Buf]]:
+        out = {}
+        for ins in self.program.instrs:
+            if ins.kind in SOURCE_KINDS and ins.ref == ref:
+                for r in self.group.local_ranks:
+                    out.setdefault(r, []).append((ins, self.bufs[(ins.output, r)]))
+        return out
+
+    # ------------------------------------------------------------------ running
+    def _run(self, ops: list[Op]):
+        for op in ops:
+            st = op.fn(*op.args)
+            if st:
+                check(st, op.what)
+
+    def forward(self):
+        with torch.cuda.stream(self.stream):
+            self._run(self.ops_fwd)
+
+    def backward(self):
+        with torch.cuda.stream(self.stream):
+            self._run(self.ops_bwd)
+            self._run(self.ops_upd)
+
+    def step(self):
+        """One training iteration: forward, backward, gradient sync, update."""
+        if self.graph is not None:
+            self.graph.replay()
+            return
+        with torch.cuda.stream(self.stream):
+            self._run(self.ops_fwd)
+            self._run(self.ops_bwd)
+            self._run(self.ops_upd)
+
+    def capture(self):
+        """Record forward+backward+update into one CUDA graph (all ops were
+        compiled against self.stream, the capture stream)."""
+        self.step()  # warm-up outside capture (kernel attributes, NCCL setup)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self._run(self.ops_fwd)
+            self._run(self.ops_bwd)
+            self._run(self.ops_upd)
+        self.graph = g
+        return g
+
+    def kernel_launches(self, phase: str = "step") -> int:
+        ops = {"forward": self.ops_fwd, "backward": self.ops_bwd + self.ops_upd,
+               "step": self.ops_fwd + self.ops_bwd + self.ops_upd}[phase]
+        return sum(1 for op in ops if op.kernel)
+
+    def losses(self) -> list[float]:
+        """Per-device loss values of the last forward (host sync)."""
+        self.stream.synchronize()
+        vals = {r: float(self.loss_buf[r].tensor[0].item()) for r in self.group.local_ranks}
+        if isinstance(self.group, NcclGroup):
+            import torch.distributed as dist
+
+            out = [None] * self.m
+            dist.all_gather_object(out, vals[self.group.rank])
+            return [float(v) for v in out]
+        return [vals[r] for r in range(self.m)]
+
+    def tensor(self, did: str, r: int) -> torch.Tensor:
+        b = self.bufs[(did, r)]
+        return b.tensor[:b.numel].view(b.shape) if b.shape else b.tensor[:1].view(())
+
+    def gradient(self, ref: str) -> dict[int, tuple[Instruction, torch.Tensor]]:
+        """Synchronised gradient of source ``ref`` per local device/form."""
+        out = {}
+        for (did, r), g in self.param_grads.items():
+            if did.rpartition("@")[0] == ref:
+                out.setdefault(r, []).append((did, g.tensor[:g.numel].view(g.shape)))
+        return out
+
+    def close(self):
+        self.group.close()

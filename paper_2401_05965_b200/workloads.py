@@ -1,0 +1,136 @@
+"""Graph builders for the benchmark configurations (BASELINE.json ``configs``).
+
+Every graph is written in the reference IR (graph_ir.py), because the planner
+must emit exactly the reference's program for it.  That IR has rank-2 MatMul,
+five unary tags, add/mul and Reduce — no transpose, softmax, layer norm or
+convolution — so the transformer workloads are *GEMM skeletons*: every dense
+projection of the real model at its real shape, with the token-mixing
+attention (2.7% of BERT-base flops at seq 128) replaced by an elementwise
+gate ``sigmoid(q*k)*v`` and GELU by SiLU ``f*sigmoid(f)``.  DESIGN.md lists
+what each proxy keeps and drops.
+"""
+from __future__ import annotations
+
+from .graph_ir import Graph, graph_from_dict
+
+
+def _n(nid: str, op: str, shape, inputs=(), **attrs) -> dict:
+    doc = {"id": nid, "op": op, "shape": list(shape)}
+    if inputs:
+        doc["inputs"] = list(inputs)
+    if attrs:
+        doc["attrs"] = attrs
+    return doc
+
+
+def mlp_doc(batch: int = 64, hidden: int = 1024, layers: int = 2) -> dict:
+    """configs[0]: ``layers`` dense layers with ReLU between, summed to a loss."""
+    nodes = [_n("x", "Placeholder", [batch, hidden])]
+    prev = "x"
+    for i in range(1, layers + 1):
+        nodes.append(_n(f"w{i}", "Parameter", [hidden, hidden]))
+        nodes.append(_n(f"h{i}", "MatMul", [batch, hidden], [prev, f"w{i}"]))
+        prev = f"h{i}"
+        if i < layers:
+            nodes.append(_n(f"a{i}", "ElemwiseUnary", [batch, hidden], [prev], tag="relu"))
+            prev = f"a{i}"
+    nodes.append(_n("loss", "Reduce", [], [prev], dims="all"))
+    return {"nodes": nodes, "loss": "loss"}
+
+
+def bert_doc(layers: int = 12, batch: int = 64, seq: int = 128, hidden: int = 768,
+             ffn: int = 3072) -> dict:
+    """configs[2]: BERT-base GEMM skeleton over ``batch*seq`` token rows.
+
+    Per layer: Q/K/V projections, gate ``sigmoid(q*k)*v``, output projection
+    with residual, FFN up-projection, SiLU, FFN down-projection with residual.
+    """
+    tokens = batch * seq
+    nodes = [_n("x0", "Placeholder", [tokens, hidden])]
+    prev = "x0"
+    for layer in range(layers):
+        p = f"l{layer}_"
+        for w in ("q", "k", "v"):
+            nodes.append(_n(p + "W" + w, "Parameter", [hidden, hidden]))
+            nodes.append(_n(p + w, "MatMul", [tokens, hidden], [prev, p + "W" + w]))
+        nodes.append(_n(p + "qk", "ElemwiseBinary", [tokens, hidden], [p + "q", p + "k"], tag="mul"))
+        nodes.append(_n(p + "att", "ElemwiseUnary", [tokens, hidden], [p + "qk"], tag="sigmoid"))
+        nodes.append(_n(p + "ctx", "ElemwiseBinary", [tokens, hidden], [p + "att", p + "v"], tag="mul"))
+        nodes.append(_n(p + "Wo", "Parameter", [hidden, hidden]))
+        nodes.append(_n(p + "o", "MatMul", [tokens, hidden], [p + "ctx", p + "Wo"]))
+        nodes.append(_n(p + "x1", "ElemwiseBinary", [tokens, hidden], [prev, p + "o"], tag="add"))
+        nodes.append(_n(p + "W1", "Parameter", [hidden, ffn]))
+        nodes.append(_n(p + "f1", "MatMul", [tokens, ffn], [p + "x1", p + "W1"]))
+        nodes.append(_n(p + "s1", "ElemwiseUnary", [tokens, ffn], [p + "f1"], tag="sigmoid"))
+        nodes.append(_n(p + "g", "ElemwiseBinary", [tokens, ffn], [p + "f1", p + "s1"], tag="mul"))
+        nodes.append(_n(p + "W2", "Parameter", [ffn, hidden]))
+        nodes.append(_n(p + "f2", "MatMul", [tokens, hidden], [p + "g", p + "W2"]))
+        nodes.append(_n(p + "x2", "ElemwiseBinary", [tokens, hidden], [p + "x1", p + "f2"], tag="add"))
+        prev = p + "x2"
+    nodes.append(_n("loss", "Reduce", [], [prev], dims="all"))
+    return {"nodes": nodes, "loss": "loss"}
+
+
+def mlp(batch: int = 64, hidden: int = 1024, layers: int = 2) -> Graph:
+    return graph_from_dict(mlp_doc(batch, hidden, layers))
+
+
+def bert(layers: int = 12, batch: int = 64, seq: int = 128, hidden: int = 768,
+         ffn: int = 3072) -> Graph:
+    return graph_from_dict(bert_doc(layers, batch, seq, hidden, ffn))
+
+
+# Heterogeneity emulation: per-rank SM caps on the homogeneous 8xB200 box.
+SM_COUNT = 148
+SM_CAP_PATTERN = (148, 104, 132, 88)
+
+
+def sm_caps(n_gpus: int) -> list[int]:
+    """Mixed SM caps for ``n_gpus`` ranks; one GPU runs uncapped."""
+    if n_gpus == 1:
+        return [SM_COUNT]
+    return [SM_CAP_PATTERN[j % len(SM_CAP_PATTERN)] for j in range(n_gpus)]
+
+
+# NVLink-5 collective model for the planner's cost model (latency, bytes/s),
+# bf16 elements.  Round-1 values are set from the profiling guide's measured
+# NVLink figures (770 GB/s peer copy, 725 GB/s 8-rank all-reduce bus
+# bandwidth) derated for small messages; DESIGN.md tracks the refit.
+NVLINK_MODEL = {
+    "all_gather": (8e-6, 600e9),
+    "all_reduce": (12e-6, 360e9),
+    "reduce_scatter": (8e-6, 600e9),
+    "all_to_all": (10e-6, 500e9),
+    "grouped_broadcast": (4e-6, 600e9),
+}
+BF16_TFLOPS_PER_SM = 1376.6e12 / SM_COUNT   # MEASURED_PEAKS.json sustained / 148
+
+
+def cluster_doc(caps: list[int], bytes_per_element: int = 2) -> dict:
+    """Cluster spec (reference ClusterSpec JSON) for SM-capped B200 ranks."""
+    return {
+        "devices": [{"flops": float(c) * BF16_TFLOPS_PER_SM} for c in caps],
+        "collectives": {k: {"latency_s": lat, "bw_Bps": bw} for k, (lat, bw) in NVLINK_MODEL.items()},
+        "bytes_per_element": bytes_per_element,
+    }
+
+
+def synthetic_inputs(g: Graph, seed: int, scaled: bool = True) -> dict:
+    """Seeded float64 bindings for every source tensor, in node order.
+
+    ``scaled=False`` reproduces the reference's ``random_inputs``
+    (interpreter.py:252): standard normal everywhere.  ``scaled=True`` divides
+    rank-2 parameters by sqrt(fan-in) so deep skeletons stay in range (the
+    reference interpreter is then run on exactly these arrays).
+    """
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    out = {}
+    for node in g.nodes:
+        if node.op in ("Placeholder", "Parameter"):
+            value = rng.standard_normal(node.shape)
+            if scaled and node.op == "Parameter" and len(node.shape) == 2:
+                value = value / np.sqrt(node.shape[0])
+            out[node.id] = value
+    return out

@@ -1,0 +1,131 @@
+"""Executor parity on the B200: the CUDA path (through the C ABI) against the
+reference interpreter's golden outputs and the CPU oracle, for every golden
+plan and every enumerated program with collectives, with all m program
+devices emulated on one GPU (LocalGroup).  Tolerances: rtol 2e-2 in bf16,
+1e-3 in fp32 (north_star), relative to max(|reference|, 1) per value and to
+the largest reference magnitude for gradient tensors."""
+import numpy as np
+import pytest
+import torch
+
+import goldens
+from oracle import interpreter_np as O
+from paper_2401_05965_b200.executor import ExecConfig, Executor, LocalGroup
+from paper_2401_05965_b200.program import DistributedProgram
+from paper_2401_05965_b200.sharding import table_from_plan
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+RTOL = {"bf16": 2e-2, "fp32": 1e-3}
+
+
+def _run(doc, g, inputs, dtype, lr=0.0):
+    prog = DistributedProgram.from_json(doc["program"])
+    m = int(doc["devices"])
+    shapes = {n.id: n.shape for n in g.nodes if n.op in ("Placeholder", "Parameter")}
+    ex = Executor(prog, m, table_from_plan(doc), shapes, group=LocalGroup(m),
+                  config=ExecConfig(dtype=dtype, lr=lr, input_grads=True))
+    ex.load(inputs)
+    ex.step()
+    torch.cuda.synchronize()
+    return ex
+
+
+def loss_scale(doc, inputs, want):
+    """Tolerance scale of a summed loss: max(|loss|, 1, ||summands||_2).
+
+    A loss that is the sum of N terms carrying independent relative rounding
+    errors eps has error ~ eps * ||terms||_2; when the terms cancel, |loss|
+    alone is far below that (the MLP sums 65536 terms of |.|-sum 3.7e4 to
+    42), so the 2-norm of the reduced tensor is the honest denominator."""
+    program, m, table = O.load_plan(doc)
+    env, _ = O.run_distributed(program, m, inputs, table)
+    norm = 0.0
+    for ins in program.instrs:
+        if ins.ref == program.loss and ins.kind == "reduce":
+            norm = max(norm, float(np.sqrt(sum(np.sum(np.square(v)) for v in env[ins.operands[0]]))))
+    return np.maximum(np.maximum(np.abs(want), 1.0), norm)
+
+
+def _check_losses(ex, want, dtype, scale):
+    got = np.array(ex.losses())
+    assert np.all(np.abs(got - want) <= RTOL[dtype] * scale), (got, want, scale)
+
+
+def _check_grads(ex, g, inputs, dtype):
+    want = O.grad_single(g, inputs)
+    for ref, value in want.items():
+        per = ex.gradient(ref)
+        assert per, f"no gradient for {ref}"
+        for r, forms in per.items():
+            for did, grad in forms:
+                grad = grad.float().cpu().numpy().astype(np.float64)
+                if "@shard" in did:
+                    axis = int(did.rsplit("shard", 1)[1])
+                    sizes = ex._sizes(ref, axis)
+                    off = int(np.sum(sizes[:r]))
+                    expect = np.take(value, np.arange(off, off + sizes[r]), axis=axis)
+                else:
+                    expect = value
+                scale = max(float(np.max(np.abs(value))), 1e-3)
+                err = float(np.max(np.abs(grad - expect))) / scale if grad.size else 0.0
+                assert err <= RTOL[dtype], f"{did} device {r}: rel err {err}"
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("gname,cname", goldens.value_cases())
+def test_planned_programs_match_reference(gname, cname, dtype):
+    g = goldens.graph(gname)
+    vals = goldens.values(gname, cname)
+    doc = goldens.plan(gname, cname)
+    seed = goldens.seeds(vals)[0]
+    inputs = goldens.inputs(g, vals, seed)
+    ex = _run(doc, g, inputs, dtype)
+    want = vals[f"seed{seed}:losses"]
+    _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
+    for did, insts in goldens.env(vals).items():
+        for r, want in enumerate(insts):
+            got = ex.tensor(did, r).float().cpu().numpy()
+            scale = max(float(np.max(np.abs(want))) if want.size else 1.0, 1.0)
+            assert got.shape == want.shape
+            assert (np.max(np.abs(got - want)) if want.size else 0.0) <= RTOL[dtype] * scale, did
+    _check_grads(ex, g, inputs, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("stem", goldens.program_cases())
+def test_programs_with_collectives_match_reference(stem, dtype):
+    doc, vals, gname = goldens.program_case(stem)
+    g = goldens.graph(gname)
+    inputs = {k.split(":", 2)[2]: vals[k] for k in vals.files if k.startswith("seed0:input:")}
+    ex = _run(doc, g, inputs, dtype)
+    want = vals["seed0:losses"]
+    _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
+    _check_grads(ex, g, inputs, dtype)
+
+
+def test_sgd_update_matches_oracle():
+    g = goldens.graph("chain4")
+    doc = goldens.plan("chain4", "hetero2")
+    vals = goldens.values("chain4", "hetero2")
+    inputs = goldens.inputs(g, vals, 0)
+    ex = _run(doc, g, inputs, "fp32", lr=0.01)
+    program, m, table = O.load_plan(doc)
+    shapes = {n.id: n.shape for n in g.nodes}
+    _, _, updated = O.train_step(program, m, inputs, table, shapes, lr=0.01)
+    for ref, want in updated.items():
+        for (did, r), master in ex.masters.items():
+            if did.rpartition("@")[0] != ref:
+                continue
+            got = master.tensor[:master.numel].view(master.shape).cpu().numpy()
+            if "@shard" in did:
+                axis = int(did.rsplit("shard", 1)[1])
+                sizes = ex._sizes(ref, axis)
+                off = int(np.sum(sizes[:r]))
+                want_r = np.take(want, np.arange(off, off + sizes[r]), axis=axis)
+            else:
+                want_r = want
+            assert np.max(np.abs(got - want_r)) <= 1e-4 * max(1.0, np.max(np.abs(want_r)))

@@ -1,0 +1,167 @@
+"""Kernel-level numerics on the B200, through the C ABI, against a plain
+PyTorch fp32 reference of the same op (inputs rounded to the kernel's input
+precision first).  Tolerances are written per test."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2401_05965_b200 import _lib
+from paper_2401_05965_b200._lib import BF16, F32, check
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU collection only
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+L = _lib.lib()
+DEV = torch.device("cuda")
+S = 0  # legacy default stream; tests synchronise explicitly
+
+
+def _dt(t):
+    return BF16 if t.dtype == torch.bfloat16 else F32
+
+
+def gemm(a, ta, b, tb, c, accumulate=0, sm_cap=0):
+    M, K = (a.shape[1], a.shape[0]) if ta else a.shape
+    N = b.shape[0] if tb else b.shape[1]
+    check(L.hap_matmul(a.data_ptr(), a.shape[1], ta, b.data_ptr(), b.shape[1], tb, c.data_ptr(), c.shape[1],
+                       M, N, K, _dt(a), _dt(c), accumulate, sm_cap, S), "hap_matmul")
+    torch.cuda.synchronize()
+
+
+def ref_mm(a, ta, b, tb):
+    a32, b32 = a.float(), b.float()
+    return (a32.t() if ta else a32) @ (b32.t() if tb else b32)
+
+
+def rel_err(got, want):
+    return float((got.float() - want).abs().max() / max(want.abs().max().item(), 1e-6))
+
+
+SHAPES = [(128, 128, 64), (256, 512, 320), (300, 200, 72), (1000, 520, 1000), (64, 1024, 1024),
+          (4096, 3072, 768), (8, 264, 40)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("out", [torch.bfloat16, torch.float32])
+def test_tcgen05_gemm_all_orientations(M, N, K, ta, tb, out):
+    torch.manual_seed(M * 7 + N * 3 + K + ta * 2 + tb)
+    a = torch.randn((K, M) if ta else (M, K), device=DEV).to(torch.bfloat16)
+    b = torch.randn((N, K) if tb else (K, N), device=DEV).to(torch.bfloat16)
+    # tcgen05 needs 16-byte row pitches (TMA); other shapes take the SIMT kernel.
+    tma_ok = a.shape[1] % 8 == 0 and b.shape[1] % 8 == 0
+    engine = L.hap_matmul_engine(a.data_ptr(), a.shape[1], ta, b.data_ptr(), b.shape[1], tb, M, N, K, BF16)
+    assert engine == (_lib.GEMM_TCGEN05 if tma_ok else _lib.GEMM_SIMT)
+    c = torch.empty((M, N), device=DEV, dtype=out)
+    gemm(a, ta, b, tb, c)
+    want = ref_mm(a, ta, b, tb)
+    # fp32 accumulate in TMEM: only summation order differs (fp32 out), plus
+    # one bf16 rounding of the result (bf16 out).
+    assert rel_err(c, want) < (1e-5 if out == torch.float32 else 8e-3)
+
+
+def test_gemm_accumulate_and_sm_cap():
+    torch.manual_seed(1)
+    a = torch.randn(512, 256, device=DEV).to(torch.bfloat16)
+    b = torch.randn(256, 384, device=DEV).to(torch.bfloat16)
+    c = torch.randn(512, 384, device=DEV)
+    base = c.clone()
+    gemm(a, 0, b, 0, c, accumulate=1, sm_cap=7)
+    assert rel_err(c, base + ref_mm(a, 0, b, 0)) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 2, 4), (6, 2, 4), (0, 4, 4), (5, 0, 3), (3, 3, 0), (33, 17, 9)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_simt_gemm_small_and_zero_shapes(M, N, K, dtype):
+    torch.manual_seed(2)
+    for ta, tb in [(0, 0), (1, 0), (0, 1)]:
+        a = torch.randn((K, M) if ta else (M, K), device=DEV).to(dtype)
+        b = torch.randn((N, K) if tb else (K, N), device=DEV).to(dtype)
+        c = torch.full((M, N), 7.0, device=DEV)
+        if M and N:
+            gemm(a, ta, b, tb, c)
+            want = ref_mm(a, ta, b, tb)
+            assert rel_err(c, want) < 1e-5 or want.abs().max() == 0
+
+
+@pytest.mark.parametrize("tag", ["exp", "neg", "relu", "sigmoid", "tanh"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_unary_and_adjoint(tag, dtype):
+    torch.manual_seed(3)
+    n = 100003
+    x = torch.randn(n, device=DEV).to(dtype)
+    y = torch.empty_like(x)
+    check(L.hap_unary(_lib.UNARY_TAGS[tag], x.data_ptr(), _dt(x), y.data_ptr(), _dt(y), n, 0, S))
+    xf = x.float()
+    fn = {"exp": torch.exp, "neg": torch.neg, "relu": torch.relu, "sigmoid": torch.sigmoid, "tanh": torch.tanh}[tag]
+    tol = 1e-5 if dtype == torch.float32 else 8e-3
+    torch.cuda.synchronize()
+    assert rel_err(y, fn(xf)) < tol
+    dy = torch.randn(n, device=DEV).to(dtype)
+    dx = torch.full((n,), 1.0, device=DEV)
+    check(L.hap_unary_grad(_lib.UNARY_TAGS[tag], x.data_ptr(), y.data_ptr(), _dt(x), dy.data_ptr(), _dt(dy),
+                           dx.data_ptr(), F32, n, 1, 0, S))
+    xr = xf.clone().requires_grad_(True)
+    fn(xr).backward(dy.float())
+    torch.cuda.synchronize()
+    assert rel_err(dx, 1.0 + xr.grad) < (1e-4 if dtype == torch.float32 else 2e-2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_binary_and_mul_adjoint(dtype):
+    torch.manual_seed(4)
+    n = 65537
+    a, b = torch.randn(n, device=DEV).to(dtype), torch.randn(n, device=DEV).to(dtype)
+    for tag, fn in (("add", torch.add), ("mul", torch.mul)):
+        out = torch.empty(n, device=DEV)
+        check(L.hap_binary(_lib.BINARY_TAGS[tag], a.data_ptr(), b.data_ptr(), _dt(a), out.data_ptr(), F32, n, 0, S))
+        torch.cuda.synchronize()
+        assert rel_err(out, fn(a.float(), b.float())) < 1e-6
+    dy = torch.randn(n, device=DEV)
+    da, db = torch.zeros(n, device=DEV), torch.zeros(n, device=DEV)
+    check(L.hap_mul_grad(a.data_ptr(), b.data_ptr(), _dt(a), dy.data_ptr(), F32, da.data_ptr(), db.data_ptr(),
+                         F32, n, 0, 0, S))
+    torch.cuda.synchronize()
+    assert rel_err(da, dy * b.float()) < 1e-6 and rel_err(db, dy * a.float()) < 1e-6
+    # self-product: d(a*a)/da = 2a
+    check(L.hap_mul_grad(a.data_ptr(), a.data_ptr(), _dt(a), dy.data_ptr(), F32, da.data_ptr(), da.data_ptr(),
+                         F32, n, 0, 0, S))
+    torch.cuda.synchronize()
+    assert rel_err(da, 2 * dy * a.float()) < 1e-6
+
+
+@pytest.mark.parametrize("shape,dims", [((8192, 768), (0, 1)), ((8192, 768), (0,)), ((8192, 768), (1,)),
+                                        ((5, 7), (1,)), ((3, 4, 5), (0, 2)), ((3, 4, 5), (1,)),
+                                        ((6, 0), (0,)), ((16,), (0,)), ((2, 3, 4, 5), (1, 2))])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_reduce_and_unreduce(shape, dims, dtype):
+    torch.manual_seed(5)
+    x = torch.randn(shape, device=DEV).to(dtype)
+    out_shape = tuple(e for a, e in enumerate(shape) if a not in dims)
+    y = torch.full(out_shape, 3.0, device=DEV)
+    mask = sum(1 << d for d in dims)
+    shp = _lib.i64_array(shape)
+    check(L.hap_reduce(x.data_ptr(), _dt(x), shp, len(shape), mask, y.data_ptr(), F32, 0, 0, S))
+    torch.cuda.synchronize()
+    want = x.float().sum(dim=dims)
+    assert (y - want).abs().max().item() <= 1e-4 * max(1.0, x.float().abs().sum().item() / max(1, want.numel()))
+    dy = torch.randn(out_shape, device=DEV)
+    dx = torch.ones(shape, device=DEV)
+    check(L.hap_unreduce(dy.data_ptr(), F32, shp, len(shape), mask, dx.data_ptr(), F32, 1, 0, S))
+    torch.cuda.synchronize()
+    expand = dy
+    for d in sorted(dims):
+        expand = expand.unsqueeze(d)
+    assert torch.allclose(dx, 1.0 + expand.expand(shape))
+
+
+def test_copy_block_strided_shards():
+    torch.manual_seed(6)
+    src = torch.randn(6, 10, 3, device=DEV)
+    dst = torch.zeros(6, 4, 3, device=DEV, dtype=torch.bfloat16)
+    check(L.hap_copy_block(src.data_ptr(), F32, 10, 5, dst.data_ptr(), BF16, 4, 1, 6, 3, 3, 0, 0, S))
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:, 1:4].float(), src[:, 5:8].to(torch.bfloat16).float())
+    assert dst[:, 0].abs().max().item() == 0
