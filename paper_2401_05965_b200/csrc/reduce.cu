@@ -181,7 +181,9 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
   HAP_CHECK_ARG(rank >= 0 && rank <= kMaxRank, "hap_reduce: rank > 8");
   HAP_CHECK_ARG((mask >> rank) == 0 || rank == 32, "hap_reduce: dims out of range");
   Geometry g = geometry(shape, rank, mask);
-  const int64_t n_out = g.outer * g.inner;
+  int64_t n_out = 1;
+  for (int a = 0; a < rank; ++a)
+    if (!(mask & (1u << a))) n_out *= shape[a];
   if (n_out == 0) return HAP_OK;
   const size_t ysz = dtype_size(yd);
   if (g.red == 0) {  // empty reduction (zero-size shard): y = 0 (+y)
@@ -260,7 +262,8 @@ extern "C" hap_status hap_unreduce(const void* dy, hap_dtype dyd, const int64_t*
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   HAP_CHECK_ARG(rank >= 0 && rank <= kMaxRank, "hap_unreduce: rank > 8");
   Geometry g = geometry(shape, rank, mask);
-  const int64_t n = g.outer * g.red * g.inner;
+  int64_t n = 1;
+  for (int a = 0; a < rank; ++a) n *= shape[a];
   if (n == 0) return HAP_OK;
   Dims d{rank, {}, mask};
   for (int a = 0; a < rank; ++a) d.shape[a] = shape[a];

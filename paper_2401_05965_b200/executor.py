@@ -165,6 +165,8 @@ class Executor:
         self.dtypes: dict[str, int] = {}
         self.sync_choice: dict[str, str] = {}
         self.graph: torch.cuda.CUDAGraph | None = None
+        self._pool: list[Buf] = []
+        self.bytes_allocated = 0
         self.source_dids = {i.output for i in program.instrs if i.kind in SOURCE_KINDS}
         self._check_program()
         self._infer()
@@ -274,8 +276,13 @@ class Executor:
                 self.req[ins.output] = any(self.req[d] for d in ins.operands)
 
     def _new(self, shape, dtype) -> Buf:
+        """Device buffer that lives as long as the executor: compiled ops hold
+        raw pointers, so every buffer (temporaries included) is pinned here."""
         t = torch.empty(max(1, int(math.prod(shape))), dtype=_TORCH[dtype], device=self.device)
-        return Buf(t, dtype, tuple(shape))
+        buf = Buf(t, dtype, tuple(shape))
+        self._pool.append(buf)
+        self.bytes_allocated += t.numel() * t.element_size()
+        return buf
 
     def _allocate(self):
         for did, shapes in self.shapes.items():

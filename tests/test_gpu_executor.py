@@ -55,8 +55,15 @@ def _check_losses(ex, want, dtype, scale):
     assert np.all(np.abs(got - want) <= RTOL[dtype] * scale), (got, want, scale)
 
 
-def _check_grads(ex, g, inputs, dtype):
-    want = O.grad_single(g, inputs)
+def _check_grads(ex, g, inputs, dtype, doc):
+    """Gradients against the oracle's distributed adjoint run in the
+    executor's storage precision (interpreter_np.storage_dtypes): float64
+    arithmetic, values rounded to bf16/fp32 exactly where the device stores
+    them.  Against pure float64, a ReLU input within one bf16 ulp of zero
+    flips its mask (chain4: activations ~600), which no bf16 run can match."""
+    program, m, table = O.load_plan(doc)
+    shapes = {n.id: n.shape for n in g.nodes}
+    _, want, _ = O.train_step(program, m, inputs, table, shapes, precision=dtype)
     for ref, value in want.items():
         per = ex.gradient(ref)
         assert per, f"no gradient for {ref}"
@@ -92,7 +99,7 @@ def test_planned_programs_match_reference(gname, cname, dtype):
             scale = max(float(np.max(np.abs(want))) if want.size else 1.0, 1.0)
             assert got.shape == want.shape
             assert (np.max(np.abs(got - want)) if want.size else 0.0) <= RTOL[dtype] * scale, did
-    _check_grads(ex, g, inputs, dtype)
+    _check_grads(ex, g, inputs, dtype, doc)
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
@@ -104,7 +111,7 @@ def test_programs_with_collectives_match_reference(stem, dtype):
     ex = _run(doc, g, inputs, dtype)
     want = vals["seed0:losses"]
     _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
-    _check_grads(ex, g, inputs, dtype)
+    _check_grads(ex, g, inputs, dtype, doc)
 
 
 def test_sgd_update_matches_oracle():

@@ -146,6 +146,8 @@ def test_reduce_and_unreduce(shape, dims, dtype):
     check(L.hap_reduce(x.data_ptr(), _dt(x), shp, len(shape), mask, y.data_ptr(), F32, 0, 0, S))
     torch.cuda.synchronize()
     want = x.float().sum(dim=dims)
+    if want.numel() == 0:
+        return
     assert (y - want).abs().max().item() <= 1e-4 * max(1.0, x.float().abs().sum().item() / max(1, want.numel()))
     dy = torch.randn(out_shape, device=DEV)
     dx = torch.ones(shape, device=DEV)
