@@ -34,6 +34,9 @@ sys.path.insert(0, ROOT)
 SEQ = 128
 PER_GPU_BATCH = 64
 LAYERS = 12
+# SGD step size: the loss is a plain sum over batch*seq*768 outputs, so the
+# gradients scale with the token count; this keeps repeated steps finite.
+LR = 1e-9
 
 
 def _peaks() -> dict:
@@ -192,7 +195,7 @@ def main() -> None:
     group = NcclGroup.from_torch_distributed() if world > 1 else LocalGroup(1)
     shapes = {nd.id: nd.shape for nd in g.sources()}
     ex = Executor(prog, n, table, shapes, group=group,
-                  config=ExecConfig(dtype="bf16", sm_caps=caps, lr=1e-4, cluster=cluster, ratios=ratios),
+                  config=ExecConfig(dtype="bf16", sm_caps=caps, lr=LR, cluster=cluster, ratios=ratios),
                   device=dev)
     inputs = workloads.synthetic_inputs(g, 0, scaled=True)
     ex.load(inputs)

@@ -887,7 +887,8 @@ class Executor:
     def step(self):
         """One training iteration: forward, backward, gradient sync, update."""
         if self.graph is not None:
-            self.graph.replay()
+            with torch.cuda.stream(self.stream):
+                self.graph.replay()
             return
         with torch.cuda.stream(self.stream):
             self._run(self.ops_fwd)

@@ -126,11 +126,16 @@ def synthetic_inputs(g: Graph, seed: int, scaled: bool = True) -> dict:
     import numpy as np
 
     rng = np.random.default_rng(seed)
+    # residual-branch output projections get the GPT-2 1/sqrt(2L) factor so a
+    # deep skeleton without normalisation keeps O(1) activations.
+    depth = sum(1 for n in g.nodes if n.id.endswith("_Wo"))
     out = {}
     for node in g.nodes:
         if node.op in ("Placeholder", "Parameter"):
             value = rng.standard_normal(node.shape)
             if scaled and node.op == "Parameter" and len(node.shape) == 2:
                 value = value / np.sqrt(node.shape[0])
+                if depth and node.id.endswith(("_Wo", "_W2")):
+                    value = value / np.sqrt(2 * depth)
             out[node.id] = value
     return out

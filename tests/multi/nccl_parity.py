@@ -1,0 +1,103 @@
+"""Multi-process parity: every m=2 golden program (plans and enumerated
+programs with collectives) executed with one process per GPU over NCCL,
+checked against the CPU oracle.  Launched by tests/test_gpu_multi.py as
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/multi/nccl_parity.py
+"""
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import goldens  # noqa: E402
+from oracle import interpreter_np as O  # noqa: E402
+from paper_2401_05965_b200.executor import ExecConfig, Executor, NcclGroup  # noqa: E402
+from paper_2401_05965_b200.program import DistributedProgram  # noqa: E402
+from paper_2401_05965_b200.sharding import table_from_plan  # noqa: E402
+
+RTOL = {"bf16": 2e-2, "fp32": 1e-3}
+
+
+def cases(world):
+    out = []
+    for gname, cname in goldens.value_cases():
+        doc = goldens.plan(gname, cname)
+        if doc["devices"] == world:
+            vals = goldens.values(gname, cname)
+            out.append((f"{gname}.{cname}", doc, gname, goldens.inputs(goldens.graph(gname), vals, goldens.seeds(vals)[0])))
+    for stem in goldens.program_cases():
+        doc, vals, gname = goldens.program_case(stem)
+        if doc["devices"] == world:
+            inputs = {k.split(":", 2)[2]: vals[k] for k in vals.files if k.startswith("seed0:input:")}
+            out.append((stem, doc, gname, inputs))
+    return out
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    group = NcclGroup.from_torch_distributed()
+    failures, count = [], 0
+    only = sys.argv[1] if len(sys.argv) > 1 else None
+    for name, doc, gname, inputs in cases(world):
+        if only and only not in name:
+            continue
+        g = goldens.graph(gname)
+        shapes = {n.id: n.shape for n in g.sources()}
+        program, m, table = O.load_plan(doc)
+        for dtype in ("fp32", "bf16"):
+            for gather in ("padded", "p2p"):
+                count += 1
+                ex = Executor(DistributedProgram.from_json(doc["program"]), m, table_from_plan(doc), shapes,
+                              group=group, config=ExecConfig(dtype=dtype, input_grads=True, gather=gather))
+                ex.load(inputs)
+                ex.step()
+                torch.cuda.synchronize()
+                losses = ex.losses()
+                env, want = O.run_distributed(program, m, inputs, table, precision=dtype)
+                _, sg, _ = O.train_step(program, m, inputs, table, {n.id: n.shape for n in g.nodes},
+                                        precision=dtype)
+                scale = max(1.0, abs(float(want[0])))
+                for ins in program.instrs:
+                    if ins.ref == program.loss and ins.kind == "reduce":
+                        scale = max(scale, float(np.sqrt(sum(np.sum(np.square(v)) for v in env[ins.operands[0]]))))
+                if any(abs(a - float(b)) > RTOL[dtype] * scale for a, b in zip(losses, want)):
+                    failures.append(f"{name} {dtype} {gather}: losses {losses} vs {[float(v) for v in want]}")
+                for ref, value in sg.items():
+                    for r, forms in ex.gradient(ref).items():
+                        for did, grad in forms:
+                            grad = grad.float().cpu().numpy()
+                            if "@shard" in did:
+                                axis = int(did.rsplit("shard", 1)[1])
+                                sizes = table[(ref, axis)]
+                                off = int(np.sum(sizes[:r]))
+                                value_r = np.take(value, np.arange(off, off + sizes[r]), axis=axis)
+                            else:
+                                value_r = value
+                            if value_r.size == 0:
+                                continue
+                            err = float(np.max(np.abs(grad - value_r))) / max(float(np.max(np.abs(value))), 1e-3)
+                            if err > RTOL[dtype]:
+                                failures.append(f"{name} {dtype} {gather}: grad {did}@{r} rel err {err:.3g}")
+                ex.group = None  # the communicator is shared across executors
+    fl = [None] * world
+    dist.all_gather_object(fl, failures)
+    if rank == 0:
+        allf = [f for sub in fl for f in sub]
+        print(f"nccl parity: {count} runs per rank, {len(allf)} failures")
+        for f in allf[:40]:
+            print("  FAIL", f)
+    group.close()
+    dist.destroy_process_group()
+    sys.exit(1 if any(fl) else 0)
+
+
+if __name__ == "__main__":
+    main()
