@@ -901,7 +901,9 @@ class Executor:
         self.step()  # warm-up outside capture (kernel attributes, NCCL setup)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=self.stream):
+        # thread-local capture: NCCL's proxy thread keeps issuing CUDA calls
+        # while this thread captures the collectives' kernels.
+        with torch.cuda.graph(g, stream=self.stream, capture_error_mode="thread_local"):
             self._run(self.ops_fwd)
             self._run(self.ops_bwd)
             self._run(self.ops_upd)
