@@ -97,9 +97,31 @@ __global__ void __launch_bounds__(kBlock) unary_kernel(int tag, const Tin* __res
 template <typename Txy, typename Tdy, typename Tdx>
 __global__ void __launch_bounds__(kBlock)
     unary_grad_kernel(int tag, const Txy* __restrict__ x, const Txy* __restrict__ y,
-                      const Tdy* __restrict__ dy, Tdx* dx, int64_t n, int accumulate) {
+                      const Tdy* __restrict__ dy, Tdx* dx, int64_t n, int accumulate, int vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t start = 0;
+  if (vec) {  // x / y only read when the derivative needs them
+    const int64_t nv = n / 8;
+    const bool need_x = tag == HAP_RELU, need_y = tag != HAP_RELU && tag != HAP_NEG;
+    for (int64_t i = tid; i < nv; i += stride) {
+      float xv[8] = {}, yv[8] = {}, g[8];
+      if (need_x) Vec8<Txy>::load(x + 8 * i, xv);
+      if (need_y) Vec8<Txy>::load(y + 8 * i, yv);
+      Vec8<Tdy>::load(dy + 8 * i, g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] *= unary_deriv(tag, xv[j], yv[j]);
+      if (accumulate) {
+        float o[8];
+        Vec8<Tdx>::load(dx + 8 * i, o);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] += o[j];
+      }
+      Vec8<Tdx>::store(dx + 8 * i, g);
+    }
+    start = nv * 8;
+  }
+  for (int64_t i = start + tid; i < n; i += stride) {
     const float xv = x ? to_f32(x[i]) : 0.f;
     const float yv = y ? to_f32(y[i]) : 0.f;
     float g = to_f32(dy[i]) * unary_deriv(tag, xv, yv);
@@ -137,10 +159,49 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(int tag, const Tin* __re
 template <typename Tin, typename Tdy, typename Td>
 __global__ void __launch_bounds__(kBlock)
     mul_grad_kernel(const Tin* __restrict__ a, const Tin* __restrict__ b, const Tdy* __restrict__ dy,
-                    Td* da, Td* db, int64_t n, int accumulate) {
+                    Td* da, Td* db, int64_t n, int accumulate, int vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool same = da == db;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  int64_t start = 0;
+  if (vec) {
+    const int64_t nv = n / 8;
+    for (int64_t i = tid; i < nv; i += stride) {
+      float va[8], vb[8], g[8], ga[8], gb[8];
+      Vec8<Tin>::load(a + 8 * i, va);
+      Vec8<Tin>::load(b + 8 * i, vb);
+      Vec8<Tdy>::load(dy + 8 * i, g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ga[j] = g[j] * vb[j];
+        gb[j] = g[j] * va[j];
+      }
+      if (same && da) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ga[j] += gb[j];
+      }
+      if (da) {
+        if (accumulate) {
+          float o[8];
+          Vec8<Td>::load(da + 8 * i, o);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ga[j] += o[j];
+        }
+        Vec8<Td>::store(da + 8 * i, ga);
+      }
+      if (db && !same) {
+        if (accumulate) {
+          float o[8];
+          Vec8<Td>::load(db + 8 * i, o);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) gb[j] += o[j];
+        }
+        Vec8<Td>::store(db + 8 * i, gb);
+      }
+    }
+    start = nv * 8;
+  }
+  for (int64_t i = start + tid; i < n; i += stride) {
     const float g = to_f32(dy[i]);
     const float ga = g * to_f32(b[i]), gb = g * to_f32(a[i]);
     if (same && da) {
@@ -256,15 +317,16 @@ extern "C" hap_status hap_unary_grad(int tag, const void* x, const void* y, hap_
   if (n <= 0) return HAP_OK;
   HAP_CHECK_ARG(tag == HAP_NEG || (tag == HAP_RELU ? x != nullptr : y != nullptr),
                 "hap_unary_grad: missing saved activation");
+  const int vec = (!x || aligned16(x)) && (!y || aligned16(y)) && aligned16(dy) && aligned16(dx);
   return HAP_DISPATCH_IO(xyd, dxd, [&] {
     if (dyd == HAP_BF16)
       unary_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
           tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
-          static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(dx), n, accumulate);
+          static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(dx), n, accumulate, vec);
     else
       unary_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
           tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
-          static_cast<const float*>(dy), static_cast<Tout*>(dx), n, accumulate);
+          static_cast<const float*>(dy), static_cast<Tout*>(dx), n, accumulate, vec);
     return launch_status("unary_grad_kernel");
   });
 }
@@ -287,16 +349,18 @@ extern "C" hap_status hap_mul_grad(const void* a, const void* b, hap_dtype ind, 
                                    int accumulate, int sm_cap, void* stream_) {
   HAP_STREAM;
   if (n <= 0) return HAP_OK;
+  const int vec = aligned16(a) && aligned16(b) && aligned16(dy) && (!da || aligned16(da)) &&
+                  (!db || aligned16(db));
   return HAP_DISPATCH_IO(ind, dd, [&] {
     if (dyd == HAP_BF16)
       mul_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
           static_cast<const Tin*>(a), static_cast<const Tin*>(b),
           static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(da), static_cast<Tout*>(db), n,
-          accumulate);
+          accumulate, vec);
     else
       mul_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
           static_cast<const Tin*>(a), static_cast<const Tin*>(b), static_cast<const float*>(dy),
-          static_cast<Tout*>(da), static_cast<Tout*>(db), n, accumulate);
+          static_cast<Tout*>(da), static_cast<Tout*>(db), n, accumulate, vec);
     return launch_status("mul_grad_kernel");
   });
 }

@@ -20,6 +20,7 @@
 // multiple of 16 bytes) — small corpus shapes and zero-size shards.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -185,11 +186,27 @@ __device__ __forceinline__ void store_row_chunk(OutT* dst, const uint32_t (&r)[3
   }
 }
 
+// Split-K partial: C += r (fp32, vector reduction in L2).
+__device__ __forceinline__ void red_row_chunk(float* dst, const uint32_t (&r)[32], int valid, bool vec) {
+  if (vec && valid == 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * i),
+                   "f"(__uint_as_float(r[4 * i])), "f"(__uint_as_float(r[4 * i + 1])),
+                   "f"(__uint_as_float(r[4 * i + 2])), "f"(__uint_as_float(r[4 * i + 3]))
+                   : "memory");
+  } else {
+    for (int i = 0; i < valid; ++i) atomicAdd(dst + i, __uint_as_float(r[i]));
+  }
+}
+
+// Work unit u covers output tile (u % num_tiles) and K-blocks
+// [split * kb_per_split, min(k_blocks, (split + 1) * kb_per_split)), split = u / num_tiles.
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    OutT* __restrict__ C, int64_t ldc, int M, int N, int K, int accumulate,
-                   int vec_ok) {
+                   int vec_ok, int splits, int kb_per_split) {
   using G = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -206,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
+  const int num_units = num_tiles * splits;
   const int k_blocks = (K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -239,10 +257,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int t = u % num_tiles;
+        const int kb0 = (u / num_tiles) * kb_per_split;
+        const int kb1 = min(k_blocks, kb0 + kb_per_split);
         const int m0 = (t % m_tiles) * BM;
         const int n0 = (t / m_tiles) * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_expect_tx(fb, G::kStageBytes);
@@ -281,11 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int kb0 = (u / num_tiles) * kb_per_split;
+        const int kb1 = min(k_blocks, kb0 + kb_per_split);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
@@ -295,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t aoff = kAMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             const uint32_t boff = kBMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             tc_mma(d_tmem, sdesc(sa + aoff, kALbo, 1024), sdesc(sb + boff, kBLbo, 1024), kIdesc,
-                   (kb | kk) != 0);
+                   (kb != kb0) || (kk != 0));
           }
           tc_commit(empty0 + 8 * stage);
           if (++stage == G::kStages) {
@@ -313,7 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const int t = u % num_tiles;
       const int m0 = (t % m_tiles) * BM;
       const int n0 = (t / m_tiles) * BN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
@@ -326,7 +350,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
         const int col0 = n0 + c * 32;
         const int valid = N - col0 < 32 ? N - col0 : 32;
-        if (row < M && valid > 0) store_row_chunk<OutT>(crow + col0, r, valid, vec_ok, accumulate);
+        if (row < M && valid > 0) {
+          if constexpr (std::is_same<OutT, float>::value) {
+            if (splits > 1) {
+              red_row_chunk(crow + col0, r, valid, vec_ok);
+              continue;
+            }
+          }
+          store_row_chunk<OutT>(crow + col0, r, valid, vec_ok, accumulate);
+        }
       }
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
@@ -376,7 +408,8 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, i
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M,
-                  int N, int K, int accumulate, int vec_ok, int sm_cap, cudaStream_t stream) {
+                  int N, int K, int accumulate, int vec_ok, int sm_cap, int splits, int kb_per_split,
+                  cudaStream_t stream) {
   using G = Cfg<BN>;
   auto kern = gemm_tc_kernel<BN, kAMN, kBMN, OutT>;
   static bool configured = false;
@@ -385,20 +418,55 @@ hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t
     configured = true;
   }
   const int64_t tiles = static_cast<int64_t>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = capped_grid(tiles, sm_cap);
+  const int grid = capped_grid(tiles * splits, sm_cap);
   kern<<<grid, kThreads, G::kSmem, stream>>>(ma, mb, static_cast<OutT*>(C), ldc, M, N, K,
-                                              accumulate, vec_ok);
+                                              accumulate, vec_ok, splits, kb_per_split);
   return launch_status("gemm_tc_kernel");
 }
 
 template <int BN, typename OutT>
 hap_status dispatch_major(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
                           void* C, int64_t ldc, int M, int N, int K, int acc, int vec, int cap,
-                          cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
-  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
-  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
-  return launch<BN, true, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, s);
+                          int sp, int kps, cudaStream_t s) {
+  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  return launch<BN, true, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+}
+
+// Tile width and split-K factor: maximise the fraction of the (capped) SMs
+// kept busy over the rounds of a persistent launch.  BN=128 tiles are
+// smem-bandwidth bound on one SM (8 KB of operands per 64-cycle MMA), so they
+// are discounted; split-K (fp32 output only, partials reduced in L2) fills
+// the GPU for the weight-gradient GEMMs, whose M x N is small and K = tokens.
+struct Shape {
+  int bn, splits, kb_per_split;
+};
+
+Shape choose_shape(int64_t M, int64_t N, int64_t K, bool fp32_out, int cap) {
+  const int64_t k_blocks = (K + BK - 1) / BK;
+  Shape best{256, 1, static_cast<int>(k_blocks)};
+  double best_eff = -1.0;
+  for (int bn : {256, 128}) {
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    int64_t splits = 1;
+    if (fp32_out && tiles < cap && k_blocks >= 8) {
+      splits = std::min<int64_t>(cap / tiles, k_blocks / 4);
+      if (splits < 1) splits = 1;
+    }
+    const int64_t kps = (k_blocks + splits - 1) / splits;
+    splits = (k_blocks + kps - 1) / kps;
+    const int64_t work = tiles * splits;
+    const int64_t rounds = (work + cap - 1) / cap;
+    double eff = static_cast<double>(work) / static_cast<double>(rounds * cap);
+    if (bn == 128) eff *= 0.9;
+    if (splits > 1) eff *= 0.97;  // partial-sum traffic
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = {bn, static_cast<int>(splits), static_cast<int>(kps)};
+    }
+  }
+  return best;
 }
 
 }  // namespace tc
@@ -530,7 +598,9 @@ extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const v
   }
   HAP_CHECK_ARG(A != nullptr && B != nullptr, "hap_matmul: null operand");
   if (tc_eligible(A, lda, transA, B, ldb, transB, M, N, K, in_dtype)) {
-    const int BN = N > 128 ? 256 : 128;
+    const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
+    const tc::Shape shp = tc::choose_shape(M, N, K, out_dtype == HAP_F32, cap);
+    const int BN = shp.bn;
     CUtensorMap ma, mb;
     bool ok = transA ? tc::make_map(&ma, A, M, K, lda, tc::BK)
                      : tc::make_map(&ma, A, K, M, lda, tc::BM);
@@ -540,17 +610,20 @@ extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const v
     const size_t osz = dtype_size(out_dtype);
     const int vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * osz) % 16 == 0);
     const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+    const int sp = shp.splits, kps = shp.kb_per_split;
     if (out_dtype == HAP_BF16) {
       return BN == 256
                  ? tc::dispatch_major<256, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
-                                                          accumulate, vec, sm_cap, stream)
+                                                          accumulate, vec, sm_cap, 1, kps, stream)
                  : tc::dispatch_major<128, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
-                                                          accumulate, vec, sm_cap, stream);
+                                                          accumulate, vec, sm_cap, 1, kps, stream);
     }
+    if (sp > 1 && !accumulate)  // split-K partials add into a zeroed output
+      HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, stream));
     return BN == 256 ? tc::dispatch_major<256, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
-                                                      accumulate, vec, sm_cap, stream)
+                                                      accumulate, vec, sm_cap, sp, kps, stream)
                      : tc::dispatch_major<128, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
-                                                      accumulate, vec, sm_cap, stream);
+                                                      accumulate, vec, sm_cap, sp, kps, stream);
   }
   return HAP_DISPATCH_IO(in_dtype, out_dtype, [&] {
     return simt_launch<Tin, Tout>(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, accumulate,

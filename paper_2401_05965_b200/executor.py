@@ -569,6 +569,7 @@ class Executor:
         L = self.group.local_ranks
         loss = self.program.loss
         written: set[str] = set()   # grads that already hold a contribution
+        self._written = written
 
         def contrib(did: str) -> int:
             """accumulate flag for the next contribution to grad(did)."""
@@ -646,6 +647,17 @@ class Executor:
                         g = self._grad(ops[0], r)
                         self._emit("hap_mul_grad", a.ptr, a.ptr, a.dtype, dy[r].ptr, dy[r].dtype, g.ptr,
                                    g.ptr, g.dtype, g.numel, acc, self.caps[r], self._sptr())
+                elif need[0] and need[1] and (ops[0] in self._written) == (ops[1] in self._written):
+                    # both adjoints in one pass over dy, a and b
+                    acc = contrib(ops[0])
+                    contrib(ops[1])
+                    for r in L:
+                        a, b = x[0][r], x[1][r]
+                        ga, gb = self._grad(ops[0], r), self._grad(ops[1], r)
+                        if a.dtype != b.dtype or ga.dtype != gb.dtype:
+                            raise ExecutionError("mixed-precision mul operands")
+                        self._emit("hap_mul_grad", a.ptr, b.ptr, a.dtype, dy[r].ptr, dy[r].dtype, ga.ptr,
+                                   gb.ptr, ga.dtype, ga.numel, acc, self.caps[r], self._sptr())
                 else:
                     for i in (0, 1):
                         if not need[i]:
