@@ -167,6 +167,65 @@ def enumerated_cases(per_case: int = 10) -> None:
             print(f"programs {gname}.{cname}: {len(chosen)} of {len(groups)} signatures", flush=True)
 
 
+def planner_goldens() -> None:
+    """Reference planner internals on the corpus: theory digests, search
+    statistics under every optimisation toggle, LP solutions, rounding,
+    segmentation and exhaustive-enumeration minima (planner restatement pins)."""
+    import hashlib
+    import itertools
+
+    from shardplan import (ShardingRatios, assign_segments, build_theory, enumerate_programs,
+                           optimize_ratios, round_shards, single_segment, synthesize)
+    from shardplan.load_balancer import SegmentProblem, build_lp, lp_solve
+    from shardplan.synthesizer import SearchConfig
+    from shardplan.theory import theory_to_json
+
+    out: dict = {"theory": {}, "search": {}, "enumerate": {}, "lp": [], "round": [], "segments": {},
+                 "ratios": {}}
+    homog2 = ClusterSpec.from_dict(ref_corpus.HOMOG2)
+    for name, doc in ref_corpus.CORPUS.items():
+        g = graph_from_dict(doc)
+        for guards, fuse in itertools.product((False, True), repeat=2):
+            js = json.dumps(theory_to_json(build_theory(g, 2, guards=guards, fuse=fuse)), sort_keys=True)
+            out["theory"][f"{name}:{int(guards)}{int(fuse)}"] = hashlib.sha256(js.encode()).hexdigest()
+        B = ShardingRatios.uniform(2)
+        for guards, fuse, prune in itertools.product((False, True), repeat=3):
+            th = build_theory(g, 2, guards=guards, fuse=fuse)
+            res = synthesize(g, th, homog2, B, cfg=SearchConfig(prune_properties=prune))
+            out["search"][f"{name}:{int(guards)}{int(fuse)}{int(prune)}"] = {
+                "cost": res.cost_s, "expansions": res.expansions, "generated": res.generated,
+                "purged": res.purged, "program": res.program.canonical()}
+        en = enumerate_programs(g, build_theory(g, 2, guards=False, fuse=False), homog2, B)
+        out["enumerate"][name] = {"cost": en.cost_s, "explored": en.explored,
+                                  "complete": en.complete_states, "program": en.program.canonical()}
+        for k in range(1, min(4, len(g.nodes)) + 1):
+            out["segments"][f"{name}:{k}"] = assign_segments(g, k).segment_of
+        for cname in ("hetero2", "skew2", "homog3"):
+            spec = ClusterSpec.from_dict(getattr(ref_corpus, cname.upper()))
+            res = synthesize(g, build_theory(g, spec.m), spec, ShardingRatios.proportional_to_flops(spec))
+            out["ratios"][f"{name}:{cname}"] = [list(r) for r in optimize_ratios(res.program, g, spec).rows]
+    rng = np.random.default_rng(5)
+    for i in range(40):
+        m = 2 + i % 3
+        stages = int(rng.integers(1, 4))
+        prob = SegmentProblem(row_index=0, m=m, comp_a=[rng.uniform(0.0, 4.0, m) for _ in range(stages)],
+                              comp_c=[rng.uniform(0.0, 1.0, m) for _ in range(stages)],
+                              slope_M=float(rng.uniform(0.0, 3.0)) if i % 3 else 0.0,
+                              linear_B=rng.uniform(0.0, 2.0, m), const_s=float(rng.uniform(0.0, 1.0)))
+        sol = lp_solve(build_lp(prob))
+        out["lp"].append({"m": m, "comp_a": [a.tolist() for a in prob.comp_a],
+                          "comp_c": [c.tolist() for c in prob.comp_c], "slope_M": prob.slope_M,
+                          "linear_B": prob.linear_B.tolist(), "const_s": prob.const_s,
+                          "status": sol.status, "x": sol.x.tolist(), "objective": sol.objective})
+    for i in range(200):
+        m = 1 + i % 5
+        row = tuple(float(v) for v in rng.dirichlet(np.ones(m)))
+        extent = int(rng.integers(0, 40))
+        out["round"].append({"extent": extent, "row": list(row), "sizes": round_shards(extent, row)})
+    _dump(os.path.join(HERE, "planner.json"), out)
+    print("planner goldens written", flush=True)
+
+
 def fd_gradients(gname: str, gdoc: dict, eps: float = 1e-5) -> None:
     g = graph_from_dict(gdoc)
     inputs = random_inputs(g, np.random.default_rng(0))
@@ -208,6 +267,7 @@ def main() -> None:
         fd_gradients(gname, gdoc)
 
     enumerated_cases()
+    planner_goldens()
 
     # configs[0]: 2-layer MLP, hidden 1024, batch 64, two devices at speed 1:2.
     mlp_cluster = workloads.cluster_doc([148, 296], bytes_per_element=2)

@@ -1,0 +1,125 @@
+"""The planner restatement emits exactly what the reference planner emits:
+plan documents byte for byte (program, ratios, shard table, estimate), the
+derived theory, the search's statistics under every optimisation toggle, LP
+solutions, shard rounding and segmentation — all against goldens the
+reference package generated (tests/golden/make_golden.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import goldens
+from paper_2401_05965_b200 import (ClusterSpec, ShardingRatios, alternate, assign_segments, build_theory,
+                                   enumerate_programs, optimize_ratios, round_shards, synthesize)
+from paper_2401_05965_b200.cli import main as cli_main, plan_document, plan_text
+from paper_2401_05965_b200.load_balancer import SegmentProblem, build_lp, lp_solve
+from paper_2401_05965_b200.synthesizer import SearchConfig
+from paper_2401_05965_b200.theory import theory_to_json
+
+PLANNER = goldens.load_json("planner.json")
+CORPUS = sorted({k.split(":")[0] for k in PLANNER["theory"]})
+HOMOG2 = ClusterSpec.from_dict(goldens.load_json("clusters", "homog2.json"))
+SLOW = os.environ.get("HAP_SLOW_TESTS") == "1"
+
+
+def _plan_cases():
+    cases = []
+    for name in sorted(os.listdir(os.path.join(goldens.GOLDEN, "plans"))):
+        gname, cname = name[:-5].rsplit(".", 1)
+        if gname.startswith("bert12") and not SLOW:
+            continue  # 75-170 s each; HAP_SLOW_TESTS=1 includes them
+        cases.append((gname, cname))
+    return cases
+
+
+@pytest.mark.parametrize("gname,cname", _plan_cases())
+def test_plan_documents_are_byte_identical_to_the_reference(gname, cname):
+    g = goldens.graph(gname)
+    spec = ClusterSpec.from_dict(goldens.load_json("clusters", f"{cname}.json"))
+    text = plan_text(plan_document(g, spec, alternate(g, spec)))
+    with open(os.path.join(goldens.GOLDEN, "plans", f"{gname}.{cname}.json")) as fh:
+        assert text == fh.read()
+
+
+@pytest.mark.parametrize("name", CORPUS)
+def test_theory_matches_reference(name):
+    import hashlib
+
+    g = goldens.graph(name)
+    for guards in (False, True):
+        for fuse in (False, True):
+            js = json.dumps(theory_to_json(build_theory(g, 2, guards=guards, fuse=fuse)), sort_keys=True)
+            want = PLANNER["theory"][f"{name}:{int(guards)}{int(fuse)}"]
+            assert hashlib.sha256(js.encode()).hexdigest() == want, (guards, fuse)
+
+
+@pytest.mark.parametrize("name", CORPUS)
+def test_search_statistics_match_reference_under_every_toggle(name):
+    g = goldens.graph(name)
+    B = ShardingRatios.uniform(2)
+    for guards in (False, True):
+        for fuse in (False, True):
+            th = build_theory(g, 2, guards=guards, fuse=fuse)
+            for prune in (False, True):
+                res = synthesize(g, th, HOMOG2, B, cfg=SearchConfig(prune_properties=prune))
+                want = PLANNER["search"][f"{name}:{int(guards)}{int(fuse)}{int(prune)}"]
+                assert res.cost_s == want["cost"]
+                assert (res.expansions, res.generated, res.purged) == \
+                    (want["expansions"], want["generated"], want["purged"])
+                assert res.program.canonical() == want["program"]
+
+
+@pytest.mark.parametrize("name", CORPUS)
+def test_enumeration_and_segments_and_ratios_match_reference(name):
+    g = goldens.graph(name)
+    en = enumerate_programs(g, build_theory(g, 2, guards=False, fuse=False), HOMOG2, ShardingRatios.uniform(2))
+    want = PLANNER["enumerate"][name]
+    assert (en.cost_s, en.explored, en.complete_states) == (want["cost"], want["explored"], want["complete"])
+    assert en.program.canonical() == want["program"]
+    for k in range(1, min(4, len(g.nodes)) + 1):
+        assert assign_segments(g, k).segment_of == PLANNER["segments"][f"{name}:{k}"]
+    for cname in ("hetero2", "skew2", "homog3"):
+        spec = ClusterSpec.from_dict(goldens.load_json("clusters", f"{cname}.json"))
+        res = synthesize(g, build_theory(g, spec.m), spec, ShardingRatios.proportional_to_flops(spec))
+        rows = [list(r) for r in optimize_ratios(res.program, g, spec).rows]
+        assert rows == PLANNER["ratios"][f"{name}:{cname}"]
+
+
+def test_lp_solutions_match_reference_exactly():
+    for case in PLANNER["lp"]:
+        prob = SegmentProblem(row_index=0, m=case["m"], comp_a=[np.array(a) for a in case["comp_a"]],
+                              comp_c=[np.array(c) for c in case["comp_c"]], slope_M=case["slope_M"],
+                              linear_B=np.array(case["linear_B"]), const_s=case["const_s"])
+        sol = lp_solve(build_lp(prob))
+        assert sol.status == case["status"]
+        assert sol.x.tolist() == case["x"]
+        assert sol.objective == case["objective"]
+
+
+def test_lp_worked_examples():
+    # load_balancer.py build_lp docstring: B = [2/3, 1/3]; uniform; [0.5, 0.5] with objective 2.5
+    for prob, want_b, want_obj in (
+            (SegmentProblem(0, 2, comp_a=[np.array([1.0, 2.0])], comp_c=[np.zeros(2)]), [2 / 3, 1 / 3], 2 / 3),
+            (SegmentProblem(0, 2, slope_M=1e6), [0.5, 0.5], 5e5),
+            (SegmentProblem(0, 2, comp_a=[np.array([1.0, 2.0])], comp_c=[np.zeros(2)], slope_M=3.0),
+             [0.5, 0.5], 2.5)):
+        sol = lp_solve(build_lp(prob))
+        assert np.allclose(sol.x[:2], want_b, atol=1e-6) and abs(sol.objective - want_obj) <= 1e-6
+
+
+def test_round_shards_matches_reference():
+    for case in PLANNER["round"]:
+        assert round_shards(case["extent"], case["row"]) == case["sizes"]
+
+
+def test_cli_plan_writes_the_reference_bytes(tmp_path, capsys):
+    out = tmp_path / "plan.json"
+    graph = os.path.join(goldens.GOLDEN, "graphs", "matmul_reduce.json")
+    cluster = os.path.join(goldens.GOLDEN, "clusters", "hetero2.json")
+    assert cli_main(["plan", graph, cluster, "-o", str(out)]) == 0
+    assert "cost: 5.76e-10 s" in capsys.readouterr().out
+    with open(os.path.join(goldens.GOLDEN, "plans", "matmul_reduce.hetero2.json")) as fh:
+        assert out.read_text() == fh.read()
+    assert cli_main(["plan", str(tmp_path / "missing.json"), cluster]) == 2
+    assert cli_main(["enumerate", graph, os.path.join(goldens.GOLDEN, "clusters", "homog2.json")]) == 0
