@@ -21,6 +21,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -32,17 +34,22 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int UMMA_K = 16;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
+
+// Epilogue staging: 8 warps x 2 buffers x (32 rows x 128 B), 128B-swizzled
+// boxes for TMA bulk stores.
+constexpr int kStageOutBytes = kEpiWarps * 2 * 32 * 128;
 
 template <int BN>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kStages = BN == 256 ? 3 : 5;
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kBarrierBytes = 256;
-  static constexpr int kSmem = kStages * kStageBytes + kBarrierBytes + 1024;
+  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + kBarrierBytes + 1024;
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -200,18 +207,124 @@ __device__ __forceinline__ void red_row_chunk(float* dst, const uint32_t (&r)[32
   }
 }
 
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+
+// Epilogue modes: direct per-thread stores (any layout), TMA bulk store, TMA
+// bulk reduce-add (fp32 accumulate / split-K partials).
+enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2 };
+
+// Drain one warp's 32 rows x BN/2 columns of a finished accumulator.
+// TMA modes stage 32 x 128 B boxes (64 bf16 or 32 fp32 columns) in a
+// 128B-swizzled double buffer — 16-byte chunk c of row r at c ^ (r & 7), the
+// TMA SWIZZLE_128B pattern, which spreads a warp's 16 B stores over all banks —
+// and hand each box to the TMA engine, so global writes are full lines issued
+// asynchronously instead of 32 scattered row segments per store instruction.
+template <int BN, typename OutT>
+__device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter, int half, int lane, int row0,
+                                                  int col0, int M, int N, OutT* C, int64_t ldc, int mode,
+                                                  int vec_ok, int accumulate, int splits,
+                                                  const CUtensorMap* tmC, uint8_t* buf) {
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16);
+  const int first = col0 + half * (BN / 2);
+  if (mode == EPI_DIRECT) {
+    const int row = row0 + lane;
+    OutT* crow = C + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + half * (BN / 2) + c * 32, r);
+      const int col = first + c * 32;
+      const int valid = N - col < 32 ? N - col : 32;
+      if (row < M && valid > 0) {
+        if constexpr (std::is_same<OutT, float>::value) {
+          if (splits > 1) {
+            red_row_chunk(crow + col, r, valid, vec_ok);
+            continue;
+          }
+        }
+        store_row_chunk<OutT>(crow + col, r, valid, vec_ok, accumulate);
+      }
+    }
+    return;
+  }
+  constexpr int W = 128 / static_cast<int>(sizeof(OutT));   // columns per box
+  constexpr int kBoxes = (BN / 2) / W;
+  const uint32_t buf0 = smem_u32(buf);
+#pragma unroll 1
+  for (int b = 0; b < kBoxes; ++b) {
+    const uint32_t dst = buf0 + (b & 1) * 4096;
+    if (lane == 0) bulk_wait_read1();   // the buffer's previous box has been read out
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < W / 32; ++k) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + half * (BN / 2) + b * W + k * 32, r);
+      if constexpr (std::is_same<OutT, float>::value) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t at = dst + lane * 128 + (((j) ^ (lane & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(r[4 * j]), "r"(r[4 * j + 1]),
+                       "r"(r[4 * j + 2]), "r"(r[4 * j + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t p[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * j + 2 * e]),
+                                                     __uint_as_float(r[8 * j + 2 * e + 1]));
+            p[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          const uint32_t at = dst + lane * 128 + (((k * 4 + j) ^ (lane & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]),
+                       "r"(p[3]));
+        }
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (mode == EPI_TMA_ADD) tma_reduce_add_2d(tmC, dst, first + b * W, row0);
+      else tma_store_2d(tmC, dst, first + b * W, row0);
+      bulk_commit();
+    }
+  }
+}
+
 // Work unit u covers output tile (u % num_tiles) and K-blocks
 // [split * kb_per_split, min(k_blocks, (split + 1) * kb_per_split)), split = u / num_tiles.
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   OutT* __restrict__ C, int64_t ldc, int M, int N, int K, int accumulate,
-                   int vec_ok, int splits, int kb_per_split) {
+                   const __grid_constant__ CUtensorMap tmC, OutT* __restrict__ C, int64_t ldc, int M, int N,
+                   int K, int accumulate, int vec_ok, int splits, int kb_per_split, int epi_mode) {
   using G = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + G::kStages * G::kStageBytes);
+  uint8_t* staging = smem + G::kStages * G::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStageOutBytes);
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + G::kStages);
   const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
@@ -237,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 128);
+      mbar_init(tempty0 + 8 * a, kEpiWarps * 32);
     }
     fence_barrier_init();
   }
@@ -332,8 +445,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> global
-    const int quarter = warp & 3;
+    // ---------------- epilogue: TMEM -> registers -> (smem -> TMA | global)
+    const int quarter = warp & 3;              // TMEM lanes 32*quarter .. +31
+    const int half = (warp - 4) >> 2;          // which half of the tile's columns
+    uint8_t* buf = staging + (warp - 4) * 8192;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -342,29 +457,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = (t / m_tiles) * BN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const int row = m0 + quarter * 32 + lane;
-      OutT* crow = C + static_cast<int64_t>(row) * ldc;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
-        const int col0 = n0 + c * 32;
-        const int valid = N - col0 < 32 ? N - col0 : 32;
-        if (row < M && valid > 0) {
-          if constexpr (std::is_same<OutT, float>::value) {
-            if (splits > 1) {
-              red_row_chunk(crow + col0, r, valid, vec_ok);
-              continue;
-            }
-          }
-          store_row_chunk<OutT>(crow + col0, r, valid, vec_ok, accumulate);
-        }
-      }
+      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, n0, M, N, C, ldc,
+                                  epi_mode, vec_ok, accumulate, splits, &tmC, buf);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -372,6 +472,241 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(G::kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ 2-CTA (SM pair) variant
+// A cluster of two CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2: CTA r stages rows [128r, 128r+128) of A and
+// columns [r*BN/2, (r+1)*BN/2) of B; the pair's tensor cores read the peer's
+// B half, so each SM moves half the B bytes of the single-CTA kernel.  CTA 0
+// (the leader) issues every MMA; both CTAs' TMA loads complete on the
+// leader's full barrier, the leader's commits multicast to both CTAs' empty
+// and TMEM-full barriers, and both epilogues release the accumulator on the
+// leader's TMEM-empty barrier.
+template <int BN>
+struct Cfg2 {
+  static constexpr int kStages = BN == 256 ? 5 : 6;
+  static constexpr int kABytes = 128 * BK * 2;
+  static constexpr int kBBytes = (BN / 2) * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 256 + 1024;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t cta) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(cta));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cluster_bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAITC_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar,
+                                                 int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int BN, bool kAMN, bool kBMN, typename OutT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmC, OutT* __restrict__ C, int64_t ldc, int M, int N,
+                    int K, int accumulate, int vec_ok, int splits, int kb_per_split, int epi_mode) {
+  using G = Cfg2<BN>;
+  constexpr int HB = BN / 2;  // B columns staged per CTA
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* staging = smem + G::kStages * G::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStageOutBytes);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = smem_u32(bars + G::kStages);
+  const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
+  const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int num_pairs = gridDim.x >> 1;
+  const int m_tiles = (M + 255) / 256;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_units = num_tiles * splits;
+  const int k_blocks = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < G::kStages; ++s) {
+      mbar_init(full0 + 8 * s, 2);   // one producer arrival per CTA (+ both CTAs' bytes)
+      mbar_init(empty0 + 8 * s, 1);  // the leader's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(G::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < num_units; u += num_pairs) {
+        const int t = u % num_tiles;
+        const int kb0 = (u / num_tiles) * kb_per_split;
+        const int kb1 = min(k_blocks, kb0 + kb_per_split);
+        const int m0 = (t % m_tiles) * 256 + 128 * static_cast<int>(rank);
+        const int n0 = (t / m_tiles) * BN + HB * static_cast<int>(rank);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t leader_full = map_to_cta(full0 + 8 * stage, 0);
+          if (rank == 0) mbar_expect_tx_cluster(leader_full, 2 * G::kStageBytes);
+          else mbar_arrive_cluster(leader_full);
+          const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
+          const uint32_t sb = sa + G::kABytes;
+          const int k0 = kb * BK;
+          if (kAMN) {
+            tma_load_2d_pair(sa, &tmA, leader_full, m0, k0);
+            tma_load_2d_pair(sa + BK * 128, &tmA, leader_full, m0 + 64, k0);
+          } else {
+            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+          }
+          if (kBMN) {
+#pragma unroll
+            for (int c = 0; c < HB / 64; ++c) tma_load_2d_pair(sb + c * BK * 128, &tmB, leader_full, n0 + 64 * c, k0);
+          } else {
+            tma_load_2d_pair(sb, &tmB, leader_full, k0, n0);
+          }
+          if (++stage == G::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA only)
+      constexpr uint32_t kIdesc = idesc(256, BN, kAMN, kBMN);
+      constexpr uint32_t kALbo = kAMN ? BK * 128 : 16;
+      constexpr uint32_t kBLbo = kBMN ? BK * 128 : 16;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = pair; u < num_units; u += num_pairs) {
+        const int kb0 = (u / num_tiles) * kb_per_split;
+        const int kb1 = min(k_blocks, kb0 + kb_per_split);
+        mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait_cluster(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
+          const uint32_t sb = sa + G::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint32_t aoff = kAMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
+            const uint32_t boff = kBMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
+            tc_mma_pair(d_tmem, sdesc(sa + aoff, kALbo, 1024), sdesc(sb + boff, kBLbo, 1024), kIdesc,
+                        (kb != kb0) || (kk != 0));
+          }
+          tc_commit_pair(empty0 + 8 * stage);
+          if (++stage == G::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(tfull0 + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): own 128 rows of the 256-row tile
+    const int quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
+    uint8_t* buf = staging + (warp - 4) * 8192;
+    const uint32_t leader_tempty = map_to_cta(tempty0, 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < num_units; u += num_pairs) {
+      const int t = u % num_tiles;
+      const int m0 = (t % m_tiles) * 256 + 128 * static_cast<int>(rank);
+      const int n0 = (t / m_tiles) * BN;
+      mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, n0, M, N, C, ldc,
+                                  epi_mode, vec_ok, accumulate, splits, &tmC, buf);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(G::kTmemCols));
   }
 }
 
@@ -406,10 +741,25 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, i
   return r == CUDA_SUCCESS;
 }
 
+// Output tensor map for the TMA epilogue: boxes of 128 bytes x 32 rows.
+bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int es = dt == HAP_BF16 ? 2 : 4;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * es};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt == HAP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr,
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int BN, bool kAMN, bool kBMN, typename OutT>
-hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t ldc, int M,
-                  int N, int K, int accumulate, int vec_ok, int sm_cap, int splits, int kb_per_split,
-                  cudaStream_t stream) {
+hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int mode, void* C,
+                  int64_t ldc, int M, int N, int K, int accumulate, int vec_ok, int sm_cap, int splits,
+                  int kb_per_split, cudaStream_t stream) {
   using G = Cfg<BN>;
   auto kern = gemm_tc_kernel<BN, kAMN, kBMN, OutT>;
   static bool configured = false;
@@ -419,19 +769,49 @@ hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int64_t
   }
   const int64_t tiles = static_cast<int64_t>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = capped_grid(tiles * splits, sm_cap);
-  kern<<<grid, kThreads, G::kSmem, stream>>>(ma, mb, static_cast<OutT*>(C), ldc, M, N, K,
-                                              accumulate, vec_ok, splits, kb_per_split);
+  kern<<<grid, kThreads, G::kSmem, stream>>>(ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K,
+                                              accumulate, vec_ok, splits, kb_per_split, mode);
   return launch_status("gemm_tc_kernel");
+}
+
+template <int BN, bool kAMN, bool kBMN, typename OutT>
+hap_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int mode, void* C,
+                   int64_t ldc, int M, int N, int K, int accumulate, int vec_ok, int sm_cap, int splits,
+                   int kb_per_split, cudaStream_t stream) {
+  using G = Cfg2<BN>;
+  auto kern = gemm_tc2_kernel<BN, kAMN, kBMN, OutT>;
+  static bool configured = false;
+  if (!configured) {
+    HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    configured = true;
+  }
+  const int64_t tiles = static_cast<int64_t>((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
+  int64_t pairs = std::min<int64_t>(tiles * splits, std::max(1, cap / 2));
+  kern<<<static_cast<int>(2 * pairs), kThreads, G::kSmem, stream>>>(
+      ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K, accumulate, vec_ok, splits, kb_per_split, mode);
+  return launch_status("gemm_tc2_kernel");
+}
+
+template <int BN, typename OutT>
+hap_status dispatch_major2(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
+                           const CUtensorMap& mc, int mode, void* C,
+                           int64_t ldc, int M, int N, int K, int acc, int vec, int cap, int sp, int kps,
+                           cudaStream_t s) {
+  if (!amn && !bmn) return launch2<BN, false, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (!amn && bmn) return launch2<BN, false, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (amn && !bmn) return launch2<BN, true, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  return launch2<BN, true, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
 }
 
 template <int BN, typename OutT>
 hap_status dispatch_major(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
-                          void* C, int64_t ldc, int M, int N, int K, int acc, int vec, int cap,
+                          const CUtensorMap& mc, int mode, void* C, int64_t ldc, int M, int N, int K, int acc, int vec, int cap,
                           int sp, int kps, cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  return launch<BN, true, true, OutT>(ma, mb, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+  return launch<BN, true, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
 }
 
 // Tile width and split-K factor: maximise the fraction of the (capped) SMs
@@ -441,29 +821,39 @@ hap_status dispatch_major(bool amn, bool bmn, const CUtensorMap& ma, const CUten
 // the GPU for the weight-gradient GEMMs, whose M x N is small and K = tokens.
 struct Shape {
   int bn, splits, kb_per_split;
+  bool pair;
 };
 
-Shape choose_shape(int64_t M, int64_t N, int64_t K, bool fp32_out, int cap) {
+// Tile shape: single-CTA 128 x BN or SM-pair 256 x BN (cta_group::2), BN in
+// {128, 256}, and a split-K factor (fp32 output only).  Each candidate is
+// scored by the fraction of the capped SMs kept busy across the persistent
+// rounds, times a per-shape efficiency (operand bytes per MMA: the pair tile
+// halves B traffic per SM; 128-wide tiles are smem-bandwidth bound).
+Shape choose_shape(int64_t M, int64_t N, int64_t K, bool fp32_out, int cap, int allow_pair) {
   const int64_t k_blocks = (K + BK - 1) / BK;
-  Shape best{256, 1, static_cast<int>(k_blocks)};
-  double best_eff = -1.0;
-  for (int bn : {256, 128}) {
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  Shape best{256, 1, static_cast<int>(k_blocks), false};
+  double best_score = -1.0;
+  struct Cand { bool pair; int bn; double weight; };
+  const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.88}, {false, 256, 0.8}, {false, 128, 0.7}};
+  for (const Cand& c : cands) {
+    if (c.pair && (!allow_pair || M < 256 || cap < 2)) continue;
+    const int64_t rows = c.pair ? 256 : 128;
+    const int64_t slots = c.pair ? cap / 2 : cap;
+    const int64_t tiles = ((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
     int64_t splits = 1;
-    if (fp32_out && tiles < cap && k_blocks >= 8) {
-      splits = std::min<int64_t>(cap / tiles, k_blocks / 4);
+    if (fp32_out && tiles < slots && k_blocks >= 8) {
+      splits = std::min<int64_t>(slots / tiles, k_blocks / 4);
       if (splits < 1) splits = 1;
     }
     const int64_t kps = (k_blocks + splits - 1) / splits;
     splits = (k_blocks + kps - 1) / kps;
     const int64_t work = tiles * splits;
-    const int64_t rounds = (work + cap - 1) / cap;
-    double eff = static_cast<double>(work) / static_cast<double>(rounds * cap);
-    if (bn == 128) eff *= 0.9;
-    if (splits > 1) eff *= 0.97;  // partial-sum traffic
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = {bn, static_cast<int>(splits), static_cast<int>(kps)};
+    const int64_t rounds = (work + slots - 1) / slots;
+    double score = static_cast<double>(work) / static_cast<double>(rounds * slots) * c.weight;
+    if (splits > 1) score *= 0.97;  // partial-sum traffic
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = {c.bn, static_cast<int>(splits), static_cast<int>(kps), c.pair};
     }
   }
   return best;
@@ -543,6 +933,22 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const Tin* __restrict__ 
 
 namespace {
 
+int tma_epilogue() {
+  static int mode = [] {
+    const char* v = getenv("HAP_GEMM_TMA_EPI");
+    return v ? atoi(v) : 1;
+  }();
+  return mode;
+}
+
+int pair_mode() {
+  static int mode = [] {
+    const char* v = getenv("HAP_GEMM_PAIR");
+    return v ? atoi(v) : 1;
+  }();
+  return mode;
+}
+
 bool tc_eligible(const void* A, int64_t lda, int transA, const void* B, int64_t ldb, int transB,
                  int64_t M, int64_t N, int64_t K, hap_dtype in_dtype) {
   if (in_dtype != HAP_BF16) return false;
@@ -599,30 +1005,53 @@ extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const v
   HAP_CHECK_ARG(A != nullptr && B != nullptr, "hap_matmul: null operand");
   if (tc_eligible(A, lda, transA, B, ldb, transB, M, N, K, in_dtype)) {
     const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
-    const tc::Shape shp = tc::choose_shape(M, N, K, out_dtype == HAP_F32, cap);
+    const tc::Shape shp = tc::choose_shape(M, N, K, out_dtype == HAP_F32, cap, pair_mode());
     const int BN = shp.bn;
+    const int b_box = shp.pair ? BN / 2 : BN;   // B columns one CTA stages (K-major box)
     CUtensorMap ma, mb;
     bool ok = transA ? tc::make_map(&ma, A, M, K, lda, tc::BK)
                      : tc::make_map(&ma, A, K, M, lda, tc::BM);
-    ok = ok && (transB ? tc::make_map(&mb, B, K, N, ldb, BN) : tc::make_map(&mb, B, N, K, ldb, tc::BK));
+    ok = ok && (transB ? tc::make_map(&mb, B, K, N, ldb, b_box) : tc::make_map(&mb, B, N, K, ldb, tc::BK));
     HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout");
     const bool amn = transA != 0, bmn = transB == 0;
     const size_t osz = dtype_size(out_dtype);
     const int vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * osz) % 16 == 0);
     const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
     const int sp = shp.splits, kps = shp.kb_per_split;
+    // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
+    // accumulation and split-K partials use TMA reduce-add; a bf16
+    // accumulate (read-modify-round) stays on per-thread stores.
+    CUtensorMap mc;
+    int mode = tc::EPI_DIRECT;
+    const bool fp32 = out_dtype == HAP_F32;
+    if (vec && tma_epilogue() && (!accumulate || fp32) && tc::make_map_c(&mc, C, out_dtype, N, M, ldc))
+      mode = (fp32 && (accumulate || sp > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
+    if (mode == tc::EPI_DIRECT) std::memset(&mc, 0, sizeof(mc));
+    if (shp.pair) {
+      if (out_dtype == HAP_BF16)
+        return BN == 256 ? tc::dispatch_major2<256, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate,
+                                                                   vec, sm_cap, 1, kps, stream)
+                         : tc::dispatch_major2<128, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate,
+                                                                   vec, sm_cap, 1, kps, stream);
+      if (sp > 1 && !accumulate)
+        HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, stream));
+      return BN == 256 ? tc::dispatch_major2<256, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate, vec,
+                                                         sm_cap, sp, kps, stream)
+                       : tc::dispatch_major2<128, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate, vec,
+                                                         sm_cap, sp, kps, stream);
+    }
     if (out_dtype == HAP_BF16) {
       return BN == 256
-                 ? tc::dispatch_major<256, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                 ? tc::dispatch_major<256, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
                                                           accumulate, vec, sm_cap, 1, kps, stream)
-                 : tc::dispatch_major<128, __nv_bfloat16>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                 : tc::dispatch_major<128, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
                                                           accumulate, vec, sm_cap, 1, kps, stream);
     }
     if (sp > 1 && !accumulate)  // split-K partials add into a zeroed output
       HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, stream));
-    return BN == 256 ? tc::dispatch_major<256, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
+    return BN == 256 ? tc::dispatch_major<256, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
                                                       accumulate, vec, sm_cap, sp, kps, stream)
-                     : tc::dispatch_major<128, float>(amn, bmn, ma, mb, C, ldc, m, n, k,
+                     : tc::dispatch_major<128, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
                                                       accumulate, vec, sm_cap, sp, kps, stream);
   }
   return HAP_DISPATCH_IO(in_dtype, out_dtype, [&] {
