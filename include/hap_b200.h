@@ -113,6 +113,14 @@ hap_status hap_fill(void* y, hap_dtype y_dtype, float value, int64_t n, void* st
 hap_status hap_sgd(float* master, const float* grad, void* weight, hap_dtype w_dtype, float lr,
                    int64_t n, int sm_cap, void* stream);
 
+/* Multi-tensor SGD in one launch.  `tensors` is a DEVICE array of `count`
+ * records {float* master; const float* grad; void* weight; int64_t n;
+ * int64_t first_chunk;} (40 bytes each), where first_chunk is the prefix sum
+ * of ceil(n / 8192) over the preceding records and total_chunks the sum over
+ * all of them. */
+hap_status hap_sgd_multi(const void* tensors, int count, int64_t total_chunks, hap_dtype w_dtype, float lr,
+                         int sm_cap, void* stream);
+
 /* ---- collectives (NCCL over NVLink / NVSwitch) ---------------------------
  * One communicator per process (rank = device index of the program).  The
  * 128-byte unique id is created on rank 0 and broadcast by the host. */

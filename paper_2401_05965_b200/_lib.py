@@ -44,6 +44,7 @@ SIGNATURES = {
     "hap_axpy": (c_int, [c_float, _P, c_int, _P, c_int, c_int64, c_int, c_int, _P]),
     "hap_fill": (c_int, [_P, c_int, c_float, c_int64, _P]),
     "hap_sgd": (c_int, [_P, _P, _P, c_int, c_float, c_int64, c_int, _P]),
+    "hap_sgd_multi": (c_int, [_P, c_int, c_int64, c_int, c_float, c_int, _P]),
     "hap_nccl_version": (c_int, []),
     "hap_comm_unique_id": (c_int, [ctypes.c_char_p]),
     "hap_comm_init": (c_int, [POINTER(c_void_p), ctypes.c_char_p, c_int, c_int]),

@@ -13,6 +13,7 @@ namespace hap {
 namespace {
 
 constexpr int kBlock = 1024;
+constexpr int kUnroll = 4;   // independent 16-byte vectors in flight per thread
 
 __device__ __forceinline__ float unary_fwd(int tag, float x) {
   switch (tag) {
@@ -81,12 +82,18 @@ __global__ void __launch_bounds__(kBlock) unary_kernel(int tag, const Tin* __res
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vec) {
     const int64_t nv = n / 8;
-    for (int64_t i = tid; i < nv; i += stride) {
-      float v[8];
-      Vec8<Tin>::load(x + 8 * i, v);
+    for (int64_t base = tid; base < nv; base += kUnroll * stride) {
+      float v[kUnroll][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = unary_fwd(tag, v[j]);
-      Vec8<Tout>::store(y + 8 * i, v);
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + u * stride < nv) Vec8<Tin>::load(x + 8 * (base + u * stride), v[u]);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (base + u * stride >= nv) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[u][j] = unary_fwd(tag, v[u][j]);
+        Vec8<Tout>::store(y + 8 * (base + u * stride), v[u]);
+      }
     }
     for (int64_t i = nv * 8 + tid; i < n; i += stride) y[i] = from_f32<Tout>(unary_fwd(tag, to_f32(x[i])));
   } else {
@@ -104,20 +111,25 @@ __global__ void __launch_bounds__(kBlock)
   if (vec) {  // x / y only read when the derivative needs them
     const int64_t nv = n / 8;
     const bool need_x = tag == HAP_RELU, need_y = tag != HAP_RELU && tag != HAP_NEG;
-    for (int64_t i = tid; i < nv; i += stride) {
-      float xv[8] = {}, yv[8] = {}, g[8];
-      if (need_x) Vec8<Txy>::load(x + 8 * i, xv);
-      if (need_y) Vec8<Txy>::load(y + 8 * i, yv);
-      Vec8<Tdy>::load(dy + 8 * i, g);
+    for (int64_t base = tid; base < nv; base += kUnroll * stride) {
+      float xv[kUnroll][8] = {}, yv[kUnroll][8] = {}, g[kUnroll][8], o[kUnroll][8] = {};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] *= unary_deriv(tag, xv[j], yv[j]);
-      if (accumulate) {
-        float o[8];
-        Vec8<Tdx>::load(dx + 8 * i, o);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) g[j] += o[j];
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+        if (need_x) Vec8<Txy>::load(x + 8 * i, xv[u]);
+        if (need_y) Vec8<Txy>::load(y + 8 * i, yv[u]);
+        Vec8<Tdy>::load(dy + 8 * i, g[u]);
+        if (accumulate) Vec8<Tdx>::load(dx + 8 * i, o[u]);
       }
-      Vec8<Tdx>::store(dx + 8 * i, g);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[u][j] = g[u][j] * unary_deriv(tag, xv[u][j], yv[u][j]) + o[u][j];
+        Vec8<Tdx>::store(dx + 8 * i, g[u]);
+      }
     }
     start = nv * 8;
   }
@@ -140,13 +152,23 @@ __global__ void __launch_bounds__(kBlock) binary_kernel(int tag, const Tin* __re
   int64_t start = 0;
   if (vec) {
     const int64_t nv = n / 8;
-    for (int64_t i = tid; i < nv; i += stride) {
-      float va[8], vb[8];
-      Vec8<Tin>::load(a + 8 * i, va);
-      Vec8<Tin>::load(b + 8 * i, vb);
+    for (int64_t base = tid; base < nv; base += kUnroll * stride) {
+      float va[kUnroll][8], vb[kUnroll][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) va[j] = tag == HAP_ADD ? va[j] + vb[j] : va[j] * vb[j];
-      Vec8<Tout>::store(out + 8 * i, va);
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+        Vec8<Tin>::load(a + 8 * i, va[u]);
+        Vec8<Tin>::load(b + 8 * i, vb[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) va[u][j] = tag == HAP_ADD ? va[u][j] + vb[u][j] : va[u][j] * vb[u][j];
+        Vec8<Tout>::store(out + 8 * i, va[u]);
+      }
     }
     start = nv * 8;
   }
@@ -166,6 +188,7 @@ __global__ void __launch_bounds__(kBlock)
   int64_t start = 0;
   if (vec) {
     const int64_t nv = n / 8;
+#pragma unroll 2
     for (int64_t i = tid; i < nv; i += stride) {
       float va[8], vb[8], g[8], ga[8], gb[8];
       Vec8<Tin>::load(a + 8 * i, va);
@@ -224,19 +247,23 @@ __global__ void __launch_bounds__(kBlock)
   int64_t start = 0;
   if (vec) {
     const int64_t nv = n / 8;
-    for (int64_t i = tid; i < nv; i += stride) {
-      float v[8];
-      Vec8<Tin>::load(x + 8 * i, v);
-      if (accumulate) {
-        float o[8];
-        Vec8<Tout>::load(y + 8 * i, o);
+    for (int64_t base = tid; base < nv; base += kUnroll * stride) {
+      float v[kUnroll][8], o[kUnroll][8] = {};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = o[j] + alpha * v[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] *= alpha;
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+        Vec8<Tin>::load(x + 8 * i, v[u]);
+        if (accumulate) Vec8<Tout>::load(y + 8 * i, o[u]);
       }
-      Vec8<Tout>::store(y + 8 * i, v);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= nv) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[u][j] = o[u][j] + alpha * v[u][j];
+        Vec8<Tout>::store(y + 8 * i, v[u]);
+      }
     }
     start = nv * 8;
   }
@@ -286,8 +313,52 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Multi-tensor SGD: one launch updates every parameter tensor of the step.
+// Work is split into 8192-element chunks; chunk c belongs to the tensor whose
+// prefix range contains it (binary search over the chunk offsets).
+struct SgdTensor {
+  float* master;
+  const float* grad;
+  void* weight;
+  int64_t n;
+  int64_t first_chunk;
+};
+
 template <typename T>
-using cptr = const T*;
+__global__ void __launch_bounds__(kBlock) sgd_multi_kernel(const SgdTensor* __restrict__ ts, int count,
+                                                           int64_t total_chunks, float lr) {
+  constexpr int64_t kChunk = 8192;
+  for (int64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
+    int lo = 0, hi = count - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ts[mid].first_chunk <= c) lo = mid; else hi = mid - 1;
+    }
+    const SgdTensor t = ts[lo];
+    const int64_t start = (c - t.first_chunk) * kChunk;
+    const int64_t end = start + kChunk < t.n ? start + kChunk : t.n;
+    T* w = static_cast<T*>(t.weight);
+    const bool vec = ((reinterpret_cast<uintptr_t>(t.master) | reinterpret_cast<uintptr_t>(t.grad) |
+                       reinterpret_cast<uintptr_t>(w)) & 15) == 0 && (t.n % 8 == 0);
+    if (vec) {
+      for (int64_t i = start + 8 * threadIdx.x; i < end; i += 8 * blockDim.x) {
+        float m[8], g[8];
+        Vec8<float>::load(t.master + i, m);
+        Vec8<float>::load(t.grad + i, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] -= lr * g[j];
+        Vec8<float>::store(t.master + i, m);
+        Vec8<T>::store(w + i, m);
+      }
+    } else {
+      for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
+        const float v = t.master[i] - lr * t.grad[i];
+        t.master[i] = v;
+        w[i] = from_f32<T>(v);
+      }
+    }
+  }
+}
 
 }  // namespace
 }  // namespace hap
@@ -425,4 +496,17 @@ extern "C" hap_status hap_sgd(float* master, const float* grad, void* w, hap_dty
     sgd_kernel<float><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(master, grad,
                                                                   static_cast<float*>(w), lr, n);
   return launch_status("sgd_kernel");
+}
+
+extern "C" hap_status hap_sgd_multi(const void* tensors, int count, int64_t total_chunks, hap_dtype wd,
+                                    float lr, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (count <= 0 || total_chunks <= 0) return HAP_OK;
+  const SgdTensor* ts = static_cast<const SgdTensor*>(tensors);
+  const int grid = capped_grid(total_chunks, sm_cap);
+  if (wd == HAP_BF16)
+    sgd_multi_kernel<__nv_bfloat16><<<grid, kBlock, 0, stream>>>(ts, count, total_chunks, lr);
+  else
+    sgd_multi_kernel<float><<<grid, kBlock, 0, stream>>>(ts, count, total_chunks, lr);
+  return launch_status("sgd_multi_kernel");
 }

@@ -84,19 +84,24 @@ class LocalGroup:
 
 
 class NcclGroup:
-    """One program device per process; collectives over NCCL (C ABI)."""
+    """One program device per process; collectives over NCCL (C ABI).
 
-    def __init__(self, rank: int, m: int, comm_handle):
+    Two communicators: ``comm`` carries the program's collectives on the
+    compute stream, ``comm_grad`` the parameter-gradient all-reduces on a side
+    stream that overlaps the rest of the backward pass (NCCL operations on
+    one communicator must not run concurrently from two streams)."""
+
+    def __init__(self, rank: int, m: int, comm_handle, grad_handle=None):
         self.m = m
         self.rank = rank
         self.local_ranks = [rank]
         self.comm = comm_handle
+        self.comm_grad = grad_handle
 
-    @classmethod
-    def from_torch_distributed(cls) -> "NcclGroup":
+    @staticmethod
+    def _init_comm(rank: int, world: int):
         import torch.distributed as dist
 
-        rank, world = dist.get_rank(), dist.get_world_size()
         uid = ctypes.create_string_buffer(128)
         if rank == 0:
             check(_lib.lib().hap_comm_unique_id(uid), "hap_comm_unique_id")
@@ -104,12 +109,21 @@ class NcclGroup:
         dist.broadcast_object_list(obj, src=0)
         handle = ctypes.c_void_p()
         check(_lib.lib().hap_comm_init(ctypes.byref(handle), obj[0], world, rank), "hap_comm_init")
-        return cls(rank, world, handle)
+        return handle
+
+    @classmethod
+    def from_torch_distributed(cls) -> "NcclGroup":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        return cls(rank, world, cls._init_comm(rank, world), cls._init_comm(rank, world))
 
     def close(self):
-        if self.comm is not None:
-            check(_lib.lib().hap_comm_destroy(self.comm), "hap_comm_destroy")
-            self.comm = None
+        for name in ("comm", "comm_grad"):
+            handle = getattr(self, name)
+            if handle is not None:
+                check(_lib.lib().hap_comm_destroy(handle), "hap_comm_destroy")
+                setattr(self, name, None)
 
 
 # ---------------------------------------------------------------------------- config
@@ -166,6 +180,11 @@ class Executor:
         self.sync_choice: dict[str, str] = {}
         self.graph: torch.cuda.CUDAGraph | None = None
         self._pool: list[Buf] = []
+        self.sfb: dict = {}
+        self.sfb_done: set = set()
+        self.overlapped: set = set()
+        self._grad_ready_at: dict = {}
+        self.comm_stream = None
         self.bytes_allocated = 0
         self.source_dids = {i.output for i in program.instrs if i.kind in SOURCE_KINDS}
         self._check_program()
@@ -590,6 +609,8 @@ class Executor:
         written.add(seed_did)
 
         self._plan_sfb()
+        self._grad_ready_at: dict = {}
+        self.overlapped: set = set()
         for ins in reversed(self.program.instrs):
             if ins.output not in written or ins.kind in SOURCE_KINDS:
                 continue
@@ -597,6 +618,10 @@ class Executor:
             if not any(need):
                 continue
             self._adjoint(ins, need, contrib)
+            for d in ins.operands:
+                if d in self.source_dids:
+                    self._grad_ready_at[d] = len(self._ops)
+        self._overlap_grad_sync()
         self._finish_update(written)
 
     def _adjoint(self, ins: Instruction, need: list, contrib):
@@ -778,6 +803,46 @@ class Executor:
         for r in L:
             self._gemm(xfull[r], True, yfull[r], False, self._grad(w, r), self.caps[r], acc)
 
+    def _overlap_grad_sync(self):
+        """NCCL groups: all-reduce each replicated parameter's gradient on a
+        side stream as soon as its last contribution is enqueued, so the
+        transfer overlaps the remaining backward kernels; the compute stream
+        joins the side stream before the update."""
+        g = self.group
+        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None:
+            return
+        forms: dict = {}
+        for ins in self.program.instrs:
+            if ins.kind.startswith("parameter") or (self.cfg.input_grads and ins.kind.startswith("placeholder")):
+                forms.setdefault(ins.ref, []).append(ins)
+        plan = []
+        for ref, fs in forms.items():
+            f = fs[0]
+            if len(fs) != 1 or f.kind not in ("parameter", "placeholder") or f.output in self.sfb_done:
+                continue
+            if f.output not in self._grad_ready_at:
+                continue
+            plan.append((self._grad_ready_at[f.output], f.output))
+        if not plan:
+            return
+        self.comm_stream = torch.cuda.Stream(self.device)
+        r = g.rank
+        ops = self.ops_bwd
+        for pos, did in sorted(plan, reverse=True):
+            gb = self.grads[(did, r)]
+            ev = torch.cuda.Event()
+            self._keep(ev)
+            inserted = [Op(ev.record, (self.stream,), "event.record", False),
+                        Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False),
+                        Op(self.lib.hap_all_reduce, (g.comm_grad, gb.ptr, gb.ptr, gb.numel, gb.dtype,
+                                                     self.comm_stream.cuda_stream), "hap_all_reduce", False)]
+            ops[pos:pos] = inserted
+            self.overlapped.add(did)
+        done = torch.cuda.Event()
+        self._keep(done)
+        ops.append(Op(done.record, (self.comm_stream,), "event.record", False))
+        ops.append(Op(self.stream.wait_event, (done,), "stream.wait_event", False))
+
     def _finish_update(self, written: set):
         """Turn per-device parameter gradients into true gradients and apply SGD.
 
@@ -798,7 +863,8 @@ class Executor:
             if len(fs) == 1:
                 f = fs[0]
                 g = {r: self.grads[(f.output, r)] for r in L}
-                if f.kind in ("parameter", "placeholder") and f.output not in sfb_done and self.m > 1:
+                if (f.kind in ("parameter", "placeholder") and f.output not in sfb_done and self.m > 1
+                        and f.output not in self.overlapped):
                     self._coll_all_reduce(g, g, 0)
                 for r in L:
                     self.param_grads[(f.output, r)] = g[r]
@@ -836,12 +902,28 @@ class Executor:
                             self.param_grads[(f.output, r)] = fullg[r]
         self._ops = self.ops_upd = []
         if self.cfg.lr:
-            for (did, r), g in self.param_grads.items():
-                if (did, r) not in self.masters:
-                    continue
-                mst, wb = self.masters[(did, r)], self.bufs[(did, r)]
-                self._emit("hap_sgd", mst.ptr, g.ptr, wb.ptr, wb.dtype, float(self.cfg.lr), mst.numel,
-                           self.caps[r], self._sptr())
+            self._compile_sgd()
+
+    def _compile_sgd(self):
+        """One multi-tensor SGD launch per local device and weight dtype: a
+        device table of {master, grad, weight, n, first_chunk} records."""
+        import struct
+
+        groups: dict = {}
+        for (did, r), g in self.param_grads.items():
+            if (did, r) not in self.masters:
+                continue
+            mst, wb = self.masters[(did, r)], self.bufs[(did, r)]
+            groups.setdefault((r, wb.dtype), []).append((mst, g, wb))
+        for (r, wdt), items in sorted(groups.items()):
+            records, chunk = bytearray(), 0
+            for mst, g, wb in items:
+                records += struct.pack("<QQQqq", mst.ptr, g.ptr, wb.ptr, mst.numel, chunk)
+                chunk += (mst.numel + 8191) // 8192
+            table = torch.frombuffer(bytes(records), dtype=torch.uint8).to(self.device)
+            self._keep(table)
+            self._emit("hap_sgd_multi", table.data_ptr(), len(items), chunk, wdt, float(self.cfg.lr),
+                       self.caps[r], self._sptr())
 
     # ------------------------------------------------------------------ binding
     def load(self, inputs: dict):

@@ -167,3 +167,22 @@ def test_copy_block_strided_shards():
     torch.cuda.synchronize()
     assert torch.equal(dst[:, 1:4].float(), src[:, 5:8].to(torch.bfloat16).float())
     assert dst[:, 0].abs().max().item() == 0
+
+
+def test_sgd_multi_tensor():
+    import struct
+    torch.manual_seed(7)
+    sizes = [1000, 8192 * 3 + 5, 16, 70000]
+    masters = [torch.randn(n, device=DEV) for n in sizes]
+    grads = [torch.randn(n, device=DEV) for n in sizes]
+    weights = [torch.empty(n, device=DEV, dtype=torch.bfloat16) for n in sizes]
+    want = [m - 0.5 * g for m, g in zip(masters, grads)]
+    rec, chunk = bytearray(), 0
+    for m, g, w in zip(masters, grads, weights):
+        rec += struct.pack("<QQQqq", m.data_ptr(), g.data_ptr(), w.data_ptr(), m.numel(), chunk)
+        chunk += (m.numel() + 8191) // 8192
+    table = torch.frombuffer(bytes(rec), dtype=torch.uint8).to(DEV)
+    check(L.hap_sgd_multi(table.data_ptr(), len(sizes), chunk, BF16, 0.5, 0, S))
+    torch.cuda.synchronize()
+    for m, w, ref in zip(masters, weights, want):
+        assert torch.allclose(m, ref) and torch.equal(w, ref.to(torch.bfloat16))

@@ -31,7 +31,7 @@ def launches(src: str, dst: str) -> None:
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in data:
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         k = _kernel(r[ki])
         tot[k] += v
         cnt[k] += 1
