@@ -7,13 +7,15 @@
 //   elemwise_binary  reference interpreter.py:144-148
 //   identity         reference interpreter.py:151-152 (a copy / axpy)
 //   *_shard slicing  reference interpreter.py:81-91, 135-138 (copy_block)
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace hap {
 namespace {
 
 constexpr int kBlock = 1024;
-constexpr int kUnroll = 4;   // independent 16-byte vectors in flight per thread
+constexpr int kUnroll = 2;   // independent 16-byte vectors in flight per thread
 
 __device__ __forceinline__ float unary_fwd(int tag, float x) {
   switch (tag) {
@@ -75,9 +77,9 @@ inline int grid_for(int64_t n, int sm_cap) {
 }
 
 // ---------------------------------------------------------------- unary
-template <typename Tin, typename Tout>
-__global__ void __launch_bounds__(kBlock) unary_kernel(int tag, const Tin* __restrict__ x,
-                                                       Tout* __restrict__ y, int64_t n, int vec) {
+template <int tag, typename Tin, typename Tout>
+__global__ void __launch_bounds__(kBlock) unary_kernel(const Tin* __restrict__ x, Tout* __restrict__ y,
+                                                       int64_t n, int vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vec) {
@@ -101,10 +103,10 @@ __global__ void __launch_bounds__(kBlock) unary_kernel(int tag, const Tin* __res
   }
 }
 
-template <typename Txy, typename Tdy, typename Tdx>
+template <int tag, typename Txy, typename Tdy, typename Tdx>
 __global__ void __launch_bounds__(kBlock)
-    unary_grad_kernel(int tag, const Txy* __restrict__ x, const Txy* __restrict__ y,
-                      const Tdy* __restrict__ dy, Tdx* dx, int64_t n, int accumulate, int vec) {
+    unary_grad_kernel(const Txy* __restrict__ x, const Txy* __restrict__ y, const Tdy* __restrict__ dy,
+                      Tdx* dx, int64_t n, int accumulate, int vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t start = 0;
@@ -374,8 +376,18 @@ extern "C" hap_status hap_unary(int tag, const void* x, hap_dtype xd, void* y, h
   if (n <= 0) return HAP_OK;
   const int vec = aligned16(x) && aligned16(y);
   return HAP_DISPATCH_IO(xd, yd, [&] {
-    unary_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
-        tag, static_cast<const Tin*>(x), static_cast<Tout*>(y), n, vec);
+    auto go = [&](auto tag_c) {
+      constexpr int T = decltype(tag_c)::value;
+      unary_kernel<T, Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+          static_cast<const Tin*>(x), static_cast<Tout*>(y), n, vec);
+    };
+    switch (tag) {
+      case HAP_EXP: go(std::integral_constant<int, HAP_EXP>{}); break;
+      case HAP_NEG: go(std::integral_constant<int, HAP_NEG>{}); break;
+      case HAP_RELU: go(std::integral_constant<int, HAP_RELU>{}); break;
+      case HAP_SIGMOID: go(std::integral_constant<int, HAP_SIGMOID>{}); break;
+      default: go(std::integral_constant<int, HAP_TANH>{}); break;
+    }
     return launch_status("unary_kernel");
   });
 }
@@ -390,14 +402,24 @@ extern "C" hap_status hap_unary_grad(int tag, const void* x, const void* y, hap_
                 "hap_unary_grad: missing saved activation");
   const int vec = (!x || aligned16(x)) && (!y || aligned16(y)) && aligned16(dy) && aligned16(dx);
   return HAP_DISPATCH_IO(xyd, dxd, [&] {
-    if (dyd == HAP_BF16)
-      unary_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
-          tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
-          static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(dx), n, accumulate, vec);
-    else
-      unary_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
-          tag, static_cast<const Tin*>(x), static_cast<const Tin*>(y),
-          static_cast<const float*>(dy), static_cast<Tout*>(dx), n, accumulate, vec);
+    auto go = [&](auto tag_c) {
+      constexpr int T = decltype(tag_c)::value;
+      if (dyd == HAP_BF16)
+        unary_grad_kernel<T, Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+            static_cast<const Tin*>(x), static_cast<const Tin*>(y), static_cast<const __nv_bfloat16*>(dy),
+            static_cast<Tout*>(dx), n, accumulate, vec);
+      else
+        unary_grad_kernel<T, Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+            static_cast<const Tin*>(x), static_cast<const Tin*>(y), static_cast<const float*>(dy),
+            static_cast<Tout*>(dx), n, accumulate, vec);
+    };
+    switch (tag) {
+      case HAP_EXP: go(std::integral_constant<int, HAP_EXP>{}); break;
+      case HAP_NEG: go(std::integral_constant<int, HAP_NEG>{}); break;
+      case HAP_RELU: go(std::integral_constant<int, HAP_RELU>{}); break;
+      case HAP_SIGMOID: go(std::integral_constant<int, HAP_SIGMOID>{}); break;
+      default: go(std::integral_constant<int, HAP_TANH>{}); break;
+    }
     return launch_status("unary_grad_kernel");
   });
 }
