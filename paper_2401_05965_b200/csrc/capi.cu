@@ -1,4 +1,5 @@
 // Library-level entry points: error reporting, version, device queries.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -8,6 +9,14 @@ namespace hap {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+int pdl_enabled() {
+  static int on = [] {
+    const char* v = getenv("HAP_PDL");
+    return v ? atoi(v) : 1;
+  }();
+  return on;
+}
 
 int sm_count() {
   static int cached[64] = {0};

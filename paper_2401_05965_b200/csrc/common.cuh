@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/hap_b200.h"
 
@@ -51,6 +52,36 @@ inline int capped_grid(int64_t work_blocks, int sm_cap) {
   if (cap > sm_count()) cap = sm_count();
   int64_t g = work_blocks < cap ? work_blocks : cap;
   return g < 1 ? 1 : static_cast<int>(g);
+}
+
+// Programmatic dependent launch (PDL): every kernel is launched with
+// programmatic stream serialisation, so the next kernel in the stream (or
+// CUDA graph) is scheduled while this one drains; each kernel first waits for
+// its predecessor's memory (griddepcontrol.wait) and then immediately lets its
+// own successor start launching.  Setup that touches no global memory (smem
+// barriers, TMEM allocation, descriptor prefetch) runs before the wait and so
+// overlaps the previous kernel's tail.  HAP_PDL=0 disables it.
+int pdl_enabled();
+
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ float to_f32(float v) { return v; }

@@ -80,6 +80,7 @@ inline int grid_for(int64_t n, int sm_cap) {
 template <int tag, typename Tin, typename Tout>
 __global__ void __launch_bounds__(kBlock) unary_kernel(const Tin* __restrict__ x, Tout* __restrict__ y,
                                                        int64_t n, int vec) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (vec) {
@@ -107,6 +108,7 @@ template <int tag, typename Txy, typename Tdy, typename Tdx>
 __global__ void __launch_bounds__(kBlock)
     unary_grad_kernel(const Txy* __restrict__ x, const Txy* __restrict__ y, const Tdy* __restrict__ dy,
                       Tdx* dx, int64_t n, int accumulate, int vec) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t start = 0;
@@ -149,6 +151,7 @@ template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kBlock) binary_kernel(int tag, const Tin* __restrict__ a,
                                                         const Tin* __restrict__ b,
                                                         Tout* __restrict__ out, int64_t n, int vec) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t start = 0;
@@ -184,6 +187,7 @@ template <typename Tin, typename Tdy, typename Td>
 __global__ void __launch_bounds__(kBlock)
     mul_grad_kernel(const Tin* __restrict__ a, const Tin* __restrict__ b, const Tdy* __restrict__ dy,
                     Td* da, Td* db, int64_t n, int accumulate, int vec) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool same = da == db;
@@ -244,6 +248,7 @@ __global__ void __launch_bounds__(kBlock)
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kBlock)
     axpy_kernel(float alpha, const Tin* __restrict__ x, Tout* y, int64_t n, int accumulate, int vec) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int64_t start = 0;
@@ -282,6 +287,7 @@ __global__ void __launch_bounds__(kBlock)
     copy_block_kernel(const Tin* __restrict__ src, int64_t src_extent, int64_t src_off, Tout* dst,
                       int64_t dst_extent, int64_t dst_off, int64_t outer, int64_t count,
                       int64_t inner, int accumulate) {
+  hap::pdl_enter();
   const int64_t per_outer = count * inner;
   const int64_t total = outer * per_outer;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(kBlock)
 
 template <typename T>
 __global__ void fill_kernel(T* y, float value, int64_t n) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     y[i] = from_f32<T>(value);
@@ -307,6 +314,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
     sgd_kernel(float* __restrict__ master, const float* __restrict__ grad, T* __restrict__ w,
                float lr, int64_t n) {
+  hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const float v = master[i] - lr * grad[i];
@@ -329,6 +337,7 @@ struct SgdTensor {
 template <typename T>
 __global__ void __launch_bounds__(kBlock) sgd_multi_kernel(const SgdTensor* __restrict__ ts, int count,
                                                            int64_t total_chunks, float lr) {
+  hap::pdl_enter();
   constexpr int64_t kChunk = 8192;
   for (int64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
     int lo = 0, hi = count - 1;
@@ -378,7 +387,7 @@ extern "C" hap_status hap_unary(int tag, const void* x, hap_dtype xd, void* y, h
   return HAP_DISPATCH_IO(xd, yd, [&] {
     auto go = [&](auto tag_c) {
       constexpr int T = decltype(tag_c)::value;
-      unary_kernel<T, Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+      hap::launch_k(unary_kernel<T, Tin, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
           static_cast<const Tin*>(x), static_cast<Tout*>(y), n, vec);
     };
     switch (tag) {
@@ -405,11 +414,11 @@ extern "C" hap_status hap_unary_grad(int tag, const void* x, const void* y, hap_
     auto go = [&](auto tag_c) {
       constexpr int T = decltype(tag_c)::value;
       if (dyd == HAP_BF16)
-        unary_grad_kernel<T, Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        hap::launch_k(unary_grad_kernel<T, Tin, __nv_bfloat16, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
             static_cast<const Tin*>(x), static_cast<const Tin*>(y), static_cast<const __nv_bfloat16*>(dy),
             static_cast<Tout*>(dx), n, accumulate, vec);
       else
-        unary_grad_kernel<T, Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+        hap::launch_k(unary_grad_kernel<T, Tin, float, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
             static_cast<const Tin*>(x), static_cast<const Tin*>(y), static_cast<const float*>(dy),
             static_cast<Tout*>(dx), n, accumulate, vec);
     };
@@ -431,7 +440,7 @@ extern "C" hap_status hap_binary(int tag, const void* a, const void* b, hap_dtyp
   if (n <= 0) return HAP_OK;
   const int vec = aligned16(a) && aligned16(b) && aligned16(out);
   return HAP_DISPATCH_IO(ind, outd, [&] {
-    binary_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+    hap::launch_k(binary_kernel<Tin, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
         tag, static_cast<const Tin*>(a), static_cast<const Tin*>(b), static_cast<Tout*>(out), n, vec);
     return launch_status("binary_kernel");
   });
@@ -446,12 +455,12 @@ extern "C" hap_status hap_mul_grad(const void* a, const void* b, hap_dtype ind, 
                   (!db || aligned16(db));
   return HAP_DISPATCH_IO(ind, dd, [&] {
     if (dyd == HAP_BF16)
-      mul_grad_kernel<Tin, __nv_bfloat16, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+      hap::launch_k(mul_grad_kernel<Tin, __nv_bfloat16, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
           static_cast<const Tin*>(a), static_cast<const Tin*>(b),
           static_cast<const __nv_bfloat16*>(dy), static_cast<Tout*>(da), static_cast<Tout*>(db), n,
           accumulate, vec);
     else
-      mul_grad_kernel<Tin, float, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+      hap::launch_k(mul_grad_kernel<Tin, float, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
           static_cast<const Tin*>(a), static_cast<const Tin*>(b), static_cast<const float*>(dy),
           static_cast<Tout*>(da), static_cast<Tout*>(db), n, accumulate, vec);
     return launch_status("mul_grad_kernel");
@@ -464,7 +473,7 @@ extern "C" hap_status hap_axpy(float alpha, const void* x, hap_dtype xd, void* y
   if (n <= 0) return HAP_OK;
   const int vec = aligned16(x) && aligned16(y);
   return HAP_DISPATCH_IO(xd, yd, [&] {
-    axpy_kernel<Tin, Tout><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+    hap::launch_k(axpy_kernel<Tin, Tout>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
         alpha, static_cast<const Tin*>(x), static_cast<Tout*>(y), n, accumulate, vec);
     return launch_status("axpy_kernel");
   });
@@ -489,7 +498,7 @@ extern "C" hap_status hap_copy_block(const void* src, hap_dtype sd, int64_t src_
     return HAP_OK;
   }
   return HAP_DISPATCH_IO(sd, dd, [&] {
-    copy_block_kernel<Tin, Tout><<<grid_for(total, sm_cap), kBlock, 0, stream>>>(
+    hap::launch_k(copy_block_kernel<Tin, Tout>, dim3(grid_for(total, sm_cap)), dim3(kBlock), 0, stream, 
         static_cast<const Tin*>(src), src_extent, src_off, static_cast<Tout*>(dst), dst_extent,
         dst_off, outer, count, inner, accumulate);
     return launch_status("copy_block_kernel");
@@ -501,9 +510,9 @@ extern "C" hap_status hap_fill(void* y, hap_dtype yd, float value, int64_t n, vo
   if (n <= 0) return HAP_OK;
   const int grid = capped_grid((n + 1023) / 1024, 0);
   if (yd == HAP_BF16)
-    fill_kernel<__nv_bfloat16><<<grid, 1024, 0, stream>>>(static_cast<__nv_bfloat16*>(y), value, n);
+    hap::launch_k(fill_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream, static_cast<__nv_bfloat16*>(y), value, n);
   else
-    fill_kernel<float><<<grid, 1024, 0, stream>>>(static_cast<float*>(y), value, n);
+    hap::launch_k(fill_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<float*>(y), value, n);
   return launch_status("fill_kernel");
 }
 
@@ -512,10 +521,10 @@ extern "C" hap_status hap_sgd(float* master, const float* grad, void* w, hap_dty
   HAP_STREAM;
   if (n <= 0) return HAP_OK;
   if (wd == HAP_BF16)
-    sgd_kernel<__nv_bfloat16><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(
+    hap::launch_k(sgd_kernel<__nv_bfloat16>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, 
         master, grad, static_cast<__nv_bfloat16*>(w), lr, n);
   else
-    sgd_kernel<float><<<grid_for(n, sm_cap), kBlock, 0, stream>>>(master, grad,
+    hap::launch_k(sgd_kernel<float>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, master, grad,
                                                                   static_cast<float*>(w), lr, n);
   return launch_status("sgd_kernel");
 }
@@ -527,8 +536,8 @@ extern "C" hap_status hap_sgd_multi(const void* tensors, int count, int64_t tota
   const SgdTensor* ts = static_cast<const SgdTensor*>(tensors);
   const int grid = capped_grid(total_chunks, sm_cap);
   if (wd == HAP_BF16)
-    sgd_multi_kernel<__nv_bfloat16><<<grid, kBlock, 0, stream>>>(ts, count, total_chunks, lr);
+    hap::launch_k(sgd_multi_kernel<__nv_bfloat16>, dim3(grid), dim3(kBlock), 0, stream, ts, count, total_chunks, lr);
   else
-    sgd_multi_kernel<float><<<grid, kBlock, 0, stream>>>(ts, count, total_chunks, lr);
+    hap::launch_k(sgd_multi_kernel<float>, dim3(grid), dim3(kBlock), 0, stream, ts, count, total_chunks, lr);
   return launch_status("sgd_multi_kernel");
 }

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  hap::pdl_enter();   // everything above touched no global memory
 
   if (warp == 0) {
     if (lane == 0) {
@@ -600,6 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  hap::pdl_enter();   // everything above touched no global memory
 
   if (warp == 0) {
     if (lane == 0) {
@@ -769,7 +771,7 @@ hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMa
   }
   const int64_t tiles = static_cast<int64_t>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = capped_grid(tiles * splits, sm_cap);
-  kern<<<grid, kThreads, G::kSmem, stream>>>(ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K,
+  hap::launch_k(kern, dim3(grid), dim3(kThreads), G::kSmem, stream, ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K,
                                               accumulate, vec_ok, splits, kb_per_split, mode);
   return launch_status("gemm_tc_kernel");
 }
@@ -788,7 +790,7 @@ hap_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   const int64_t tiles = static_cast<int64_t>((M + 255) / 256) * ((N + BN - 1) / BN);
   const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
   int64_t pairs = std::min<int64_t>(tiles * splits, std::max(1, cap / 2));
-  kern<<<static_cast<int>(2 * pairs), kThreads, G::kSmem, stream>>>(
+  hap::launch_k(kern, dim3(static_cast<int>(2 * pairs)), dim3(kThreads), G::kSmem, stream, 
       ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K, accumulate, vec_ok, splits, kb_per_split, mode);
   return launch_status("gemm_tc2_kernel");
 }
@@ -873,6 +875,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const Tin* __restrict__ 
                                                         Tout* __restrict__ C, int64_t ldc,
                                                         int64_t M, int64_t N, int64_t K,
                                                         int accumulate) {
+  hap::pdl_enter();
   __shared__ float As[TK][TM + 1];
   __shared__ float Bs[TK][TN + 1];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -969,7 +972,7 @@ hap_status simt_launch(const void* A, int64_t lda, int transA, const void* B, in
                        int accumulate, int sm_cap, cudaStream_t stream) {
   const int64_t tiles = ((M + simt::TM - 1) / simt::TM) * ((N + simt::TN - 1) / simt::TN);
   const int grid = capped_grid(tiles, sm_cap > 0 ? sm_cap * 4 : sm_count() * 4);
-  simt::gemm_simt_kernel<Tin, Tout><<<grid, 256, 0, stream>>>(
+  hap::launch_k(simt::gemm_simt_kernel<Tin, Tout>, dim3(grid), dim3(256), 0, stream, 
       static_cast<const Tin*>(A), lda, transA, static_cast<const Tin*>(B), ldb, transB,
       static_cast<Tout*>(C), ldc, M, N, K, accumulate);
   return launch_status("gemm_simt_kernel");

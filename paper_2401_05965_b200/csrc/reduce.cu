@@ -62,6 +62,7 @@ __device__ __forceinline__ float block_sum(float v) {
 template <typename Tin>
 __global__ void __launch_bounds__(1024) sum_all_kernel(const Tin* __restrict__ x, int64_t n,
                                                        float* y) {
+  hap::pdl_enter();
   float acc = 0.f;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(1024) sum_all_kernel(const Tin* __restrict__ x
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(256) row_sum_kernel(const Tin* __restrict__ x, int64_t outer,
                                                       int64_t red, Tout* y, int accumulate) {
+  hap::pdl_enter();
   for (int64_t o = blockIdx.x; o < outer; o += gridDim.x) {
     float acc = 0.f;
     const Tin* row = x + o * red;
@@ -89,6 +91,7 @@ template <typename Tin>
 __global__ void __launch_bounds__(256) col_sum_kernel(const Tin* __restrict__ x, int64_t outer,
                                                       int64_t red, int64_t inner, int64_t chunk,
                                                       float* y) {
+  hap::pdl_enter();
   const int64_t i_tiles = (inner + 255) / 256;
   for (int64_t t = blockIdx.x; t < outer * i_tiles; t += gridDim.x) {
     const int64_t o = t / i_tiles;
@@ -113,6 +116,7 @@ struct Dims {
 template <typename Tin, typename Tout>
 __global__ void generic_reduce_kernel(const Tin* __restrict__ x, Dims d, int64_t n_out,
                                       int64_t n_red, Tout* y, int accumulate) {
+  hap::pdl_enter();
   int64_t strides[kMaxRank];
   int64_t s = 1;
   for (int a = d.rank - 1; a >= 0; --a) {
@@ -145,6 +149,7 @@ __global__ void generic_reduce_kernel(const Tin* __restrict__ x, Dims d, int64_t
 template <typename Tin, typename Tout>
 __global__ void unreduce_kernel(const Tin* __restrict__ dy, Dims d, Geometry g, int64_t n,
                                 Tout* dx, int accumulate) {
+  hap::pdl_enter();
   const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += step) {
     int64_t src;
@@ -198,15 +203,15 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
       if (mask & (1u << a)) n_red *= shape[a];
     }
     return HAP_DISPATCH_IO(xd, yd, [&] {
-      generic_reduce_kernel<Tin, Tout><<<capped_grid((n_out + 255) / 256, sm_cap), 256, 0, stream>>>(
+      hap::launch_k(generic_reduce_kernel<Tin, Tout>, dim3(capped_grid((n_out + 255) / 256, sm_cap)), dim3(256), 0, stream, 
           static_cast<const Tin*>(x), d, n_out, n_red, static_cast<Tout*>(y), accumulate);
       return launch_status("generic_reduce_kernel");
     });
   }
   if (g.inner == 1 && g.outer >= 64) {
     return HAP_DISPATCH_IO(xd, yd, [&] {
-      row_sum_kernel<Tin, Tout><<<capped_grid(g.outer, sm_cap > 0 ? 4 * sm_cap : 4 * sm_count()), 256, 0,
-                                  stream>>>(static_cast<const Tin*>(x), g.outer, g.red,
+      const int rows_grid = capped_grid(g.outer, sm_cap > 0 ? 4 * sm_cap : 4 * sm_count());
+      hap::launch_k(row_sum_kernel<Tin, Tout>, dim3(rows_grid), dim3(256), 0, stream, static_cast<const Tin*>(x), g.outer, g.red,
                                             static_cast<Tout*>(y), accumulate);
       return launch_status("row_sum_kernel");
     });
@@ -217,10 +222,10 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
   if (g.outer == 1 && g.inner == 1) {
     const int grid = capped_grid((g.red + 4095) / 4096, sm_cap);
     if (xd == HAP_BF16)
-      sum_all_kernel<__nv_bfloat16><<<grid, 1024, 0, stream>>>(
+      hap::launch_k(sum_all_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream, 
           static_cast<const __nv_bfloat16*>(x), g.red, static_cast<float*>(y));
     else
-      sum_all_kernel<float><<<grid, 1024, 0, stream>>>(static_cast<const float*>(x), g.red,
+      hap::launch_k(sum_all_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<const float*>(x), g.red,
                                                        static_cast<float*>(y));
     return launch_status("sum_all_kernel");
   }
@@ -230,10 +235,10 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
       const size_t xs = dtype_size(xd);
       const void* row = static_cast<const char*>(x) + o * g.red * xs;
       if (xd == HAP_BF16)
-        sum_all_kernel<__nv_bfloat16><<<grid, 1024, 0, stream>>>(
+        hap::launch_k(sum_all_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream, 
             static_cast<const __nv_bfloat16*>(row), g.red, static_cast<float*>(y) + o);
       else
-        sum_all_kernel<float><<<grid, 1024, 0, stream>>>(static_cast<const float*>(row), g.red,
+        hap::launch_k(sum_all_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<const float*>(row), g.red,
                                                          static_cast<float*>(y) + o);
     }
     return launch_status("sum_all_kernel");
@@ -248,10 +253,10 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
   dim3 grid(static_cast<unsigned>(capped_grid(g.outer * i_tiles, 4 * cap)),
             static_cast<unsigned>(splits));
   if (xd == HAP_BF16)
-    col_sum_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>(
+    hap::launch_k(col_sum_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream, 
         static_cast<const __nv_bfloat16*>(x), g.outer, g.red, g.inner, chunk, static_cast<float*>(y));
   else
-    col_sum_kernel<float><<<grid, 256, 0, stream>>>(static_cast<const float*>(x), g.outer, g.red,
+    hap::launch_k(col_sum_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(x), g.outer, g.red,
                                                     g.inner, chunk, static_cast<float*>(y));
   return launch_status("col_sum_kernel");
 }
@@ -268,7 +273,7 @@ extern "C" hap_status hap_unreduce(const void* dy, hap_dtype dyd, const int64_t*
   Dims d{rank, {}, mask};
   for (int a = 0; a < rank; ++a) d.shape[a] = shape[a];
   return HAP_DISPATCH_IO(dyd, dxd, [&] {
-    unreduce_kernel<Tin, Tout><<<capped_grid((n + 1023) / 1024, sm_cap), 1024, 0, stream>>>(
+    hap::launch_k(unreduce_kernel<Tin, Tout>, dim3(capped_grid((n + 1023) / 1024, sm_cap)), dim3(1024), 0, stream, 
         static_cast<const Tin*>(dy), d, g, n, static_cast<Tout*>(dx), accumulate);
     return launch_status("unreduce_kernel");
   });
