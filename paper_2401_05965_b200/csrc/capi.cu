@@ -12,8 +12,10 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 
 int pdl_enabled() {
   static int on = [] {
+    // Off by default: back-to-back GEMMs gain ~10% from it, but the full
+    // training step measured ~2% slower with it (profiles/README.md, PDL).
     const char* v = getenv("HAP_PDL");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 0;
   }();
   return on;
 }

@@ -60,13 +60,16 @@ inline int capped_grid(int64_t work_blocks, int sm_cap) {
 // its predecessor's memory (griddepcontrol.wait) and then immediately lets its
 // own successor start launching.  Setup that touches no global memory (smem
 // barriers, TMEM allocation, descriptor prefetch) runs before the wait and so
-// overlaps the previous kernel's tail.  HAP_PDL=0 disables it.
+// overlaps the previous kernel's tail.  Enabled with HAP_PDL=1 (default off:
+// measured slower on the mixed GEMM/elementwise step, faster GEMM-to-GEMM).
 int pdl_enabled();
 
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Short grid-stride kernels only wait: their successors launch at their
+// completion (an early trigger let the next GEMM's CTAs occupy SMs while the
+// elementwise kernel still streamed, which measured slower end to end).
+__device__ __forceinline__ void pdl_enter() { pdl_wait(); }
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,

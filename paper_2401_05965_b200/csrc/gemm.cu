@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  hap::pdl_enter();   // everything above touched no global memory
+  hap::pdl_wait();   // everything above touched no global memory
 
   if (warp == 0) {
     if (lane == 0) {
@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
@@ -601,7 +602,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  hap::pdl_enter();   // everything above touched no global memory
+  hap::pdl_wait();   // everything above touched no global memory
 
   if (warp == 0) {
     if (lane == 0) {
@@ -702,6 +703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
