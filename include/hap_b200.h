@@ -155,6 +155,31 @@ hap_status hap_reduce_scatter_v(void* comm, const void* send, void* recv, const 
 hap_status hap_all_to_all_v(void* comm, const void* send, const int64_t* send_counts, void* recv,
                             const int64_t* recv_counts, hap_dtype dtype, void* stream);
 
+/* ---- peer-memory collectives (hand-written, NVLink / NVSwitch) ------------
+ * A symmetric arena per rank (signal page + staging buffer of `bytes`),
+ * mapped into every peer with CUDA IPC.  Create, export the 64-byte handle,
+ * exchange handles on the host (all ranks' handles, rank-ordered), open. */
+hap_status hap_symm_create(void** ctx, int64_t bytes, int rank, int nranks);
+hap_status hap_symm_handle(void* ctx, uint8_t* out64);
+hap_status hap_symm_open(void* ctx, const uint8_t* handles64xn);
+hap_status hap_symm_destroy(void* ctx);
+int64_t hap_symm_capacity(void* ctx);
+/* all_gather along a blocked axis with uneven shards — interpreter.py:69-71:
+ * rank j's shard is [outer, sizes[j], inner]; the output is
+ * [outer, extent, inner] with shard j at offsets[j].  Peers' shards are read
+ * directly from their HBM over NVLink and written in place (no padding, no
+ * unpack pass).  `dev_sizes` / `dev_offsets` are DEVICE int64 arrays. */
+hap_status hap_p2p_all_gather_v(void* ctx, const void* send, void* recv, hap_dtype dtype, int64_t outer,
+                                int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                const int64_t* dev_offsets, int64_t max_chunk_elems, int sm_cap,
+                                void* stream);
+/* reduce_scatter — interpreter.py:94-96: `send` is this rank's partial
+ * [outer, extent, inner]; recv gets the cross-rank sum of rows
+ * [offsets[rank], offsets[rank] + sizes[rank]). */
+hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype, int64_t outer,
+                                    int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                    const int64_t* dev_offsets, int sm_cap, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,14 @@ SIGNATURES = {
     "hap_grouped_broadcast": (c_int, [_P, _P, _P, _I64P, c_int, _P]),
     "hap_reduce_scatter_v": (c_int, [_P, _P, _P, _I64P, c_int, _P, _P]),
     "hap_all_to_all_v": (c_int, [_P, _P, _I64P, _P, _I64P, c_int, _P]),
+    "hap_symm_create": (c_int, [POINTER(c_void_p), c_int64, c_int, c_int]),
+    "hap_symm_handle": (c_int, [_P, ctypes.c_char_p]),
+    "hap_symm_open": (c_int, [_P, ctypes.c_char_p]),
+    "hap_symm_destroy": (c_int, [_P]),
+    "hap_symm_capacity": (c_int64, [_P]),
+    "hap_p2p_all_gather_v": (c_int, [_P, _P, _P, c_int, c_int64, c_int64, c_int64, _P, _P, c_int64, c_int,
+                                     _P]),
+    "hap_p2p_reduce_scatter_v": (c_int, [_P, _P, _P, c_int, c_int64, c_int64, c_int64, _P, _P, c_int, _P]),
 }
 
 

@@ -1,0 +1,334 @@
+// Variable-chunk all-gather / reduce-scatter over NVLink peer memory.
+//
+// The reference's collectives (interpreter.py:69-101) concatenate / sum
+// per-device shards whose extents come from the ratio-rounded shard table —
+// uneven, possibly zero, and along any axis.  NCCL needs equal counts
+// (padding to the largest shard, the cost model's all_gather) or
+// pack/unpack passes for non-leading axes.  This kernel instead reads every
+// peer's shard straight out of its HBM through the NVSwitch (CUDA IPC mapped
+// pointers) and writes it at its final [outer, offset, inner] position:
+// exact bytes, no padding, no staging pass on the receiver.
+//
+// Protocol per call, for rank r with peers p (all ranks run the same call):
+//   1. wait until every peer has finished reading r's staging buffer from the
+//      previous call (done[p] >= epoch on r's signal page);
+//   2. copy r's shard into r's symmetric staging buffer (grid-stride), grid
+//      barrier, then one thread publishes ready[r] = epoch+1 on every peer's
+//      signal page (system-scope release);
+//   3. every CTA waits for ready[p] == epoch+1 (acquire) and pulls the peers'
+//      chunks over NVLink into the output (the own chunk from local staging);
+//   4. grid barrier, then done[r] = epoch+1 on every peer; epoch advances in
+//      device memory so CUDA-graph replays need no host bookkeeping.
+// Every CTA spins on flags another GPU writes, so the grid is one CTA per
+// (capped) SM, all resident; separate GPUs run the ranks, never one GPU.
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hap {
+namespace {
+
+constexpr int kMaxRanks = 16;
+constexpr int kThreads = 512;
+
+struct SignalPage {       // lives at the start of each rank's symmetric arena
+  uint64_t ready[kMaxRanks];
+  uint64_t done[kMaxRanks];
+  uint64_t epoch;         // calls completed by this rank
+  uint32_t arrive;        // grid-barrier counter (local)
+  uint32_t generation;    // grid-barrier generation (local)
+  uint64_t pad[5];
+};
+static_assert(sizeof(SignalPage) <= 512, "signal page too large");
+constexpr size_t kSignalBytes = 512;
+
+struct Symm {
+  int rank = 0, nranks = 1;
+  size_t bytes = 0;
+  char* local = nullptr;                 // arena base (signal page + staging)
+  char* peers[kMaxRanks] = {};           // peer arena bases (IPC-mapped), peers[rank] = local
+};
+
+struct Peers {
+  char* base[kMaxRanks];
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// All CTAs of the (fully resident) grid meet; returns true in exactly one CTA
+// (the last to arrive), after which everyone proceeds.
+__device__ bool grid_barrier(SignalPage* sig) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = *reinterpret_cast<volatile uint32_t*>(&sig->generation);
+    __threadfence();
+    const uint32_t n = atomicAdd(&sig->arrive, 1u) + 1;
+    last = n == gridDim.x;
+    if (last) {
+      sig->arrive = 0;
+      __threadfence();
+      atomicAdd(&sig->generation, 1u);
+    } else {
+      while (*reinterpret_cast<volatile uint32_t*>(&sig->generation) == gen) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return last;
+}
+
+template <typename T>
+__device__ void copy_elems(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (vec) {
+    constexpr int per = 16 / sizeof(T);
+    const int64_t nv = n / per;
+    const int4* s4 = reinterpret_cast<const int4*>(src);
+    int4* d4 = reinterpret_cast<int4*>(dst);
+    for (int64_t i = tid; i < nv; i += stride) d4[i] = s4[i];
+    for (int64_t i = nv * per + tid; i < n; i += stride) dst[i] = src[i];
+  } else {
+    for (int64_t i = tid; i < n; i += stride) dst[i] = src[i];
+  }
+}
+
+// Block placement: chunk [outer, rows, inner] -> out[outer, off + rows, inner].
+template <typename T>
+__device__ void place_chunk(T* __restrict__ out, const T* __restrict__ chunk, int64_t outer, int64_t rows,
+                            int64_t inner, int64_t extent, int64_t off) {
+  if (outer == 1) {
+    copy_elems(out + off * inner, chunk, rows * inner);
+    return;
+  }
+  const int64_t per = rows * inner;
+  const int64_t total = outer * per;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = tid; e < total; e += stride) {
+    const int64_t o = e / per, rem = e - o * per;
+    out[(o * extent + off) * inner + rem] = chunk[e];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_all_gather_kernel(Peers peers, int rank, int nranks,
+                                                                  const T* __restrict__ send, T* __restrict__ out,
+                                                                  int64_t outer, int64_t inner, int64_t extent,
+                                                                  const int64_t* __restrict__ sizes,
+                                                                  const int64_t* __restrict__ offs) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  T* staging = reinterpret_cast<T*>(peers.base[rank] + kSignalBytes);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  // 1. peers have finished reading my staging buffer from the previous call
+  if (threadIdx.x < nranks && threadIdx.x != rank)
+    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
+  __syncthreads();
+  // 2. publish my shard
+  const int64_t mine = outer * sizes[rank] * inner;
+  copy_elems(staging, send, mine);
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      SignalPage* peer_sig = reinterpret_cast<SignalPage*>(peers.base[p]);
+      st_release_sys(&peer_sig->ready[rank], epoch + 1);
+    }
+  }
+  // 3. pull every chunk into place
+  if (threadIdx.x < nranks && threadIdx.x != rank)
+    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  for (int q = 0; q < nranks; ++q) {
+    const int p = (rank + q) % nranks;  // stagger sources across ranks
+    // own chunk from `send` (staging was written by other CTAs of this grid
+    // and could be stale in this SM's L1); peers' staging over NVLink
+    const T* src = p == rank ? send : reinterpret_cast<const T*>(peers.base[p] + kSignalBytes);
+    place_chunk(out, src, outer, sizes[p], inner, extent, offs[p]);
+  }
+  // 4. done reading the peers' staging buffers
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      SignalPage* peer_sig = reinterpret_cast<SignalPage*>(peers.base[p]);
+      st_release_sys(&peer_sig->done[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+}
+
+// Reduce-scatter: rank r stages its whole partial tensor [outer, extent,
+// inner]; every rank then sums, for its own shard rows, the matching rows of
+// all peers' partial tensors over NVLink.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_kernel(Peers peers, int rank, int nranks,
+                                                                      const T* __restrict__ send,
+                                                                      T* __restrict__ out, int64_t outer,
+                                                                      int64_t inner, int64_t extent,
+                                                                      const int64_t* __restrict__ sizes,
+                                                                      const int64_t* __restrict__ offs) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  T* staging = reinterpret_cast<T*>(peers.base[rank] + kSignalBytes);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  if (threadIdx.x < nranks && threadIdx.x != rank)
+    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
+  __syncthreads();
+  copy_elems(staging, send, outer * extent * inner);
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[p])->ready[rank], epoch + 1);
+    }
+  }
+  if (threadIdx.x < nranks && threadIdx.x != rank)
+    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  const int64_t rows = sizes[rank], off = offs[rank];
+  const int64_t per = rows * inner, total = outer * per;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = tid; e < total; e += stride) {
+    const int64_t o = e / per, rem = e - o * per;
+    const int64_t at = (o * extent + off) * inner + rem;
+    float acc = 0.f;
+    for (int q = 0; q < nranks; ++q) {
+      const int p = (rank + q) % nranks;
+      acc += to_f32(p == rank ? send[at] : reinterpret_cast<const T*>(peers.base[p] + kSignalBytes)[at]);
+    }
+    out[e] = from_f32<T>(acc);
+  }
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[p])->done[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+}
+
+}  // namespace
+}  // namespace hap
+
+using namespace hap;
+
+extern "C" hap_status hap_symm_create(void** out, int64_t bytes, int rank, int nranks) {
+  HAP_CHECK_ARG(out && bytes > 0 && nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks,
+                "hap_symm_create: bad arguments");
+  auto* s = new Symm();
+  s->rank = rank;
+  s->nranks = nranks;
+  s->bytes = kSignalBytes + static_cast<size_t>(bytes);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s->local), s->bytes);
+  if (e != cudaSuccess) {
+    delete s;
+    set_error(std::string("hap_symm_create: cudaMalloc: ") + cudaGetErrorString(e));
+    return HAP_ERR_CUDA;
+  }
+  HAP_CUDA_TRY(cudaMemset(s->local, 0, kSignalBytes));
+  s->peers[rank] = s->local;
+  *out = s;
+  return HAP_OK;
+}
+
+extern "C" hap_status hap_symm_handle(void* ctx, uint8_t* out64) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && out64, "hap_symm_handle: bad arguments");
+  cudaIpcMemHandle_t h;
+  HAP_CUDA_TRY(cudaIpcGetMemHandle(&h, s->local));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out64, &h, 64);
+  return HAP_OK;
+}
+
+extern "C" hap_status hap_symm_open(void* ctx, const uint8_t* handles) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && handles, "hap_symm_open: bad arguments");
+  for (int p = 0; p < s->nranks; ++p) {
+    if (p == s->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * p, 64);
+    void* ptr = nullptr;
+    HAP_CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    s->peers[p] = static_cast<char*>(ptr);
+  }
+  return HAP_OK;
+}
+
+extern "C" hap_status hap_symm_destroy(void* ctx) {
+  auto* s = static_cast<Symm*>(ctx);
+  if (!s) return HAP_OK;
+  for (int p = 0; p < s->nranks; ++p)
+    if (p != s->rank && s->peers[p]) cudaIpcCloseMemHandle(s->peers[p]);
+  cudaFree(s->local);
+  delete s;
+  return HAP_OK;
+}
+
+extern "C" int64_t hap_symm_capacity(void* ctx) {
+  auto* s = static_cast<Symm*>(ctx);
+  return s ? static_cast<int64_t>(s->bytes - kSignalBytes) : 0;
+}
+
+namespace {
+
+template <typename T>
+hap_status p2p_launch(void (*kern)(Peers, int, int, const T*, T*, int64_t, int64_t, int64_t, const int64_t*,
+                                   const int64_t*),
+                      Symm* s, const void* send, void* out, int64_t outer, int64_t inner, int64_t extent,
+                      const int64_t* dev_sizes, const int64_t* dev_offs, int sm_cap, cudaStream_t stream) {
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  const int grid = capped_grid(sm_count(), sm_cap);  // one resident CTA per (capped) SM
+  launch_k(kern, dim3(grid), dim3(kThreads), 0, stream, peers, s->rank, s->nranks, static_cast<const T*>(send),
+           static_cast<T*>(out), outer, inner, extent, dev_sizes, dev_offs);
+  return launch_status("p2p kernel");
+}
+
+}  // namespace
+
+extern "C" hap_status hap_p2p_all_gather_v(void* ctx, const void* send, void* recv, hap_dtype dtype,
+                                           int64_t outer, int64_t inner, int64_t extent,
+                                           const int64_t* dev_sizes, const int64_t* dev_offsets,
+                                           int64_t max_chunk_elems, int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_sizes && dev_offsets, "hap_p2p_all_gather_v: bad arguments");
+  HAP_CHECK_ARG(max_chunk_elems * static_cast<int64_t>(dtype_size(dtype)) <= hap_symm_capacity(ctx),
+                "hap_p2p_all_gather_v: shard larger than the symmetric staging buffer");
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    return p2p_launch<__nv_bfloat16>(p2p_all_gather_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent, dev_sizes,
+                      dev_offsets, sm_cap, st);
+  return p2p_launch<float>(p2p_all_gather_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes, dev_offsets,
+                    sm_cap, st);
+}
+
+extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype,
+                                               int64_t outer, int64_t inner, int64_t extent,
+                                               const int64_t* dev_sizes, const int64_t* dev_offsets,
+                                               int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_sizes && dev_offsets, "hap_p2p_reduce_scatter_v: bad arguments");
+  HAP_CHECK_ARG(outer * extent * inner * static_cast<int64_t>(dtype_size(dtype)) <= hap_symm_capacity(ctx),
+                "hap_p2p_reduce_scatter_v: tensor larger than the symmetric staging buffer");
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    return p2p_launch<__nv_bfloat16>(p2p_reduce_scatter_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent, dev_sizes,
+                      dev_offsets, sm_cap, st);
+  return p2p_launch<float>(p2p_reduce_scatter_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes,
+                    dev_offsets, sm_cap, st);
+}

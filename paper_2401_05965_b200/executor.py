@@ -134,7 +134,9 @@ class ExecConfig:
     sm_caps: list | None = None       # per program-device SM cap (heterogeneity emulation)
     lr: float = 0.0                   # SGD learning rate of train_step
     grad_sync: str = "auto"           # "auto" (cost model) | "all_reduce" | "sfb"
-    gather: str = "auto"              # all_gather impl: "auto" | "padded" | "p2p"
+    gather: str = "auto"              # all_gather / reduce_scatter impl: "auto" = "kernel" (NVLink
+                                      # peer-memory kernel) | "padded" (NCCL, max-shard padding) |
+                                      # "sendrecv" (NCCL grouped point-to-point)
     input_grads: bool = False         # also differentiate w.r.t. placeholders
     cluster: object = None            # ClusterSpec for the cost-model choices
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
@@ -190,8 +192,10 @@ class Executor:
         self._check_program()
         self._infer()
         self._allocate()
+        self._symm = None
         self._compile_forward()
         self._compile_backward()
+        self._create_symm()
 
     # ------------------------------------------------------------------ analysis
     def _sizes(self, ref: str, axis: int) -> list[int]:
@@ -397,6 +401,15 @@ class Executor:
         outer, _, inner = _view(full_shape, axis)
         counts = [sz * outer * inner for sz in sizes]
         s = src[r]
+        if kind == "all_gather" and self.cfg.gather in ("auto", "kernel"):
+            # hand-written NVLink kernel: exact chunks, placed in the final layout
+            exact = not accumulate and dst[r].dtype == s.dtype
+            target = dst[r] if exact else self._new(full_shape, s.dtype)
+            self._p2p("hap_p2p_all_gather_v", s, target, outer, inner, full_shape[axis], sizes,
+                      max(counts) * (2 if s.dtype == BF16 else 4))
+            if not exact:
+                self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
+            return
         direct = outer == 1 and not accumulate and dst[r].dtype == s.dtype
         target = dst[r] if direct else self._new((sum(counts),), s.dtype)
         carr = _lib.i64_array(counts)
@@ -405,7 +418,7 @@ class Executor:
             self._emit("hap_grouped_broadcast", g.comm, s.ptr, target.ptr, carr, s.dtype,
                        self._sptr(), kernel=False)
         else:
-            padded = self.cfg.gather in ("auto", "padded")
+            padded = self.cfg.gather == "padded"
             scratch = self._new((self.m * max(counts),), s.dtype) if padded else None
             self._emit("hap_all_gather_v", g.comm, s.ptr, target.ptr, carr, s.dtype, int(padded),
                        scratch.ptr if scratch else None, self._sptr(), kernel=False)
@@ -437,6 +450,14 @@ class Executor:
         r = g.rank
         s = src[r]
         counts = [sz * outer * inner for sz in sizes]
+        if self.cfg.gather in ("auto", "kernel"):
+            exact = not accumulate and dst[r].dtype == s.dtype
+            target = dst[r] if exact else self._new(dst[r].shape, s.dtype)
+            self._p2p("hap_p2p_reduce_scatter_v", s, target, outer, inner, ext, sizes,
+                      outer * ext * inner * (2 if s.dtype == BF16 else 4))
+            if not exact:
+                self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
+            return
         if outer == 1:
             send = s
         else:  # pack rank-ordered chunks
@@ -500,6 +521,42 @@ class Executor:
                 chunk = Buf(recv.tensor[roff[k]:roff[k + 1]], s.dtype, recv_shapes[k])
                 self._block(chunk, _view(recv_shapes[k], d1), 0, dst[r], _view(dst[r].shape, d1), off1[k],
                             sizes1[k], self.caps[r], accumulate)
+
+    def _p2p(self, fn: str, send: Buf, recv: Buf, outer: int, inner: int, extent: int, sizes: list,
+             arena_bytes: int):
+        """Emit a peer-memory collective; the symmetric arena is created once
+        compilation knows the largest staging need (same on every rank)."""
+        r = self.group.rank
+        dev = torch.tensor([list(sizes), offsets(sizes)[:-1]], dtype=torch.int64, device=self.device)
+        self._keep(dev)
+        self._p2p_bytes = max(getattr(self, "_p2p_bytes", 0), arena_bytes)
+        fn_ptr = getattr(self.lib, fn)
+        stream = self._sptr()
+        cap = self.caps[r]
+        sizes_ptr, offs_ptr = dev[0].data_ptr(), dev[1].data_ptr()
+        if fn == "hap_p2p_all_gather_v":
+            max_chunk = max(sizes) * outer * inner
+            args = lambda: (self._symm, send.ptr, recv.ptr, send.dtype, outer, inner, extent, sizes_ptr,  # noqa: E731
+                            offs_ptr, max_chunk, cap, stream)
+        else:
+            args = lambda: (self._symm, send.ptr, recv.ptr, send.dtype, outer, inner, extent, sizes_ptr,  # noqa: E731
+                            offs_ptr, cap, stream)
+        self._ops.append(Op(lambda: fn_ptr(*args()), (), fn, True))
+
+    def _create_symm(self):
+        if not getattr(self, "_p2p_bytes", 0):
+            return
+        import torch.distributed as dist
+
+        g = self.group
+        ctx = ctypes.c_void_p()
+        check(self.lib.hap_symm_create(ctypes.byref(ctx), int(self._p2p_bytes), g.rank, g.m), "hap_symm_create")
+        handle = ctypes.create_string_buffer(64)
+        check(self.lib.hap_symm_handle(ctx, handle), "hap_symm_handle")
+        handles = [None] * g.m
+        dist.all_gather_object(handles, bytes(handle.raw))
+        check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
+        self._symm = ctx
 
     def _keep(self, obj):
         self.__dict__.setdefault("_keepalive", []).append(obj)
@@ -1034,4 +1091,9 @@ class Executor:
         return out
 
     def close(self):
-        self.group.close()
+        if getattr(self, "_symm", None):
+            torch.cuda.synchronize(self.device)
+            check(self.lib.hap_symm_destroy(self._symm), "hap_symm_destroy")
+            self._symm = None
+        if self.group is not None:
+            self.group.close()

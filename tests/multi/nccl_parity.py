@@ -53,7 +53,7 @@ def main():
         shapes = {n.id: n.shape for n in g.sources()}
         program, m, table = O.load_plan(doc)
         for dtype in ("fp32", "bf16"):
-            for gather in ("padded", "p2p"):
+            for gather in ("kernel", "padded", "sendrecv"):
                 count += 1
                 ex = Executor(DistributedProgram.from_json(doc["program"]), m, table_from_plan(doc), shapes,
                               group=group, config=ExecConfig(dtype=dtype, input_grads=True, gather=gather))
