@@ -96,8 +96,19 @@ __device__ void copy_elems(T* __restrict__ dst, const T* __restrict__ src, int64
     const int64_t nv = n / per;
     const int4* s4 = reinterpret_cast<const int4*>(src);
     int4* d4 = reinterpret_cast<int4*>(dst);
-    for (int64_t i = tid; i < nv; i += stride) d4[i] = s4[i];
-    for (int64_t i = nv * per + tid; i < n; i += stride) dst[i] = src[i];
+    // 8 independent 16-byte loads in flight per thread: a peer read over
+    // NVLink costs ~2 us, so bandwidth needs many outstanding requests.
+    constexpr int U = 8;
+    int64_t i = tid;
+    for (; i + (U - 1) * stride < nv; i += U * stride) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = s4[i + u * stride];
+#pragma unroll
+      for (int u = 0; u < U; ++u) d4[i + u * stride] = v[u];
+    }
+    for (; i < nv; i += stride) d4[i] = s4[i];
+    for (int64_t j = nv * per + tid; j < n; j += stride) dst[j] = src[j];
   } else {
     for (int64_t i = tid; i < n; i += stride) dst[i] = src[i];
   }

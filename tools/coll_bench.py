@@ -1,0 +1,107 @@
+"""Uneven all-gather / reduce-scatter bandwidth: NVLink peer-memory kernel vs
+NCCL (padded all-gather, grouped send/recv), shards weighted by the bench's
+SM-cap ratios.  Run with torchrun (one process per GPU):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/coll_bench.py [--json out]
+
+Reports, per implementation and size, the time (max over ranks, CUDA events)
+and the bus bandwidth = bytes each rank must receive / time.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2401_05965_b200 import workloads  # noqa: E402
+from paper_2401_05965_b200._lib import BF16, check, i64_array, lib  # noqa: E402
+from paper_2401_05965_b200.executor import NcclGroup  # noqa: E402
+from paper_2401_05965_b200.sharding import offsets, round_shards  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    L = lib()
+    group = NcclGroup.from_torch_distributed()
+    caps = workloads.sm_caps(world)
+    ratios = [c / sum(caps) for c in caps]
+    inner = 768
+    stream = torch.cuda.Stream(dev)
+    results = []
+    import ctypes
+    arena_bytes = 1 << 30
+    ctx = ctypes.c_void_p()
+    check(L.hap_symm_create(ctypes.byref(ctx), arena_bytes, rank, world))
+    h = ctypes.create_string_buffer(64)
+    check(L.hap_symm_handle(ctx, h))
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(h.raw))
+    check(L.hap_symm_open(ctx, b"".join(handles)))
+    for rows in (4096, 16384, 65536, 262144):
+        sizes = round_shards(rows, ratios)
+        counts = [s * inner for s in sizes]
+        send = torch.randn(counts[rank], device=dev).to(torch.bfloat16)
+        out = torch.empty(rows * inner, device=dev, dtype=torch.bfloat16)
+        scratch = torch.empty(world * max(counts), device=dev, dtype=torch.bfloat16)
+        devsz = torch.tensor([sizes, offsets(sizes)[:-1]], dtype=torch.int64, device=dev)
+        carr = i64_array(counts)
+        recv_bytes = (sum(counts) - counts[rank]) * 2
+        impls = {
+            "p2p_kernel": lambda: L.hap_p2p_all_gather_v(ctx, send.data_ptr(), out.data_ptr(), BF16, 1, inner, rows,
+                                                         devsz[0].data_ptr(), devsz[1].data_ptr(), max(counts), 0,
+                                                         stream.cuda_stream),
+            "nccl_padded": lambda: L.hap_all_gather_v(group.comm, send.data_ptr(), out.data_ptr(), carr, BF16, 1,
+                                                      scratch.data_ptr(), stream.cuda_stream),
+            "nccl_sendrecv": lambda: L.hap_all_gather_v(group.comm, send.data_ptr(), out.data_ptr(), carr, BF16, 0,
+                                                        None, stream.cuda_stream),
+        }
+        ref = None
+        for name, fn in impls.items():
+            for _ in range(3):
+                check(fn(), name)
+            torch.cuda.synchronize(dev)
+            if ref is None:
+                ref = out.clone()
+            else:
+                assert torch.equal(out, ref), name
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            t = torch.tensor([e0.elapsed_time(e1) / args.reps], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            rb = torch.tensor([recv_bytes], device=dev, dtype=torch.float64)
+            dist.all_reduce(rb, op=dist.ReduceOp.MAX)
+            results.append({"op": "all_gather", "impl": name, "rows": rows, "shard_rows": sizes,
+                            "ms": ms, "recv_GBps_max_rank": float(rb.item()) / (ms * 1e-3) / 1e9})
+    if rank == 0:
+        for r in results:
+            print(f"{r['op']:10s} {r['impl']:14s} rows={r['rows']:7d} {r['ms'] * 1e3:9.1f} us "
+                  f"{r['recv_GBps_max_rank']:7.1f} GB/s received per rank")
+        if args.json:
+            with open(args.json, "w") as fh:
+                json.dump({"world": world, "caps": caps, "results": results}, fh, indent=1)
+    dist.barrier()
+    check(L.hap_symm_destroy(ctx))
+    group.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
