@@ -61,6 +61,27 @@ hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B, int
                       int transB, void* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                       hap_dtype in_dtype, hap_dtype out_dtype, int accumulate, int sm_cap,
                       void* stream);
+/* Batched matmul: one persistent tcgen05 launch for up to 4 problems per
+ * chunk (more are chunked).  sum_k == 0: independent problems (e.g. the
+ * projections of one input) share the launch; sum_k != 0: every problem adds
+ * into descs[0]'s output (C = sum_i op(A_i).op(B_i), e.g. an activation
+ * gradient with several consumers), accumulate taken from descs[0].  All
+ * problems must share transA/transB and the dtypes; otherwise they run one by
+ * one.  Replaces a run of interpreter.py:139-140 matmul branches. */
+typedef struct {
+  const void* A;
+  int64_t lda;
+  int transA;
+  const void* B;
+  int64_t ldb;
+  int transB;
+  void* C;
+  int64_t ldc;
+  int64_t M, N, K;
+  int accumulate;
+} hap_gemm_desc;
+hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
+                            hap_dtype out_dtype, int sm_cap, void* stream);
 /* Which engine hap_matmul would use for these arguments (no launch). */
 int hap_matmul_engine(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                       int transB, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype);

@@ -24,6 +24,13 @@ GEMM_TCGEN05, GEMM_SIMT = 0, 1
 _P = c_void_p
 _I64P = POINTER(c_int64)
 
+class GemmDesc(ctypes.Structure):
+    """hap_gemm_desc (include/hap_b200.h)."""
+    _fields_ = [("A", c_void_p), ("lda", c_int64), ("transA", c_int), ("B", c_void_p), ("ldb", c_int64),
+                ("transB", c_int), ("C", c_void_p), ("ldc", c_int64), ("M", c_int64), ("N", c_int64),
+                ("K", c_int64), ("accumulate", c_int)]
+
+
 # name -> (restype, argtypes); must cover every function include/hap_b200.h declares.
 SIGNATURES = {
     "hap_last_error": (ctypes.c_char_p, []),
@@ -31,6 +38,7 @@ SIGNATURES = {
     "hap_sm_count": (c_int, []),
     "hap_matmul": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, _P, c_int64, c_int64, c_int64,
                            c_int64, c_int, c_int, c_int, c_int, _P]),
+    "hap_matmul_batch": (c_int, [POINTER(GemmDesc), c_int, c_int, c_int, c_int, c_int, _P]),
     "hap_matmul_engine": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, c_int64, c_int64, c_int64,
                                   c_int]),
     "hap_unary": (c_int, [c_int, _P, c_int, _P, c_int, c_int64, c_int, _P]),

@@ -20,6 +20,15 @@ int pdl_enabled() {
   return on;
 }
 
+int carveout_pref() {
+  static int pref = [] {
+    // default: leave the driver's choice (forcing 100 % measured slower)
+    const char* v = getenv("HAP_CARVEOUT");
+    return v ? atoi(v) : -1;
+  }();
+  return pref;
+}
+
 int sm_count() {
   static int cached[64] = {0};
   int dev = 0;

@@ -71,9 +71,26 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // elementwise kernel still streamed, which measured slower end to end).
 __device__ __forceinline__ void pdl_enter() { pdl_wait(); }
 
+int carveout_pref();
+
+// Every kernel asks for the maximum shared-memory carveout, so consecutive
+// GEMM (225 KB smem) and elementwise launches do not force the SMs to
+// re-partition L1/shared memory between kernels (HAP_CARVEOUT=-1 leaves the
+// driver default).
+template <typename K>
+inline void set_carveout(K kern) {
+  static bool done = false;
+  if (!done) {
+    const int pref = carveout_pref();
+    if (pref >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pref);
+    done = true;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                             Args&&... args) {
+  set_carveout(kern);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

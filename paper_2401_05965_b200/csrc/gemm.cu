@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -312,13 +313,70 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
   }
 }
 
-// Work unit u covers output tile (u % num_tiles) and K-blocks
-// [split * kb_per_split, min(k_blocks, (split + 1) * kb_per_split)), split = u / num_tiles.
+// ------------------------------------------------------------------ batched problems
+// One persistent launch serves up to kMaxProblems GEMMs of the same operand
+// orientation: either independent problems whose tiles share the launch
+// (grouped: e.g. the Q/K/V projections of one input), or problems that all
+// add into one output (sum_k: C = sum_i A_i . B_i, the K blocks of every
+// problem accumulate into the same TMEM tile — e.g. dx = dq.Wq^T + dk.Wk^T +
+// dv.Wv^T).  Small GEMMs pay the launch, prologue and partial last wave once.
+constexpr int kMaxProblems = 4;
+
+struct alignas(64) TcProblem {
+  CUtensorMap a, b, c;
+  void* C;
+  int64_t ldc;
+  int M, N, K;
+  int m_tiles, n_tiles, k_blocks;
+  int splits, kb_per_split;
+  int unit_begin;
+  int epi_mode, accumulate, vec_ok;
+};
+
+struct alignas(64) TcBatch {
+  TcProblem p[kMaxProblems];
+  int count;
+  int sum_k;
+  int total_units;
+};
+
+struct Unit {
+  int prob, m0, n0, kb0, kb1;
+};
+
+// Work unit u -> (problem, output tile, K-block range).  Grouped: units are
+// laid out problem after problem; within a problem unit = split * tiles + tile.
+template <int ROWS, int BN>
+__device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
+  int p = 0;
+  if (!bt.sum_k)
+    while (p + 1 < bt.count && u >= bt.p[p + 1].unit_begin) ++p;
+  const TcProblem& pr = bt.p[p];
+  const int local = u - pr.unit_begin;
+  const int tiles = pr.m_tiles * pr.n_tiles;
+  const int t = local % tiles;
+  Unit x;
+  x.prob = p;
+  x.m0 = (t % pr.m_tiles) * ROWS;
+  x.n0 = (t / pr.m_tiles) * BN;
+  x.kb0 = (local / tiles) * pr.kb_per_split;
+  x.kb1 = min(pr.k_blocks, x.kb0 + pr.kb_per_split);
+  return x;
+}
+
+// f(problem, k_block) for every K block a unit accumulates, in order.
+template <typename F>
+__device__ __forceinline__ void for_each_kblock(const TcBatch& bt, const Unit& x, F&& f) {
+  if (bt.sum_k) {
+    for (int q = 0; q < bt.count; ++q)
+      for (int kb = 0; kb < bt.p[q].k_blocks; ++kb) f(q, kb);
+  } else {
+    for (int kb = x.kb0; kb < x.kb1; ++kb) f(x.prob, kb);
+  }
+}
+
 template <int BN, bool kAMN, bool kBMN, typename OutT>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, OutT* __restrict__ C, int64_t ldc, int M, int N,
-                   int K, int accumulate, int vec_ok, int splits, int kb_per_split, int epi_mode) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcBatch bt) {
   using G = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -330,18 +388,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
   const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
-
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tiles = (M + BM - 1) / BM;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  const int num_units = num_tiles * splits;
-  const int k_blocks = (K + BK - 1) / BK;
+  const int num_units = bt.total_units;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    for (int q = 0; q < bt.count; ++q) {
+      tma_prefetch(&bt.p[q].a);
+      tma_prefetch(&bt.p[q].b);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < G::kStages; ++s) {
@@ -355,8 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(G::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -372,35 +426,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        const int t = u % num_tiles;
-        const int kb0 = (u / num_tiles) * kb_per_split;
-        const int kb1 = min(k_blocks, kb0 + kb_per_split);
-        const int m0 = (t % m_tiles) * BM;
-        const int n0 = (t / m_tiles) * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const Unit x = decode_unit<BM, BN>(bt, u);
+        for_each_kblock(bt, x, [&](int q, int kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_expect_tx(fb, G::kStageBytes);
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
           const int k0 = kb * BK;
+          const CUtensorMap* ma = &bt.p[q].a;
+          const CUtensorMap* mb = &bt.p[q].b;
           if (kAMN) {
-            tma_load_2d(sa, &tmA, fb, m0, k0);
-            tma_load_2d(sa + BK * 128, &tmA, fb, m0 + 64, k0);
+            tma_load_2d(sa, ma, fb, x.m0, k0);
+            tma_load_2d(sa + BK * 128, ma, fb, x.m0 + 64, k0);
           } else {
-            tma_load_2d(sa, &tmA, fb, k0, m0);
+            tma_load_2d(sa, ma, fb, k0, x.m0);
           }
           if (kBMN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * BK * 128, &tmB, fb, n0 + 64 * c, k0);
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * BK * 128, mb, fb, x.n0 + 64 * c, k0);
           } else {
-            tma_load_2d(sb, &tmB, fb, k0, n0);
+            tma_load_2d(sb, mb, fb, k0, x.n0);
           }
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
-        }
+        });
       }
     }
   } else if (warp == 1) {
@@ -417,12 +469,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        const int kb0 = (u / num_tiles) * kb_per_split;
-        const int kb1 = min(k_blocks, kb0 + kb_per_split);
+        const Unit x = decode_unit<BM, BN>(bt, u);
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        bool first = true;
+        for_each_kblock(bt, x, [&](int, int) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
@@ -432,14 +484,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t aoff = kAMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             const uint32_t boff = kBMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             tc_mma(d_tmem, sdesc(sa + aoff, kALbo, 1024), sdesc(sb + boff, kBLbo, 1024), kIdesc,
-                   (kb != kb0) || (kk != 0));
+                   (!first) || (kk != 0));
           }
+          first = false;
           tc_commit(empty0 + 8 * stage);
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
-        }
+        });
         tc_commit(tfull0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -453,13 +506,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-      const int t = u % num_tiles;
-      const int m0 = (t % m_tiles) * BM;
-      const int n0 = (t / m_tiles) * BN;
+      const Unit x = decode_unit<BM, BN>(bt, u);
+      const TcProblem& pr = bt.p[x.prob];
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, n0, M, N, C, ldc,
-                                  epi_mode, vec_ok, accumulate, splits, &tmC, buf);
+      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, pr.M,
+                                  pr.N, static_cast<OutT*>(pr.C), pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate,
+                                  pr.splits, &pr.c, buf);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
@@ -472,8 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(G::kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(G::kTmemCols));
   }
 }
 
@@ -495,6 +547,7 @@ struct Cfg2 {
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 256 + 1024;
 };
+
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -549,11 +602,10 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, OutT* __restrict__ C, int64_t ldc, int M, int N,
-                    int K, int accumulate, int vec_ok, int splits, int kb_per_split, int epi_mode) {
+    gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {
   using G = Cfg2<BN>;
   constexpr int HB = BN / 2;  // B columns staged per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -566,21 +618,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
   const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
-
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
-  const int m_tiles = (M + 255) / 256;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
-  const int num_units = num_tiles * splits;
-  const int k_blocks = (K + BK - 1) / BK;
+  const int num_units = bt.total_units;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    for (int q = 0; q < bt.count; ++q) {
+      tma_prefetch(&bt.p[q].a);
+      tma_prefetch(&bt.p[q].b);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < G::kStages; ++s) {
@@ -610,12 +659,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pair; u < num_units; u += num_pairs) {
-        const int t = u % num_tiles;
-        const int kb0 = (u / num_tiles) * kb_per_split;
-        const int kb1 = min(k_blocks, kb0 + kb_per_split);
-        const int m0 = (t % m_tiles) * 256 + 128 * static_cast<int>(rank);
-        const int n0 = (t / m_tiles) * BN + HB * static_cast<int>(rank);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const Unit x = decode_unit<256, BN>(bt, u);
+        const int m0 = x.m0 + 128 * static_cast<int>(rank);
+        const int n0 = x.n0 + HB * static_cast<int>(rank);
+        for_each_kblock(bt, x, [&](int q, int kb) {
           mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
           const uint32_t leader_full = map_to_cta(full0 + 8 * stage, 0);
           if (rank == 0) mbar_expect_tx_cluster(leader_full, 2 * G::kStageBytes);
@@ -623,23 +670,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
           const int k0 = kb * BK;
+          const CUtensorMap* ma = &bt.p[q].a;
+          const CUtensorMap* mb = &bt.p[q].b;
           if (kAMN) {
-            tma_load_2d_pair(sa, &tmA, leader_full, m0, k0);
-            tma_load_2d_pair(sa + BK * 128, &tmA, leader_full, m0 + 64, k0);
+            tma_load_2d_pair(sa, ma, leader_full, m0, k0);
+            tma_load_2d_pair(sa + BK * 128, ma, leader_full, m0 + 64, k0);
           } else {
-            tma_load_2d_pair(sa, &tmA, leader_full, k0, m0);
+            tma_load_2d_pair(sa, ma, leader_full, k0, m0);
           }
           if (kBMN) {
 #pragma unroll
-            for (int c = 0; c < HB / 64; ++c) tma_load_2d_pair(sb + c * BK * 128, &tmB, leader_full, n0 + 64 * c, k0);
+            for (int c = 0; c < HB / 64; ++c) tma_load_2d_pair(sb + c * BK * 128, mb, leader_full, n0 + 64 * c, k0);
           } else {
-            tma_load_2d_pair(sb, &tmB, leader_full, k0, n0);
+            tma_load_2d_pair(sb, mb, leader_full, k0, n0);
           }
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
-        }
+        });
       }
     }
   } else if (warp == 1) {
@@ -653,12 +702,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = pair; u < num_units; u += num_pairs) {
-        const int kb0 = (u / num_tiles) * kb_per_split;
-        const int kb1 = min(k_blocks, kb0 + kb_per_split);
+        const Unit x = decode_unit<256, BN>(bt, u);
         mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        bool first = true;
+        for_each_kblock(bt, x, [&](int, int) {
           mbar_wait_cluster(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
@@ -668,14 +717,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t aoff = kAMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             const uint32_t boff = kBMN ? kk * UMMA_K * 128 : kk * UMMA_K * 2;
             tc_mma_pair(d_tmem, sdesc(sa + aoff, kALbo, 1024), sdesc(sb + boff, kBLbo, 1024), kIdesc,
-                        (kb != kb0) || (kk != 0));
+                        (!first) || (kk != 0));
           }
+          first = false;
           tc_commit_pair(empty0 + 8 * stage);
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
-        }
+        });
         tc_commit_pair(tfull0 + 8 * acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -690,13 +740,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < num_units; u += num_pairs) {
-      const int t = u % num_tiles;
-      const int m0 = (t % m_tiles) * 256 + 128 * static_cast<int>(rank);
-      const int n0 = (t / m_tiles) * BN;
+      const Unit x = decode_unit<256, BN>(bt, u);
+      const TcProblem& pr = bt.p[x.prob];
+      const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, n0, M, N, C, ldc,
-                                  epi_mode, vec_ok, accumulate, splits, &tmC, buf);
+      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, pr.M, pr.N,
+                                  static_cast<OutT*>(pr.C), pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate,
+                                  pr.splits, &pr.c, buf);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
@@ -760,92 +811,77 @@ bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool kAMN, bool kBMN, typename OutT>
-hap_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int mode, void* C,
-                  int64_t ldc, int M, int N, int K, int accumulate, int vec_ok, int sm_cap, int splits,
-                  int kb_per_split, cudaStream_t stream) {
-  using G = Cfg<BN>;
-  auto kern = gemm_tc_kernel<BN, kAMN, kBMN, OutT>;
-  static bool configured = false;
-  if (!configured) {
-    HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-    configured = true;
+
+template <typename K>
+hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cudaStream_t stream,
+                        const char* what) {
+  static_assert(sizeof(TcBatch) < 4096, "TcBatch must fit the kernel parameter space");
+  // per-instantiation once: large dynamic shared memory
+  static std::mutex mu;
+  static std::vector<const void*> configured;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(configured.begin(), configured.end(), reinterpret_cast<const void*>(kern)) == configured.end()) {
+      HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+      configured.push_back(reinterpret_cast<const void*>(kern));
+    }
   }
-  const int64_t tiles = static_cast<int64_t>((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = capped_grid(tiles * splits, sm_cap);
-  hap::launch_k(kern, dim3(grid), dim3(kThreads), G::kSmem, stream, ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K,
-                                              accumulate, vec_ok, splits, kb_per_split, mode);
-  return launch_status("gemm_tc_kernel");
+  launch_k(kern, dim3(grid), dim3(kThreads), smem_bytes, stream, bt);
+  return launch_status(what);
 }
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
-hap_status launch2(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int mode, void* C,
-                   int64_t ldc, int M, int N, int K, int accumulate, int vec_ok, int sm_cap, int splits,
-                   int kb_per_split, cudaStream_t stream) {
-  using G = Cfg2<BN>;
-  auto kern = gemm_tc2_kernel<BN, kAMN, kBMN, OutT>;
-  static bool configured = false;
-  if (!configured) {
-    HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-    configured = true;
+hap_status launch_shape(bool pair, const TcBatch& bt, int cap, cudaStream_t stream) {
+  if (pair) {
+    const int pairs = std::min<int>(bt.total_units, std::max(1, cap / 2));
+    return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, Cfg2<BN>::kSmem, bt, 2 * pairs, stream,
+                        "gemm_tc2_kernel");
   }
-  const int64_t tiles = static_cast<int64_t>((M + 255) / 256) * ((N + BN - 1) / BN);
-  const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
-  int64_t pairs = std::min<int64_t>(tiles * splits, std::max(1, cap / 2));
-  hap::launch_k(kern, dim3(static_cast<int>(2 * pairs)), dim3(kThreads), G::kSmem, stream, 
-      ma, mb, mc, static_cast<OutT*>(C), ldc, M, N, K, accumulate, vec_ok, splits, kb_per_split, mode);
-  return launch_status("gemm_tc2_kernel");
+  return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, std::min(bt.total_units, cap),
+                      stream, "gemm_tc_kernel");
 }
 
-template <int BN, typename OutT>
-hap_status dispatch_major2(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
-                           const CUtensorMap& mc, int mode, void* C,
-                           int64_t ldc, int M, int N, int K, int acc, int vec, int cap, int sp, int kps,
-                           cudaStream_t s) {
-  if (!amn && !bmn) return launch2<BN, false, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (!amn && bmn) return launch2<BN, false, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (amn && !bmn) return launch2<BN, true, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  return launch2<BN, true, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
+template <typename OutT>
+hap_status launch_dispatch(bool pair, int bn, bool amn, bool bmn, const TcBatch& bt, int cap, cudaStream_t s) {
+#define HAP_TC_CASE(BNV, A, B) \
+  if (bn == BNV && amn == A && bmn == B) return launch_shape<BNV, A, B, OutT>(pair, bt, cap, s);
+  HAP_TC_CASE(256, false, false) HAP_TC_CASE(256, false, true) HAP_TC_CASE(256, true, false)
+  HAP_TC_CASE(256, true, true) HAP_TC_CASE(128, false, false) HAP_TC_CASE(128, false, true)
+  HAP_TC_CASE(128, true, false) HAP_TC_CASE(128, true, true)
+#undef HAP_TC_CASE
+  set_error("gemm: unsupported tile shape");
+  return HAP_ERR_UNSUPPORTED;
 }
 
-template <int BN, typename OutT>
-hap_status dispatch_major(bool amn, bool bmn, const CUtensorMap& ma, const CUtensorMap& mb,
-                          const CUtensorMap& mc, int mode, void* C, int64_t ldc, int M, int N, int K, int acc, int vec, int cap,
-                          int sp, int kps, cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (!amn && bmn) return launch<BN, false, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  if (amn && !bmn) return launch<BN, true, false, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-  return launch<BN, true, true, OutT>(ma, mb, mc, mode, C, ldc, M, N, K, acc, vec, cap, sp, kps, s);
-}
-
-// Tile width and split-K factor: maximise the fraction of the (capped) SMs
-// kept busy over the rounds of a persistent launch.  BN=128 tiles are
-// smem-bandwidth bound on one SM (8 KB of operands per 64-cycle MMA), so they
-// are discounted; split-K (fp32 output only, partials reduced in L2) fills
-// the GPU for the weight-gradient GEMMs, whose M x N is small and K = tokens.
+// Tile shape of a batch: single-CTA 128 x BN or SM-pair 256 x BN
+// (cta_group::2), BN in {128, 256}, plus a split-K factor (fp32 output, one
+// problem).  Each candidate is scored by the fraction of the capped SMs kept
+// busy across the persistent rounds, times a per-shape efficiency (operand
+// bytes per MMA: the pair tile halves B traffic per SM; 128-wide tiles are
+// smem-bandwidth bound).
 struct Shape {
   int bn, splits, kb_per_split;
   bool pair;
 };
 
-// Tile shape: single-CTA 128 x BN or SM-pair 256 x BN (cta_group::2), BN in
-// {128, 256}, and a split-K factor (fp32 output only).  Each candidate is
-// scored by the fraction of the capped SMs kept busy across the persistent
-// rounds, times a per-shape efficiency (operand bytes per MMA: the pair tile
-// halves B traffic per SM; 128-wide tiles are smem-bandwidth bound).
-Shape choose_shape(int64_t M, int64_t N, int64_t K, bool fp32_out, int cap, int allow_pair) {
-  const int64_t k_blocks = (K + BK - 1) / BK;
+Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool fp32_out,
+                   int cap, int allow_pair) {
+  int64_t k_blocks = 0;
+  for (int q = 0; q < (sum_k ? count : 1); ++q) k_blocks += (Ks[q] + BK - 1) / BK;
   Shape best{256, 1, static_cast<int>(k_blocks), false};
   double best_score = -1.0;
   struct Cand { bool pair; int bn; double weight; };
   const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.88}, {false, 256, 0.8}, {false, 128, 0.7}};
+  int64_t min_m = Ms[0];
+  for (int q = 0; q < count; ++q) min_m = std::min(min_m, Ms[q]);
   for (const Cand& c : cands) {
-    if (c.pair && (!allow_pair || M < 256 || cap < 2)) continue;
+    if (c.pair && (!allow_pair || min_m < 256 || cap < 2)) continue;
     const int64_t rows = c.pair ? 256 : 128;
     const int64_t slots = c.pair ? cap / 2 : cap;
-    const int64_t tiles = ((M + rows - 1) / rows) * ((N + c.bn - 1) / c.bn);
+    int64_t tiles = 0;
+    for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
     int64_t splits = 1;
-    if (fp32_out && tiles < slots && k_blocks >= 8) {
+    if (fp32_out && count == 1 && tiles < slots && k_blocks >= 8) {
       splits = std::min<int64_t>(slots / tiles, k_blocks / 4);
       if (splits < 1) splits = 1;
     }
@@ -992,75 +1028,158 @@ extern "C" int hap_matmul_engine(const void* A, int64_t lda, int transA, const v
                                                                          : HAP_GEMM_SIMT;
 }
 
-extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B,
-                                 int64_t ldb, int transB, void* C, int64_t ldc, int64_t M,
-                                 int64_t N, int64_t K, hap_dtype in_dtype, hap_dtype out_dtype,
-                                 int accumulate, int sm_cap, void* stream_) {
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
-  HAP_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, "hap_matmul: negative extent");
-  if (M == 0 || N == 0) return HAP_OK;  // zero-size shard: nothing to compute
-  HAP_CHECK_ARG(C != nullptr, "hap_matmul: null output");
-  if (K == 0) {
-    if (accumulate) return HAP_OK;
-    // C = 0 for an empty contraction (a zero-extent shard on the K axis).
-    const size_t osz = dtype_size(out_dtype);
-    HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * osz, 0, N * osz, M, stream));
-    return HAP_OK;
+namespace {
+
+// Build and launch one tcgen05 batch (all problems tc-eligible, same
+// orientation, <= kMaxProblems).  sum_k: every problem adds into problem 0's
+// output (same C, M, N), accumulate taken from problem 0.
+hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_dtype, int sm_cap,
+                    cudaStream_t stream) {
+  const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
+  int64_t Ms[tc::kMaxProblems], Ns[tc::kMaxProblems], Ks[tc::kMaxProblems];
+  for (int q = 0; q < count; ++q) {
+    Ms[q] = d[q].M;
+    Ns[q] = d[q].N;
+    Ks[q] = d[q].K;
   }
-  HAP_CHECK_ARG(A != nullptr && B != nullptr, "hap_matmul: null operand");
-  if (tc_eligible(A, lda, transA, B, ldb, transB, M, N, K, in_dtype)) {
-    const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
-    const tc::Shape shp = tc::choose_shape(M, N, K, out_dtype == HAP_F32, cap, pair_mode());
-    const int BN = shp.bn;
-    const int b_box = shp.pair ? BN / 2 : BN;   // B columns one CTA stages (K-major box)
-    CUtensorMap ma, mb;
-    bool ok = transA ? tc::make_map(&ma, A, M, K, lda, tc::BK)
-                     : tc::make_map(&ma, A, K, M, lda, tc::BM);
-    ok = ok && (transB ? tc::make_map(&mb, B, K, N, ldb, b_box) : tc::make_map(&mb, B, N, K, ldb, tc::BK));
+  const bool fp32 = out_dtype == HAP_F32;
+  const tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, fp32, cap, pair_mode());
+  const int rows = shp.pair ? 256 : tc::BM;
+  const int b_box = shp.pair ? shp.bn / 2 : shp.bn;
+  const bool amn = d[0].transA != 0, bmn = d[0].transB == 0;
+  const size_t osz = dtype_size(out_dtype);
+  tc::TcBatch bt;
+  std::memset(&bt, 0, sizeof(bt));
+  bt.count = count;
+  bt.sum_k = sum_k;
+  int units = 0;
+  for (int q = 0; q < count; ++q) {
+    tc::TcProblem& pr = bt.p[q];
+    const hap_gemm_desc& g = d[q];
+    bool ok = g.transA ? tc::make_map(&pr.a, g.A, g.M, g.K, g.lda, tc::BK) : tc::make_map(&pr.a, g.A, g.K, g.M, g.lda, tc::BM);
+    ok = ok && (g.transB ? tc::make_map(&pr.b, g.B, g.K, g.N, g.ldb, b_box) : tc::make_map(&pr.b, g.B, g.N, g.K, g.ldb, tc::BK));
     HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout");
-    const bool amn = transA != 0, bmn = transB == 0;
-    const size_t osz = dtype_size(out_dtype);
-    const int vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc * osz) % 16 == 0);
-    const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-    const int sp = shp.splits, kps = shp.kb_per_split;
+    const tc::TcProblem& owner = bt.p[0];
+    const hap_gemm_desc& out = sum_k ? d[0] : g;
+    pr.C = out.C;
+    pr.ldc = out.ldc;
+    pr.M = static_cast<int>(out.M);
+    pr.N = static_cast<int>(out.N);
+    pr.K = static_cast<int>(g.K);
+    pr.m_tiles = static_cast<int>((out.M + rows - 1) / rows);
+    pr.n_tiles = static_cast<int>((out.N + shp.bn - 1) / shp.bn);
+    pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
+    pr.splits = count == 1 ? shp.splits : 1;
+    pr.kb_per_split = count == 1 ? shp.kb_per_split : pr.k_blocks;
+    pr.accumulate = out.accumulate;
+    pr.vec_ok = ((reinterpret_cast<uintptr_t>(out.C) & 15) == 0) && ((out.ldc * osz) % 16 == 0);
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
     // accumulation and split-K partials use TMA reduce-add; a bf16
     // accumulate (read-modify-round) stays on per-thread stores.
-    CUtensorMap mc;
-    int mode = tc::EPI_DIRECT;
-    const bool fp32 = out_dtype == HAP_F32;
-    if (vec && tma_epilogue() && (!accumulate || fp32) && tc::make_map_c(&mc, C, out_dtype, N, M, ldc))
-      mode = (fp32 && (accumulate || sp > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
-    if (mode == tc::EPI_DIRECT) std::memset(&mc, 0, sizeof(mc));
-    if (shp.pair) {
-      if (out_dtype == HAP_BF16)
-        return BN == 256 ? tc::dispatch_major2<256, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate,
-                                                                   vec, sm_cap, 1, kps, stream)
-                         : tc::dispatch_major2<128, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate,
-                                                                   vec, sm_cap, 1, kps, stream);
-      if (sp > 1 && !accumulate)
-        HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, stream));
-      return BN == 256 ? tc::dispatch_major2<256, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate, vec,
-                                                         sm_cap, sp, kps, stream)
-                       : tc::dispatch_major2<128, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k, accumulate, vec,
-                                                         sm_cap, sp, kps, stream);
-    }
-    if (out_dtype == HAP_BF16) {
-      return BN == 256
-                 ? tc::dispatch_major<256, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
-                                                          accumulate, vec, sm_cap, 1, kps, stream)
-                 : tc::dispatch_major<128, __nv_bfloat16>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
-                                                          accumulate, vec, sm_cap, 1, kps, stream);
-    }
-    if (sp > 1 && !accumulate)  // split-K partials add into a zeroed output
-      HAP_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, stream));
-    return BN == 256 ? tc::dispatch_major<256, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
-                                                      accumulate, vec, sm_cap, sp, kps, stream)
-                     : tc::dispatch_major<128, float>(amn, bmn, ma, mb, mc, mode, C, ldc, m, n, k,
-                                                      accumulate, vec, sm_cap, sp, kps, stream);
+    pr.epi_mode = tc::EPI_DIRECT;
+    if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
+        tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc))
+      pr.epi_mode = (fp32 && (pr.accumulate || pr.splits > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
+    pr.unit_begin = units;
+    if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
+    (void)owner;
   }
+  bt.total_units = units;
+  if (count == 1 && shp.splits > 1 && !d[0].accumulate)  // split-K partials add into a zeroed output
+    HAP_CUDA_TRY(cudaMemset2DAsync(d[0].C, d[0].ldc * osz, 0, d[0].N * osz, d[0].M, stream));
+  return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
+              : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+}
+
+hap_status simt_one(const hap_gemm_desc& g, hap_dtype in_dtype, hap_dtype out_dtype, int sm_cap,
+                    cudaStream_t stream) {
   return HAP_DISPATCH_IO(in_dtype, out_dtype, [&] {
-    return simt_launch<Tin, Tout>(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, accumulate,
-                                  sm_cap, stream);
+    return simt_launch<Tin, Tout>(g.A, g.lda, g.transA, g.B, g.ldb, g.transB, g.C, g.ldc, g.M, g.N, g.K,
+                                  g.accumulate, sm_cap, stream);
   });
+}
+
+// Degenerate extents: M or N zero -> nothing; K zero -> C = 0 (or unchanged).
+bool degenerate(const hap_gemm_desc& g, hap_dtype out_dtype, cudaStream_t stream, hap_status* st) {
+  if (g.M == 0 || g.N == 0) {
+    *st = HAP_OK;
+    return true;
+  }
+  if (g.K == 0) {
+    *st = HAP_OK;
+    if (!g.accumulate) {
+      const size_t osz = dtype_size(out_dtype);
+      if (cudaMemset2DAsync(g.C, g.ldc * osz, 0, g.N * osz, g.M, stream) != cudaSuccess) {
+        set_error("hap_matmul: cudaMemset2DAsync failed");
+        *st = HAP_ERR_CUDA;
+      }
+    }
+    return true;
+  }
+  return false;
+}
+
+}  // namespace
+
+extern "C" hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
+                                       hap_dtype out_dtype, int sm_cap, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  HAP_CHECK_ARG(descs && count >= 0, "hap_matmul_batch: bad arguments");
+  for (int q = 0; q < count; ++q) {
+    HAP_CHECK_ARG(descs[q].M >= 0 && descs[q].N >= 0 && descs[q].K >= 0, "hap_matmul: negative extent");
+    HAP_CHECK_ARG(descs[q].C != nullptr || descs[q].M == 0 || descs[q].N == 0, "hap_matmul: null output");
+    if (sum_k)
+      HAP_CHECK_ARG(descs[q].C == descs[0].C && descs[q].M == descs[0].M && descs[q].N == descs[0].N &&
+                        descs[q].ldc == descs[0].ldc,
+                    "hap_matmul_batch: sum_k problems must share their output");
+  }
+  // Batchable: every problem tcgen05-eligible, one orientation, non-degenerate.
+  bool batch = count > 0;
+  for (int q = 0; q < count && batch; ++q) {
+    const hap_gemm_desc& g = descs[q];
+    batch = g.M > 0 && g.N > 0 && g.K > 0 && g.transA == descs[0].transA && g.transB == descs[0].transB &&
+            tc_eligible(g.A, g.lda, g.transA, g.B, g.ldb, g.transB, g.M, g.N, g.K, in_dtype);
+  }
+  if (batch) {
+    for (int q0 = 0; q0 < count; q0 += tc::kMaxProblems) {
+      const int n = std::min(tc::kMaxProblems, count - q0);
+      if (sum_k && q0 > 0) {  // later chunks of a sum accumulate into the first chunk's result
+        hap_gemm_desc tmp[tc::kMaxProblems];
+        for (int i = 0; i < n; ++i) {
+          tmp[i] = descs[q0 + i];
+          tmp[i].accumulate = 1;
+        }
+        hap_status st = tc_batch(tmp, n, 1, out_dtype, sm_cap, stream);
+        if (st != HAP_OK) return st;
+      } else {
+        hap_status st = tc_batch(descs + q0, n, sum_k, out_dtype, sm_cap, stream);
+        if (st != HAP_OK) return st;
+      }
+    }
+    return HAP_OK;
+  }
+  // Otherwise one problem at a time (still on the GPU: tcgen05 or SIMT each).
+  for (int q = 0; q < count; ++q) {
+    hap_gemm_desc g = descs[q];
+    if (sum_k && q > 0) g.accumulate = 1;
+    hap_status st;
+    if (degenerate(g, out_dtype, stream, &st)) {
+      if (st != HAP_OK) return st;
+      continue;
+    }
+    HAP_CHECK_ARG(g.A != nullptr && g.B != nullptr, "hap_matmul: null operand");
+    if (tc_eligible(g.A, g.lda, g.transA, g.B, g.ldb, g.transB, g.M, g.N, g.K, in_dtype))
+      st = tc_batch(&g, 1, 0, out_dtype, sm_cap, stream);
+    else
+      st = simt_one(g, in_dtype, out_dtype, sm_cap, stream);
+    if (st != HAP_OK) return st;
+  }
+  return HAP_OK;
+}
+
+extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B, int64_t ldb, int transB,
+                                 void* C, int64_t ldc, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype,
+                                 hap_dtype out_dtype, int accumulate, int sm_cap, void* stream) {
+  hap_gemm_desc g{A, lda, transA, B, ldb, transB, C, ldc, M, N, K, accumulate};
+  return hap_matmul_batch(&g, 1, 0, in_dtype, out_dtype, sm_cap, stream);
 }

@@ -140,6 +140,7 @@ class ExecConfig:
     input_grads: bool = False         # also differentiate w.r.t. placeholders
     cluster: object = None            # ClusterSpec for the cost-model choices
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
+    batch_gemms: bool = True          # merge runs of matmuls into batched launches
 
 
 @dataclass
@@ -148,6 +149,7 @@ class Op:
     args: tuple
     what: str
     kernel: bool = True               # launches one of our kernels (vs NCCL / memcpy)
+    gemm: dict | None = None          # matmul record (for launch batching)
 
 
 # ---------------------------------------------------------------------------- executor
@@ -195,6 +197,9 @@ class Executor:
         self._symm = None
         self._compile_forward()
         self._compile_backward()
+        if self.cfg.batch_gemms:
+            self.ops_fwd[:] = self._batch_gemms(self.ops_fwd)
+            self.ops_bwd[:] = self._batch_gemms(self.ops_bwd)
         self._create_symm()
 
     # ------------------------------------------------------------------ analysis
@@ -360,6 +365,10 @@ class Executor:
         b = self._as(b, in_dt, cap)
         self._emit("hap_matmul", a.ptr, a.shape[1], int(trans_a), b.ptr, b.shape[1], int(trans_b),
                    c.ptr, c.shape[1], am, bn, ak, in_dt, c.dtype, accumulate, cap, self._sptr())
+        self._ops[-1].gemm = dict(A=a.ptr, lda=a.shape[1], transA=int(trans_a), B=b.ptr, ldb=b.shape[1],
+                                  transB=int(trans_b), C=c.ptr, ldc=c.shape[1], M=am, N=bn, K=ak,
+                                  accumulate=accumulate, in_dt=in_dt, out_dt=c.dtype, cap=cap,
+                                  stream=self._sptr())
 
     # ------------------------------------------------------------------ collectives
     # Every collective maps per-device source buffers to per-device outputs with
@@ -557,6 +566,93 @@ class Executor:
         dist.all_gather_object(handles, bytes(handle.raw))
         check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
         self._symm = ctx
+
+    def _batch_gemms(self, ops: list) -> list:
+        """Merge runs of consecutive matmul launches into hap_matmul_batch
+        launches: matmuls adding into one output (the adjoint contributions of
+        an activation with several consumers) become one K-concatenated GEMM;
+        independent matmuls sharing an input (Q/K/V projections, their weight
+        gradients) share one persistent launch.  An op joins a group only if
+        nothing it reads or writes is touched by the ops it is moved past."""
+        out: list = []
+        i = 0
+        while i < len(ops):
+            if ops[i].gemm is None:
+                out.append(ops[i])
+                i += 1
+                continue
+            j = i
+            while j < len(ops) and ops[j].gemm is not None:
+                j += 1
+            out.extend(self._group_run(ops[i:j]))
+            i = j
+        return out
+
+    def _group_run(self, run: list) -> list:
+        def reads(g):
+            r = {g["A"], g["B"]}
+            if g["accumulate"]:
+                r.add(g["C"])
+            return r
+
+        def compatible(a, b):
+            keys = ("transA", "transB", "in_dt", "out_dt", "cap", "stream")
+            return all(a[k] == b[k] for k in keys)
+
+        placed = [False] * len(run)
+        result = []
+        for i, op in enumerate(run):
+            if placed[i]:
+                continue
+            g0 = op.gemm
+            members = [i]
+            placed[i] = True
+            sum_k = False
+            for j in range(i + 1, len(run)):
+                if placed[j]:
+                    continue
+                gj = run[j].gemm
+                if not compatible(g0, gj):
+                    continue
+                same_out = gj["C"] == g0["C"]
+                if same_out:
+                    if not (gj["accumulate"] and (gj["M"], gj["N"], gj["ldc"]) == (g0["M"], g0["N"], g0["ldc"])):
+                        continue
+                    if len(members) > 1 and not sum_k:
+                        continue
+                elif sum_k or any(run[m].gemm["C"] in reads(gj) for m in members) or \
+                        any(gj["C"] in reads(run[m].gemm) for m in members):
+                    continue
+                # the ops skipped over (not in the group, not yet placed) must not conflict
+                between = [k for k in range(i + 1, j) if not placed[k] and k not in members]
+                conflict = False
+                for k in between:
+                    gk = run[k].gemm
+                    if gk["C"] in reads(gj) or gj["C"] in reads(gk) or gk["C"] == gj["C"]:
+                        conflict = True
+                        break
+                if conflict:
+                    continue
+                if same_out:
+                    sum_k = True
+                members.append(j)
+                placed[j] = True
+                if len(members) == 4:
+                    break
+            if len(members) == 1:
+                result.append(op)
+                continue
+            descs = (_lib.GemmDesc * len(members))()
+            for slot, m in enumerate(members):
+                g = run[m].gemm
+                descs[slot] = _lib.GemmDesc(g["A"], g["lda"], g["transA"], g["B"], g["ldb"], g["transB"], g["C"],
+                                            g["ldc"], g["M"], g["N"], g["K"], g["accumulate"])
+            self._keep(descs)
+            result.append(Op(self.lib.hap_matmul_batch, (descs, len(members), int(sum_k), g0["in_dt"],
+                                                         g0["out_dt"], g0["cap"], g0["stream"]),
+                             "hap_matmul_batch", True,
+                             dict(g0, members=[run[m].gemm for m in members], sum_k=sum_k)))
+        return result
 
     def _keep(self, obj):
         self.__dict__.setdefault("_keepalive", []).append(obj)

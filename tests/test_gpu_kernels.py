@@ -186,3 +186,38 @@ def test_sgd_multi_tensor():
     torch.cuda.synchronize()
     for m, w, ref in zip(masters, weights, want):
         assert torch.allclose(m, ref) and torch.equal(w, ref.to(torch.bfloat16))
+
+
+def _desc(a, ta, b, tb, c, acc=0):
+    M, K = (a.shape[1], a.shape[0]) if ta else a.shape
+    N = b.shape[0] if tb else b.shape[1]
+    return _lib.GemmDesc(a.data_ptr(), a.shape[1], ta, b.data_ptr(), b.shape[1], tb, c.data_ptr(), c.shape[1],
+                         M, N, K, acc)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+@pytest.mark.parametrize("out", [torch.bfloat16, torch.float32])
+def test_matmul_batch_grouped_and_summed(ta, tb, out):
+    torch.manual_seed(11)
+    M, N, K = 1024, 768, 512
+    mk = lambda r, c: torch.randn(r, c, device=DEV).to(torch.bfloat16)  # noqa: E731
+    # grouped: three independent problems sharing A
+    a = mk(K, M) if ta else mk(M, K)
+    bs = [mk(N, K) if tb else mk(K, N) for _ in range(3)]
+    cs = [torch.empty(M, N, device=DEV, dtype=out) for _ in range(3)]
+    descs = (_lib.GemmDesc * 3)(*[_desc(a, ta, b, tb, c) for b, c in zip(bs, cs)])
+    check(L.hap_matmul_batch(descs, 3, 0, BF16, _dt(cs[0]), 0, S))
+    torch.cuda.synchronize()
+    tol = 1e-5 if out == torch.float32 else 8e-3
+    for b, c in zip(bs, cs):
+        assert rel_err(c, ref_mm(a, ta, b, tb)) < tol
+    # summed: C = sum_i A_i . B_i (+ C), five problems (chunked 4 + 1)
+    As = [mk(K, M) if ta else mk(M, K) for _ in range(5)]
+    Bs = [mk(N, K) if tb else mk(K, N) for _ in range(5)]
+    c = torch.randn(M, N, device=DEV).to(out)
+    base = c.float().clone()
+    descs = (_lib.GemmDesc * 5)(*[_desc(x, ta, y, tb, c, acc=1) for x, y in zip(As, Bs)])
+    check(L.hap_matmul_batch(descs, 5, 1, BF16, _dt(c), 0, S))
+    torch.cuda.synchronize()
+    want = base + sum(ref_mm(x, ta, y, tb) for x, y in zip(As, Bs))
+    assert rel_err(c, want) < (1e-5 if out == torch.float32 else 1.2e-2)
