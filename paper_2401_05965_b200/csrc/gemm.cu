@@ -881,7 +881,7 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
     int64_t tiles = 0;
     for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
     int64_t splits = 1;
-    if (fp32_out && count == 1 && tiles < slots && k_blocks >= 8) {
+    if (fp32_out && count == 1 && !sum_k && tiles < slots && k_blocks >= 8) {
       splits = std::min<int64_t>(slots / tiles, k_blocks / 4);
       if (splits < 1) splits = 1;
     }
@@ -1069,8 +1069,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.m_tiles = static_cast<int>((out.M + rows - 1) / rows);
     pr.n_tiles = static_cast<int>((out.N + shp.bn - 1) / shp.bn);
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
-    pr.splits = count == 1 ? shp.splits : 1;
-    pr.kb_per_split = count == 1 ? shp.kb_per_split : pr.k_blocks;
+    const bool split_ok = count == 1 && !sum_k;   // a sum walks every problem's K blocks
+    pr.splits = split_ok ? shp.splits : 1;
+    pr.kb_per_split = split_ok ? shp.kb_per_split : pr.k_blocks;
     pr.accumulate = out.accumulate;
     pr.vec_ok = ((reinterpret_cast<uintptr_t>(out.C) & 15) == 0) && ((out.ldc * osz) % 16 == 0);
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
@@ -1085,7 +1086,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     (void)owner;
   }
   bt.total_units = units;
-  if (count == 1 && shp.splits > 1 && !d[0].accumulate)  // split-K partials add into a zeroed output
+  if (bt.p[0].splits > 1 && !d[0].accumulate)  // split-K partials add into a zeroed output
     HAP_CUDA_TRY(cudaMemset2DAsync(d[0].C, d[0].ldc * osz, 0, d[0].N * osz, d[0].M, stream));
   return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
               : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
