@@ -103,6 +103,22 @@ hap_status hap_mul_grad(const void* a, const void* b, hap_dtype in_dtype, const 
                         hap_dtype dy_dtype, void* da, void* db, hap_dtype d_dtype, int64_t n,
                         int accumulate, int sm_cap, void* stream);
 
+/* Fused elementwise chains (all buffers one dtype, n elements, 16-byte
+ * aligned) — the same arithmetic and roundings as the unfused instructions:
+ *   swish: y = f(x); z = x*y           (elemwise_unary then elemwise_binary mul)
+ *   gate:  p = a*b; q = f(p); o = q*c  (mul, unary, mul)
+ * Backward: dx (+)= dz*y + (dz*x)*f'(x,y); and dc (+)= do*q,
+ * dp = (do*c)*f'(p,q), da (+)= dp*b, db (+)= dp*a (NULL grads are skipped). */
+hap_status hap_swish_fwd(int tag, const void* x, void* y, void* z, hap_dtype dtype, int64_t n, int sm_cap,
+                         void* stream);
+hap_status hap_swish_bwd(int tag, const void* x, const void* y, const void* dz, void* dx, hap_dtype dtype,
+                         int64_t n, int accumulate, int sm_cap, void* stream);
+hap_status hap_gate_fwd(int tag, const void* a, const void* b, const void* c, void* p, void* q, void* o,
+                        hap_dtype dtype, int64_t n, int sm_cap, void* stream);
+hap_status hap_gate_bwd(int tag, const void* a, const void* b, const void* c, const void* p, const void* q,
+                        const void* dout, void* da, void* db, void* dc, hap_dtype dtype, int64_t n, int acc_a,
+                        int acc_b, int acc_c, int sm_cap, void* stream);
+
 /* reduce — interpreter.py:149-150 (np.sum over `dims`).  x has `rank` dims
  * given by `shape`; bit d of dims_mask selects axis d.  y is fp32 or bf16 in
  * the shape with the reduced axes removed; accumulation is fp32. */

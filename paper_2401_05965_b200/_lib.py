@@ -45,6 +45,11 @@ SIGNATURES = {
     "hap_unary_grad": (c_int, [c_int, _P, _P, c_int, _P, c_int, _P, c_int, c_int64, c_int, c_int, _P]),
     "hap_binary": (c_int, [c_int, _P, _P, c_int, _P, c_int, c_int64, c_int, _P]),
     "hap_mul_grad": (c_int, [_P, _P, c_int, _P, c_int, _P, _P, c_int, c_int64, c_int, c_int, _P]),
+    "hap_swish_fwd": (c_int, [c_int, _P, _P, _P, c_int, c_int64, c_int, _P]),
+    "hap_swish_bwd": (c_int, [c_int, _P, _P, _P, _P, c_int, c_int64, c_int, c_int, _P]),
+    "hap_gate_fwd": (c_int, [c_int, _P, _P, _P, _P, _P, _P, c_int, c_int64, c_int, _P]),
+    "hap_gate_bwd": (c_int, [c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int, c_int64, c_int, c_int, c_int,
+                             c_int, _P]),
     "hap_reduce": (c_int, [_P, c_int, _I64P, c_int, c_uint32, _P, c_int, c_int, c_int, _P]),
     "hap_unreduce": (c_int, [_P, c_int, _I64P, c_int, c_uint32, _P, c_int, c_int, c_int, _P]),
     "hap_copy_block": (c_int, [_P, c_int, c_int64, c_int64, _P, c_int, c_int64, c_int64, c_int64,

@@ -541,3 +541,229 @@ extern "C" hap_status hap_sgd_multi(const void* tensors, int count, int64_t tota
     hap::launch_k(sgd_multi_kernel<float>, dim3(grid), dim3(kBlock), 0, stream, ts, count, total_chunks, lr);
   return launch_status("sgd_multi_kernel");
 }
+
+// ---------------------------------------------------------------- fused chains
+// Elementwise chains the executor recognises in a program (all operands one
+// dtype, same shape):
+//   swish: y = f(x); z = x * y                    (f1 -> sigmoid -> mul)
+//   gate:  p = a * b; q = f(p); o = q * c         (q*k -> sigmoid -> *v)
+// Forward kernels read each input once and write every intermediate the
+// program names (the backward reads them); backward kernels fuse the chain's
+// adjoints and skip the gradients of the chain-internal tensors, which have
+// no other consumer.
+namespace hap {
+namespace {
+
+template <int tag, typename T>
+__global__ void __launch_bounds__(kBlock) swish_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                           T* __restrict__ z, int64_t n) {
+  hap::pdl_enter();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nv = n / 8;
+  for (int64_t i = tid; i < nv; i += stride) {
+    float v[8], fy[8], fz[8];
+    Vec8<T>::load(x + 8 * i, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      fy[j] = to_f32(from_f32<T>(unary_fwd(tag, v[j])));   // z uses the stored (rounded) y
+      fz[j] = v[j] * fy[j];
+    }
+    Vec8<T>::store(y + 8 * i, fy);
+    Vec8<T>::store(z + 8 * i, fz);
+  }
+  for (int64_t i = nv * 8 + tid; i < n; i += stride) {
+    const float v = to_f32(x[i]);
+    const T yt = from_f32<T>(unary_fwd(tag, v));
+    y[i] = yt;
+    z[i] = from_f32<T>(v * to_f32(yt));
+  }
+}
+
+// dx (+)= dz * y + (dz * x) * f'(x, y)
+template <int tag, typename T>
+__global__ void __launch_bounds__(kBlock) swish_bwd_kernel(const T* __restrict__ x, const T* __restrict__ y,
+                                                           const T* __restrict__ dz, T* dx, int64_t n,
+                                                           int accumulate) {
+  hap::pdl_enter();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nv = n / 8;
+  for (int64_t i = tid; i < nv; i += stride) {
+    float vx[8], vy[8], g[8], o[8] = {};
+    Vec8<T>::load(x + 8 * i, vx);
+    Vec8<T>::load(y + 8 * i, vy);
+    Vec8<T>::load(dz + 8 * i, g);
+    if (accumulate) Vec8<T>::load(dx + 8 * i, o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float dy = to_f32(from_f32<T>(g[j] * vx[j]));   // as the unfused path stores dy
+      o[j] += g[j] * vy[j] + to_f32(from_f32<T>(dy * unary_deriv(tag, vx[j], vy[j])));
+    }
+    Vec8<T>::store(dx + 8 * i, o);
+  }
+  for (int64_t i = nv * 8 + tid; i < n; i += stride) {
+    const float vx = to_f32(x[i]), vy = to_f32(y[i]), g = to_f32(dz[i]);
+    const float dy = to_f32(from_f32<T>(g * vx));
+    float o = g * vy + to_f32(from_f32<T>(dy * unary_deriv(tag, vx, vy)));
+    if (accumulate) o += to_f32(dx[i]);
+    dx[i] = from_f32<T>(o);
+  }
+}
+
+template <int tag, typename T>
+__global__ void __launch_bounds__(kBlock) gate_fwd_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                          const T* __restrict__ c, T* __restrict__ p,
+                                                          T* __restrict__ q, T* __restrict__ o, int64_t n) {
+  hap::pdl_enter();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nv = n / 8;
+  for (int64_t i = tid; i < nv; i += stride) {
+    float va[8], vb[8], vc[8], vp[8], vq[8], vo[8];
+    Vec8<T>::load(a + 8 * i, va);
+    Vec8<T>::load(b + 8 * i, vb);
+    Vec8<T>::load(c + 8 * i, vc);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      vp[j] = to_f32(from_f32<T>(va[j] * vb[j]));
+      vq[j] = to_f32(from_f32<T>(unary_fwd(tag, vp[j])));
+      vo[j] = vq[j] * vc[j];
+    }
+    Vec8<T>::store(p + 8 * i, vp);
+    Vec8<T>::store(q + 8 * i, vq);
+    Vec8<T>::store(o + 8 * i, vo);
+  }
+  for (int64_t i = nv * 8 + tid; i < n; i += stride) {
+    const float vp = to_f32(from_f32<T>(to_f32(a[i]) * to_f32(b[i])));
+    const float vq = to_f32(from_f32<T>(unary_fwd(tag, vp)));
+    p[i] = from_f32<T>(vp);
+    q[i] = from_f32<T>(vq);
+    o[i] = from_f32<T>(vq * to_f32(c[i]));
+  }
+}
+
+// dq = do*c ; dc (+)= do*q ; dp = dq * f'(p, q) ; da (+)= dp*b ; db (+)= dp*a
+template <int tag, typename T>
+__global__ void __launch_bounds__(kBlock)
+    gate_bwd_kernel(const T* __restrict__ a, const T* __restrict__ b, const T* __restrict__ c,
+                    const T* __restrict__ p, const T* __restrict__ q, const T* __restrict__ dout, T* da, T* db,
+                    T* dc, int64_t n, int acc_a, int acc_b, int acc_c) {
+  hap::pdl_enter();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float g = to_f32(dout[i]);
+    const float vq = to_f32(q[i]), vp = to_f32(p[i]);
+    const float dq = to_f32(from_f32<T>(g * to_f32(c[i])));
+    const float dp = to_f32(from_f32<T>(dq * unary_deriv(tag, vp, vq)));
+    if (dc) dc[i] = from_f32<T>(g * vq + (acc_c ? to_f32(dc[i]) : 0.f));
+    if (da) da[i] = from_f32<T>(dp * to_f32(b[i]) + (acc_a ? to_f32(da[i]) : 0.f));
+    if (db) db[i] = from_f32<T>(dp * to_f32(a[i]) + (acc_b ? to_f32(db[i]) : 0.f));
+  }
+}
+
+template <template <int, typename> class K, typename T>
+struct TagTable;
+
+}  // namespace
+}  // namespace hap
+
+namespace {
+// Host dispatch over the unary tag for the fused kernels.
+template <typename F>
+hap_status with_tag(int tag, F&& f) {
+  switch (tag) {
+    case HAP_EXP: return f(std::integral_constant<int, HAP_EXP>{});
+    case HAP_NEG: return f(std::integral_constant<int, HAP_NEG>{});
+    case HAP_RELU: return f(std::integral_constant<int, HAP_RELU>{});
+    case HAP_SIGMOID: return f(std::integral_constant<int, HAP_SIGMOID>{});
+    default: return f(std::integral_constant<int, HAP_TANH>{});
+  }
+}
+bool all_aligned(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return false;
+  return true;
+}
+}  // namespace
+
+extern "C" hap_status hap_swish_fwd(int tag, const void* x, void* y, void* z, hap_dtype dt, int64_t n, int sm_cap,
+                                    void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  HAP_CHECK_ARG(all_aligned({x, y, z}), "hap_swish_fwd: buffers must be 16-byte aligned");
+  return with_tag(tag, [&](auto tc) {
+    constexpr int T = decltype(tc)::value;
+    if (dt == HAP_BF16)
+      launch_k(swish_fwd_kernel<T, __nv_bfloat16>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream,
+               static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), static_cast<__nv_bfloat16*>(z), n);
+    else
+      launch_k(swish_fwd_kernel<T, float>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream,
+               static_cast<const float*>(x), static_cast<float*>(y), static_cast<float*>(z), n);
+    return launch_status("swish_fwd_kernel");
+  });
+}
+
+extern "C" hap_status hap_swish_bwd(int tag, const void* x, const void* y, const void* dz, void* dx, hap_dtype dt,
+                                    int64_t n, int accumulate, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  HAP_CHECK_ARG(all_aligned({x, y, dz, dx}), "hap_swish_bwd: buffers must be 16-byte aligned");
+  return with_tag(tag, [&](auto tc) {
+    constexpr int T = decltype(tc)::value;
+    if (dt == HAP_BF16)
+      launch_k(swish_bwd_kernel<T, __nv_bfloat16>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream,
+               static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(y),
+               static_cast<const __nv_bfloat16*>(dz), static_cast<__nv_bfloat16*>(dx), n, accumulate);
+    else
+      launch_k(swish_bwd_kernel<T, float>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream,
+               static_cast<const float*>(x), static_cast<const float*>(y), static_cast<const float*>(dz),
+               static_cast<float*>(dx), n, accumulate);
+    return launch_status("swish_bwd_kernel");
+  });
+}
+
+extern "C" hap_status hap_gate_fwd(int tag, const void* a, const void* b, const void* c, void* p, void* q, void* o,
+                                   hap_dtype dt, int64_t n, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  HAP_CHECK_ARG(all_aligned({a, b, c, p, q, o}), "hap_gate_fwd: buffers must be 16-byte aligned");
+  return with_tag(tag, [&](auto tc) {
+    constexpr int T = decltype(tc)::value;
+    if (dt == HAP_BF16) {
+      using E = __nv_bfloat16;
+      launch_k(gate_fwd_kernel<T, E>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream, static_cast<const E*>(a),
+               static_cast<const E*>(b), static_cast<const E*>(c), static_cast<E*>(p), static_cast<E*>(q),
+               static_cast<E*>(o), n);
+    } else {
+      launch_k(gate_fwd_kernel<T, float>, dim3(grid_for(n, sm_cap)), dim3(kBlock), 0, stream,
+               static_cast<const float*>(a), static_cast<const float*>(b), static_cast<const float*>(c),
+               static_cast<float*>(p), static_cast<float*>(q), static_cast<float*>(o), n);
+    }
+    return launch_status("gate_fwd_kernel");
+  });
+}
+
+extern "C" hap_status hap_gate_bwd(int tag, const void* a, const void* b, const void* c, const void* p,
+                                   const void* q, const void* dout, void* da, void* db, void* dc, hap_dtype dt,
+                                   int64_t n, int acc_a, int acc_b, int acc_c, int sm_cap, void* stream_) {
+  HAP_STREAM;
+  if (n <= 0) return HAP_OK;
+  return with_tag(tag, [&](auto tc) {
+    constexpr int T = decltype(tc)::value;
+    const int grid = capped_grid((n + kBlock - 1) / kBlock, sm_cap);
+    if (dt == HAP_BF16) {
+      using E = __nv_bfloat16;
+      launch_k(gate_bwd_kernel<T, E>, dim3(grid), dim3(kBlock), 0, stream, static_cast<const E*>(a),
+               static_cast<const E*>(b), static_cast<const E*>(c), static_cast<const E*>(p),
+               static_cast<const E*>(q), static_cast<const E*>(dout), static_cast<E*>(da), static_cast<E*>(db),
+               static_cast<E*>(dc), n, acc_a, acc_b, acc_c);
+    } else {
+      launch_k(gate_bwd_kernel<T, float>, dim3(grid), dim3(kBlock), 0, stream, static_cast<const float*>(a),
+               static_cast<const float*>(b), static_cast<const float*>(c), static_cast<const float*>(p),
+               static_cast<const float*>(q), static_cast<const float*>(dout), static_cast<float*>(da),
+               static_cast<float*>(db), static_cast<float*>(dc), n, acc_a, acc_b, acc_c);
+    }
+    return launch_status("gate_bwd_kernel");
+  });
+}

@@ -141,6 +141,7 @@ class ExecConfig:
     cluster: object = None            # ClusterSpec for the cost-model choices
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
     batch_gemms: bool = True          # merge runs of matmuls into batched launches
+    fuse_elementwise: bool = True     # fuse swish / gate elementwise chains
 
 
 @dataclass
@@ -189,6 +190,8 @@ class Executor:
         self.overlapped: set = set()
         self._grad_ready_at: dict = {}
         self.comm_stream = None
+        self.aliased: set = set()
+        self._n_contrib: dict = {}
         self.bytes_allocated = 0
         self.source_dids = {i.output for i in program.instrs if i.kind in SOURCE_KINDS}
         self._check_program()
@@ -660,9 +663,93 @@ class Executor:
     # ------------------------------------------------------------------ forward
     def _compile_forward(self):
         self._ops = self.ops_fwd
-        for ins in self.program.instrs:
+        self._find_chains()
+        skip: set = set()
+        for idx, ins in enumerate(self.program.instrs):
+            if idx in skip:
+                continue
+            chain = self.chains.get(idx)
+            if chain is not None:
+                self._forward_chain(chain)
+                skip.update(chain["members"][1:])
+                continue
             self._forward_instr(ins)
         self._loss_closure()
+
+    def _find_chains(self):
+        """Elementwise chains fused into one kernel (forward and backward):
+        swish  y = f(x), z = x*y   and   gate  p = a*b, q = f(p), o = q*c,
+        consecutive compute instructions over one dtype and shape.  The
+        backward fusion additionally needs each chain-internal tensor (y; p
+        and q) to have no consumer outside the chain."""
+        self.chains: dict = {}
+        self.chain_of: dict = {}
+        if not self.cfg.fuse_elementwise:
+            return
+        consumers: dict = {}
+        for ins in self.program.instrs:
+            for d in ins.operands:
+                consumers.setdefault(d, []).append(ins)
+        compute = [(i, ins) for i, ins in enumerate(self.program.instrs) if ins.kind not in SOURCE_KINDS]
+        L = self.group.local_ranks
+
+        def uniform(dids):
+            dts = {self.dtypes[d] for d in dids}
+            shapes = {tuple(self.shapes[d][r]) for d in dids for r in L}
+            return len(dts) == 1 and len(shapes) == 1
+
+        used: set = set()
+        for pos, (i, u) in enumerate(compute):
+            if i in used:
+                continue
+            nxt = compute[pos + 1] if pos + 1 < len(compute) else None
+            nxt2 = compute[pos + 2] if pos + 2 < len(compute) else None
+            # swish at a unary instruction
+            if u.kind == "elemwise_unary" and nxt is not None:
+                j, bm = nxt
+                x, y = u.operands[0], u.output
+                if (bm.kind == "elemwise_binary" and bm.tag == "mul" and set(bm.operands) == {x, y} and x != y
+                        and uniform([x, y, bm.output])):
+                    c = {"kind": "swish", "members": [i, j], "u": u, "b": bm, "x": x, "y": y, "z": bm.output,
+                         "bwd": [ins.output for ins in consumers.get(y, [])] == [bm.output]}
+                    self.chains[i] = c
+                    self.chain_of[j] = c
+                    self.chain_of[i] = c
+                    used.update((i, j))
+                    continue
+            # gate at a mul instruction
+            if (u.kind == "elemwise_binary" and u.tag == "mul" and nxt is not None and nxt2 is not None):
+                (j, un), (k, b2) = nxt, nxt2
+                a_, b_ = u.operands
+                p_ = u.output
+                if (un.kind == "elemwise_unary" and un.operands[0] == p_ and b2.kind == "elemwise_binary"
+                        and b2.tag == "mul" and un.output in b2.operands):
+                    q_ = un.output
+                    c_ = b2.operands[1] if b2.operands[0] == q_ else b2.operands[0]
+                    dids = [a_, b_, c_, p_, q_, b2.output]
+                    if len({a_, b_, c_, p_, q_}) == 5 and uniform(dids):
+                        c = {"kind": "gate", "members": [i, j, k], "b1": u, "u": un, "b2": b2, "a": a_, "b": b_,
+                             "c": c_, "p": p_, "q": q_, "o": b2.output,
+                             "bwd": ([ins.output for ins in consumers.get(p_, [])] == [q_]
+                                     and [ins.output for ins in consumers.get(q_, [])] == [b2.output])}
+                        self.chains[i] = c
+                        for m in (i, j, k):
+                            self.chain_of[m] = c
+                        used.update((i, j, k))
+
+    def _forward_chain(self, c: dict):
+        L = self.group.local_ranks
+        B = lambda d, r: self.bufs[(d, r)]  # noqa: E731
+        for r in L:
+            if c["kind"] == "swish":
+                x, y, z = B(c["x"], r), B(c["y"], r), B(c["z"], r)
+                self._emit("hap_swish_fwd", _lib.UNARY_TAGS[c["u"].tag], x.ptr, y.ptr, z.ptr, x.dtype, x.numel,
+                           self.caps[r], self._sptr())
+            else:
+                a, b, cc = B(c["a"], r), B(c["b"], r), B(c["c"], r)
+                p, q, o = B(c["p"], r), B(c["q"], r), B(c["o"], r)
+                self._emit("hap_gate_fwd", _lib.UNARY_TAGS[c["u"].tag], a.ptr, b.ptr, cc.ptr, p.ptr, q.ptr, o.ptr,
+                           a.dtype, a.numel, self.caps[r], self._sptr())
 
     def _forward_instr(self, ins: Instruction):
         k = ins.kind
@@ -764,11 +851,25 @@ class Executor:
         self._plan_sfb()
         self._grad_ready_at: dict = {}
         self.overlapped: set = set()
+        self._count_contributions(seed_did)
+        index = {id(ins): i for i, ins in enumerate(self.program.instrs)}
+        handled: set = set()
         for ins in reversed(self.program.instrs):
             if ins.output not in written or ins.kind in SOURCE_KINDS:
                 continue
             need = [self.req[d] for d in ins.operands]
             if not any(need):
+                continue
+            idx = index[id(ins)]
+            if idx in handled:
+                continue
+            chain = self.chain_of.get(idx)
+            if chain is not None and chain["bwd"] and idx == chain["members"][-1] and self._chain_bwd_ok(chain):
+                self._adjoint_chain(chain, contrib)
+                handled.update(chain["members"])
+                for d in self._chain_inputs(chain):
+                    if d in self.source_dids:
+                        self._grad_ready_at[d] = len(self._ops)
                 continue
             self._adjoint(ins, need, contrib)
             for d in ins.operands:
@@ -776,6 +877,81 @@ class Executor:
                     self._grad_ready_at[d] = len(self._ops)
         self._overlap_grad_sync()
         self._finish_update(written)
+
+    def _chain_bwd_ok(self, c: dict) -> bool:
+        """The fused adjoint keeps one dtype: every input gradient must be
+        stored in the chain's working precision (sources keep fp32 grads)."""
+        dt = self.dtypes[self._chain_inputs(c)[0]]
+        for d in self._chain_inputs(c):
+            if self.req[d] and (d in self.source_dids and dt != F32):
+                return False
+        return all(self.dtypes[d] == dt for d in self._chain_inputs(c))
+
+    @staticmethod
+    def _chain_inputs(c: dict) -> list:
+        return [c["x"]] if c["kind"] == "swish" else [c["a"], c["b"], c["c"]]
+
+    def _adjoint_chain(self, c: dict, contrib):
+        """Fused adjoint of a whole chain: contributions to the chain inputs
+        only (the internal gradients dy / dq, dp are never materialised)."""
+        L = self.group.local_ranks
+        tag = _lib.UNARY_TAGS[c["u"].tag]
+        if c["kind"] == "swish":
+            if not self.req[c["x"]]:
+                return
+            acc = contrib(c["x"])
+            for r in L:
+                x, y = self.bufs[(c["x"], r)], self.bufs[(c["y"], r)]
+                dz, dx = self.grads[(c["z"], r)], self._grad(c["x"], r)
+                self._emit("hap_swish_bwd", tag, x.ptr, y.ptr, dz.ptr, dx.ptr, x.dtype, x.numel, acc, self.caps[r],
+                           self._sptr())
+            return
+        flags = {}
+        for key in ("a", "b", "c"):
+            flags[key] = contrib(c[key]) if self.req[c[key]] else 0
+        for r in L:
+            bf = lambda d: self.bufs[(d, r)]  # noqa: E731
+            grad = lambda key: self._grad(c[key], r).ptr if self.req[c[key]] else None  # noqa: E731
+            a = bf(c["a"])
+            self._emit("hap_gate_bwd", tag, a.ptr, bf(c["b"]).ptr, bf(c["c"]).ptr, bf(c["p"]).ptr, bf(c["q"]).ptr,
+                       self.grads[(c["o"], r)].ptr, grad("a"), grad("b"), grad("c"), a.dtype, a.numel, flags["a"],
+                       flags["b"], flags["c"], self.caps[r], self._sptr())
+
+    def _count_contributions(self, seed_did: str):
+        """How many adjoint contributions each gradient will receive (a dry
+        run of the reverse pass), so a gradient that receives exactly one
+        plain copy can alias its source instead of being copied."""
+        live = {seed_did}
+        self._n_contrib: dict = {}
+        for ins in reversed(self.program.instrs):
+            if ins.output not in live or ins.kind in SOURCE_KINDS:
+                continue
+            need = [self.req[d] for d in ins.operands]
+            if not any(need):
+                continue
+            operands = ins.operands
+            if ins.kind == "elemwise_binary" and ins.tag == "mul" and operands[0] == operands[1]:
+                operands = operands[:1]
+            for d, nd in zip(operands, need):
+                if nd:
+                    self._n_contrib[d] = self._n_contrib.get(d, 0) + 1
+                    live.add(d)
+
+    def _alias_grad(self, did: str, dy: dict) -> bool:
+        """Give grad(did) the buffers of dy when dy is its only contribution
+        (dy is complete and never written again once its adjoint runs)."""
+        L = self.group.local_ranks
+        # sources are excluded: their gradients are synchronised in place
+        if did in self.source_dids or self._n_contrib.get(did) != 1 or any((did, r) in self.grads for r in L):
+            return False
+        if any(dy[r].dtype != (F32 if (self.dtypes[did] == F32 or did in self.source_dids) else self.dtypes[did])
+               for r in L):
+            return False
+        for r in L:
+            self.grads[(did, r)] = dy[r]
+        self._written.add(did)
+        self.aliased.add(did)
+        return True
 
     def _adjoint(self, ins: Instruction, need: list, contrib):
         L = self.group.local_ranks
@@ -806,13 +982,15 @@ class Executor:
                 self._emit("hap_unary_grad", tag, xb.ptr, yb.ptr, yb.dtype, dy[r].ptr, dy[r].dtype,
                            g.ptr, g.dtype, g.numel, acc, self.caps[r], self._sptr())
         elif k == "identity":
+            if self._alias_grad(ops[0], dy):
+                return
             acc = contrib(ops[0])
             for r in L:
                 self._copy(dy[r], self._grad(ops[0], r), self.caps[r], accumulate=acc)
         elif k == "elemwise_binary":
             if ins.tag == "add":
                 for i in (0, 1):
-                    if need[i]:
+                    if need[i] and not (ops[0] != ops[1] and self._alias_grad(ops[i], dy)):
                         acc = contrib(ops[i])
                         for r in L:
                             self._copy(dy[r], self._grad(ops[i], r), self.caps[r], accumulate=acc)
