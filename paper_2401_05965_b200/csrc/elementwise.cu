@@ -651,7 +651,32 @@ __global__ void __launch_bounds__(kBlock)
                     T* dc, int64_t n, int acc_a, int acc_b, int acc_c) {
   hap::pdl_enter();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nv = n / 8;
+  for (int64_t i = tid; i < nv; i += stride) {   // 16-byte vectors (buffers are aligned)
+    float vg[8], vq[8], vp[8], vc[8], va[8], vb[8], oa[8] = {}, ob[8] = {}, oc[8] = {};
+    Vec8<T>::load(dout + 8 * i, vg);
+    Vec8<T>::load(q + 8 * i, vq);
+    Vec8<T>::load(p + 8 * i, vp);
+    Vec8<T>::load(c + 8 * i, vc);
+    Vec8<T>::load(a + 8 * i, va);
+    Vec8<T>::load(b + 8 * i, vb);
+    if (da && acc_a) Vec8<T>::load(da + 8 * i, oa);
+    if (db && acc_b) Vec8<T>::load(db + 8 * i, ob);
+    if (dc && acc_c) Vec8<T>::load(dc + 8 * i, oc);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float dq = to_f32(from_f32<T>(vg[j] * vc[j]));
+      const float dp = to_f32(from_f32<T>(dq * unary_deriv(tag, vp[j], vq[j])));
+      oc[j] += vg[j] * vq[j];
+      oa[j] += dp * vb[j];
+      ob[j] += dp * va[j];
+    }
+    if (dc) Vec8<T>::store(dc + 8 * i, oc);
+    if (da) Vec8<T>::store(da + 8 * i, oa);
+    if (db) Vec8<T>::store(db + 8 * i, ob);
+  }
+  for (int64_t i = nv * 8 + tid; i < n; i += stride) {
     const float g = to_f32(dout[i]);
     const float vq = to_f32(q[i]), vp = to_f32(p[i]);
     const float dq = to_f32(from_f32<T>(g * to_f32(c[i])));
@@ -751,7 +776,8 @@ extern "C" hap_status hap_gate_bwd(int tag, const void* a, const void* b, const 
   if (n <= 0) return HAP_OK;
   return with_tag(tag, [&](auto tc) {
     constexpr int T = decltype(tc)::value;
-    const int grid = capped_grid((n + kBlock - 1) / kBlock, sm_cap);
+    HAP_CHECK_ARG(all_aligned({a, b, c, p, q, dout, da, db, dc}), "hap_gate_bwd: buffers must be 16-byte aligned");
+    const int grid = grid_for(n, sm_cap);
     if (dt == HAP_BF16) {
       using E = __nv_bfloat16;
       launch_k(gate_bwd_kernel<T, E>, dim3(grid), dim3(kBlock), 0, stream, static_cast<const E*>(a),

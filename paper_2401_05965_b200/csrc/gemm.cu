@@ -234,6 +234,13 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 // bulk reduce-add (fp32 accumulate / split-K partials).
 enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2 };
 
+// Byte offset of 16-byte chunk c of row r in a TMA-swizzled staging box.
+template <int kRowBytes>
+__device__ __forceinline__ uint32_t swz_offset(int r, int c) {
+  if constexpr (kRowBytes == 128) return r * 128 + ((c ^ (r & 7)) << 4);
+  else return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+}
+
 // Drain one warp's 32 rows x BN/2 columns of a finished accumulator.
 // TMA modes stage 32 x 128 B boxes (64 bf16 or 32 fp32 columns) in a
 // 128B-swizzled double buffer — 16-byte chunk c of row r at c ^ (r & 7), the
@@ -268,7 +275,11 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
     }
     return;
   }
-  constexpr int W = 128 / static_cast<int>(sizeof(OutT));   // columns per box
+  // Box rows of 128 B (SWIZZLE_128B) when the warp's BN/2 columns split into
+  // them evenly, else 64 B rows (SWIZZLE_64B: chunk c of row r at c ^ (r>>1 & 3)).
+  constexpr int kWide = 128 / static_cast<int>(sizeof(OutT));
+  constexpr int W = ((BN / 2) % kWide == 0) ? kWide : kWide / 2;   // columns per box
+  constexpr int kRowBytes = W * static_cast<int>(sizeof(OutT));
   constexpr int kBoxes = (BN / 2) / W;
   const uint32_t buf0 = smem_u32(buf);
 #pragma unroll 1
@@ -281,9 +292,10 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
       uint32_t r[32];
       tmem_ld32(lane_base + half * (BN / 2) + b * W + k * 32, r);
       if constexpr (std::is_same<OutT, float>::value) {
+        static_assert(W % 32 == 0 || W == 16, "fp32 box width");
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t at = dst + lane * 128 + (((j) ^ (lane & 7)) << 4);
+          const uint32_t at = dst + swz_offset<kRowBytes>(lane, j);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(r[4 * j]), "r"(r[4 * j + 1]),
                        "r"(r[4 * j + 2]), "r"(r[4 * j + 3]));
         }
@@ -297,7 +309,7 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
                                                      __uint_as_float(r[8 * j + 2 * e + 1]));
             p[e] = *reinterpret_cast<uint32_t*>(&h);
           }
-          const uint32_t at = dst + lane * 128 + (((k * 4 + j) ^ (lane & 7)) << 4);
+          const uint32_t at = dst + swz_offset<kRowBytes>(lane, k * 4 + j);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]),
                        "r"(p[3]));
         }
@@ -538,13 +550,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 // leader's full barrier, the leader's commits multicast to both CTAs' empty
 // and TMEM-full barriers, and both epilogues release the accumulator on the
 // leader's TMEM-empty barrier.
-template <int BN>
+// BN in {128, 192, 256}; each CTA stages BN/2 columns of B.  MN-major B is
+// loaded in 64-column TMA boxes, so a 96-column half loads 128 columns (the
+// MMA reads the first 96).
+template <int BN, bool kBMN = false>
 struct Cfg2 {
-  static constexpr int kStages = BN == 256 ? 5 : 6;
+  static constexpr int kHalfLoaded = kBMN ? ((BN / 2 + 63) / 64) * 64 : BN / 2;
+  static constexpr int kStages = BN == 128 ? 6 : 5;
   static constexpr int kABytes = 128 * BK * 2;
-  static constexpr int kBBytes = (BN / 2) * BK * 2;
+  static constexpr int kBBytes = kHalfLoaded * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 256 + 1024;
 };
 
@@ -606,8 +622,8 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {
-  using G = Cfg2<BN>;
-  constexpr int HB = BN / 2;  // B columns staged per CTA
+  using G = Cfg2<BN, kBMN>;
+  constexpr int HB = BN / 2;  // B columns of the tile each CTA supplies
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -680,7 +696,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           if (kBMN) {
 #pragma unroll
-            for (int c = 0; c < HB / 64; ++c) tma_load_2d_pair(sb + c * BK * 128, mb, leader_full, n0 + 64 * c, k0);
+            for (int c = 0; c < G::kHalfLoaded / 64; ++c)
+              tma_load_2d_pair(sb + c * BK * 128, mb, leader_full, n0 + 64 * c, k0);
           } else {
             tma_load_2d_pair(sb, mb, leader_full, k0, n0);
           }
@@ -797,16 +814,19 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, i
 }
 
 // Output tensor map for the TMA epilogue: boxes of 128 bytes x 32 rows.
-bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld) {
+bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld, int bn) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int es = dt == HAP_BF16 ? 2 : 4;
+  const int wide = 128 / es;                               // must match drain_accumulator's W
+  const int w = ((bn / 2) % wide == 0) ? wide : wide / 2;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * es};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(w), 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt == HAP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr,
-                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  w * es == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -832,13 +852,16 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 hap_status launch_shape(bool pair, const TcBatch& bt, int cap, cudaStream_t stream) {
-  if (pair) {
+  if (pair || BN == 192) {   // 192-wide tiles exist only for SM pairs
     const int pairs = std::min<int>(bt.total_units, std::max(1, cap / 2));
-    return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, Cfg2<BN>::kSmem, bt, 2 * pairs, stream,
+    return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, Cfg2<BN, kBMN>::kSmem, bt, 2 * pairs, stream,
                         "gemm_tc2_kernel");
   }
-  return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, std::min(bt.total_units, cap),
-                      stream, "gemm_tc_kernel");
+  if constexpr (BN != 192) {
+    return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, std::min(bt.total_units, cap),
+                        stream, "gemm_tc_kernel");
+  }
+  return HAP_ERR_UNSUPPORTED;
 }
 
 template <typename OutT>
@@ -847,7 +870,8 @@ hap_status launch_dispatch(bool pair, int bn, bool amn, bool bmn, const TcBatch&
   if (bn == BNV && amn == A && bmn == B) return launch_shape<BNV, A, B, OutT>(pair, bt, cap, s);
   HAP_TC_CASE(256, false, false) HAP_TC_CASE(256, false, true) HAP_TC_CASE(256, true, false)
   HAP_TC_CASE(256, true, true) HAP_TC_CASE(128, false, false) HAP_TC_CASE(128, false, true)
-  HAP_TC_CASE(128, true, false) HAP_TC_CASE(128, true, true)
+  HAP_TC_CASE(128, true, false) HAP_TC_CASE(128, true, true) HAP_TC_CASE(192, false, false)
+  HAP_TC_CASE(192, false, true) HAP_TC_CASE(192, true, false) HAP_TC_CASE(192, true, true)
 #undef HAP_TC_CASE
   set_error("gemm: unsupported tile shape");
   return HAP_ERR_UNSUPPORTED;
@@ -871,7 +895,8 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
   Shape best{256, 1, static_cast<int>(k_blocks), false};
   double best_score = -1.0;
   struct Cand { bool pair; int bn; double weight; };
-  const Cand cands[] = {{true, 256, 1.0}, {true, 128, 0.88}, {false, 256, 0.8}, {false, 128, 0.7}};
+  const Cand cands[] = {{true, 256, 1.0}, {true, 192, 0.85}, {true, 128, 0.8}, {false, 256, 0.75},
+                        {false, 128, 0.65}};
   int64_t min_m = Ms[0];
   for (int q = 0; q < count; ++q) min_m = std::min(min_m, Ms[q]);
   for (const Cand& c : cands) {
@@ -881,7 +906,7 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
     int64_t tiles = 0;
     for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
     int64_t splits = 1;
-    if (fp32_out && count == 1 && !sum_k && tiles < slots && k_blocks >= 8) {
+    if (fp32_out && !sum_k && tiles < slots && k_blocks >= 8) {
       splits = std::min<int64_t>(slots / tiles, k_blocks / 4);
       if (splits < 1) splits = 1;
     }
@@ -1069,9 +1094,15 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.m_tiles = static_cast<int>((out.M + rows - 1) / rows);
     pr.n_tiles = static_cast<int>((out.N + shp.bn - 1) / shp.bn);
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
-    const bool split_ok = count == 1 && !sum_k;   // a sum walks every problem's K blocks
-    pr.splits = split_ok ? shp.splits : 1;
-    pr.kb_per_split = split_ok ? shp.kb_per_split : pr.k_blocks;
+    // a sum walks every problem's K blocks; grouped problems may split K
+    // (same factor for all; problems with fewer K blocks get fewer splits)
+    if (!sum_k && shp.splits > 1) {
+      pr.kb_per_split = std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
+      pr.splits = (pr.k_blocks + pr.kb_per_split - 1) / pr.kb_per_split;
+    } else {
+      pr.splits = 1;
+      pr.kb_per_split = pr.k_blocks;
+    }
     pr.accumulate = out.accumulate;
     pr.vec_ok = ((reinterpret_cast<uintptr_t>(out.C) & 15) == 0) && ((out.ldc * osz) % 16 == 0);
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
@@ -1079,15 +1110,16 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     // accumulate (read-modify-round) stays on per-thread stores.
     pr.epi_mode = tc::EPI_DIRECT;
     if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
-        tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc))
+        tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc, shp.bn))
       pr.epi_mode = (fp32 && (pr.accumulate || pr.splits > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
     pr.unit_begin = units;
     if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
     (void)owner;
   }
   bt.total_units = units;
-  if (bt.p[0].splits > 1 && !d[0].accumulate)  // split-K partials add into a zeroed output
-    HAP_CUDA_TRY(cudaMemset2DAsync(d[0].C, d[0].ldc * osz, 0, d[0].N * osz, d[0].M, stream));
+  for (int q = 0; q < (sum_k ? 1 : count); ++q)  // split-K partials add into a zeroed output
+    if (bt.p[q].splits > 1 && !d[q].accumulate)
+      HAP_CUDA_TRY(cudaMemset2DAsync(d[q].C, d[q].ldc * osz, 0, d[q].N * osz, d[q].M, stream));
   return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
               : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
 }

@@ -40,7 +40,7 @@ def rel_err(got, want):
 
 
 SHAPES = [(128, 128, 64), (256, 512, 320), (300, 200, 72), (1000, 520, 1000), (64, 1024, 1024),
-          (4096, 3072, 768), (8, 264, 40)]
+          (4096, 3072, 768), (8, 264, 40), (8192, 768, 3072), (2048, 768, 1024)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)

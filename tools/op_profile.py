@@ -28,11 +28,10 @@ torch.cuda.synchronize()
 agg = collections.defaultdict(lambda: [0, 0.0])
 for op, a, b in zip(ops, evs[:-1], evs[1:]):
     key = op.what
-    if op.what == "hap_matmul":
-        key = f"matmul M={op.args[8]} N={op.args[9]} K={op.args[10]} tA={op.args[2]} tB={op.args[5]} out={'bf16' if op.args[12] else 'f32'}"
-    elif op.what in ("hap_binary", "hap_unary", "hap_axpy", "hap_mul_grad", "hap_unary_grad"):
-        n = [x for x in op.args if isinstance(x, int) and 1000 < x < 1e9]
-        key = f"{op.what} n={n[-1] if n else '?'}"
+    if op.gemm is not None:
+        ms = op.gemm.get("members", [op.gemm])
+        key = (f"{op.what} x{len(ms)}{' sum' if op.gemm.get('sum_k') else ''} M={ms[0]['M']} N={ms[0]['N']} "
+               f"K={ms[0]['K']} tA={ms[0]['transA']} tB={ms[0]['transB']} out={'bf16' if ms[0]['out_dt'] else 'f32'}")
     agg[key][0] += 1
     agg[key][1] += a.elapsed_time(b)
 total = sum(v[1] for v in agg.values())
