@@ -293,9 +293,19 @@ def main() -> None:
                                         m["N"], m["K"], m["in_dt"]) for m in members}
     peaks = _peaks()
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    gemm_bytes = sum(2 * (m["M"] * m["K"] + m["K"] * m["N"]) + m["M"] * m["N"] * (2 if m["out_dt"] else 4)
+                     * (2 if m["accumulate"] else 1) for m in members)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    if n == 1 and os.path.exists(prof):
+        with open(prof) as fh:
+            tr = json.load(fh)
+        traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]
     roofline = {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, all GEMMs of one step)",
                 "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": None,
+                "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
+                "traffic_note": "DRAM bytes per step over all GEMM launches (ncu, profiles/r01_gemm_traffic.json)",
+                "algorithmic_bytes_per_step": gemm_bytes, "gemm_flops_per_step": gemm_flops,
                 "peak_source": peaks["source"] + ", burst (GEMMs timed alone)",
                 "gemm_launches_per_step": len(gemm_ops), "gemms_per_step": len(members),
                 "gemm_ms_per_step": round(gemm_ms, 4),

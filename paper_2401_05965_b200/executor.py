@@ -1251,7 +1251,7 @@ class Executor:
             for mst, g, wb in items:
                 records += struct.pack("<QQQqq", mst.ptr, g.ptr, wb.ptr, mst.numel, chunk)
                 chunk += (mst.numel + 8191) // 8192
-            table = torch.frombuffer(bytes(records), dtype=torch.uint8).to(self.device)
+            table = torch.frombuffer(records, dtype=torch.uint8).to(self.device)
             self._keep(table)
             self._emit("hap_sgd_multi", table.data_ptr(), len(items), chunk, wdt, float(self.cfg.lr),
                        self.caps[r], self._sptr())
