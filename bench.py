@@ -12,6 +12,11 @@ collectives, tcgen05 GEMMs, every kernel grid capped at the rank's SMs.  One
 step = forward + adjoint backward + gradient sync (all-reduce or SFB, cost
 model) + SGD update, replayed as one CUDA graph.
 
+``--workload moe`` runs configs[4] instead: a 12-layer stack of 2-expert SiLU
+FFN mixtures at 2 sequences per GPU, where the cost model picks sufficient-
+factor broadcasting (gather x and dy, rebuild dW locally) at 2 and 4 GPUs and
+all-reduce at 8 (the grad_sync map in ``config`` records each choice).
+
 The printed JSON line follows the driver contract; ``value`` is samples
 (sequences) per second for the whole job with inputs resident in HBM,
 ``e2e`` the same metric through the public API with the batch copied from
@@ -32,8 +37,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEQ = 128
-PER_GPU_BATCH = 64
 LAYERS = 12
+# --workload: graph builder, sequences per GPU, plan-file stem, description.
+WORKLOADS = {
+    "bert": {"per_gpu_batch": 64, "stem": "bert12",
+             "desc": "BERT-base GEMM skeleton (configs[2]): 12 layers, seq 128, hidden 768, FFN 3072, "
+                     "train step fwd+bwd+sync+SGD"},
+    "moe": {"per_gpu_batch": 2, "stem": "moe12",
+            "desc": "BERT-MoE FFN stack (configs[4]): 12 layers x 2 SiLU experts (768->3072->768), seq 128, "
+                    "SFB-vs-all-reduce chosen per weight by the cost model, train step fwd+bwd+sync+SGD"},
+}
+
+
+def _graph(workload: str, batch: int):
+    from paper_2401_05965_b200 import workloads
+    if workload == "moe":
+        return workloads.moe_stack(layers=LAYERS, batch=batch, seq=SEQ)
+    return workloads.bert(layers=LAYERS, batch=batch, seq=SEQ)
 # SGD step size.  The skeleton's loss is the reference's plain sum over
 # batch*seq*768 outputs (unbounded below, gradients ~1e4-1e5 per weight), so
 # the step is chosen to move weights ~1e-5 relative per step: long runs stay
@@ -54,10 +74,11 @@ def _peaks() -> dict:
             "source": "fallback (B200_PROFILING.md)"}
 
 
-def _plan_doc(n: int) -> dict | None:
+def _plan_doc(workload: str, n: int) -> dict | None:
     if n == 1:
         return None
-    path = os.path.join(ROOT, "tests", "golden", "plans", f"bert12_b{PER_GPU_BATCH * n}.b200x{n}.json")
+    w = WORKLOADS[workload]
+    path = os.path.join(ROOT, "tests", "golden", "plans", f"{w['stem']}_b{w['per_gpu_batch'] * n}.b200x{n}.json")
     with open(path) as fh:
         return json.load(fh)
 
@@ -112,7 +133,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(steps: int, sample_batch: int) -> dict:
+def cpu_baseline(steps: int, sample_batch: int, workload: str = "bert") -> dict:
     """Reference CPU path (the oracle port of the reference interpreter plus
     its adjoint, float64 numpy) on a bounded sample of the same workload."""
     import numpy as np
@@ -121,7 +142,7 @@ def cpu_baseline(steps: int, sample_batch: int) -> dict:
     from oracle import interpreter_np as O
     from paper_2401_05965_b200 import api, workloads
 
-    g = workloads.bert(layers=LAYERS, batch=sample_batch, seq=SEQ)
+    g = _graph(workload, sample_batch)
     prog = O.Program(api.single_device_program(g).to_json())
     inputs = workloads.synthetic_inputs(g, 0, scaled=True)
     shapes = {n.id: n.shape for n in g.nodes}
@@ -132,7 +153,7 @@ def cpu_baseline(steps: int, sample_batch: int) -> dict:
     dt = (time.perf_counter() - t0) / steps
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     return {"value": sample_batch / dt, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{steps} train steps (fwd+bwd+SGD, float64) of the 12-layer skeleton at batch "
+            "sample": f"{steps} train steps (fwd+bwd+SGD, float64) of the 12-layer {workload} graph at batch "
                       f"{sample_batch} x seq {SEQ} on one simulated device",
             "seconds_per_step": dt}
 
@@ -140,12 +161,13 @@ def cpu_baseline(steps: int, sample_batch: int) -> dict:
 def run_reference_arm(args, rank: int) -> None:
     if rank != 0:
         return
-    cb = cpu_baseline(max(1, args.steps), sample_batch=4)
+    sample = 4 if args.workload == "bert" else 2
+    cb = cpu_baseline(max(1, args.steps), sample_batch=sample, workload=args.workload)
     line = {"impl": "reference", "metric": "samples/sec per train iter of HAP program", "value": cb["value"],
             "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "BERT-base GEMM skeleton (configs[2]), 12 layers, seq 128",
-                       "global_batch": 4, "seq_len": SEQ, "parallelism": "cpu"},
+            "config": {"workload": WORKLOADS[args.workload]["desc"],
+                       "global_batch": sample, "seq_len": SEQ, "parallelism": "cpu"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -157,6 +179,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch ops eagerly instead of one CUDA graph")
@@ -195,14 +218,15 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=dev)
     caps = workloads.sm_caps(n)
     cluster = ClusterSpec.from_dict(workloads.cluster_doc(caps))
-    batch = PER_GPU_BATCH * n
-    g = workloads.bert(layers=LAYERS, batch=batch, seq=SEQ)
-    doc = _plan_doc(n)
+    wl = WORKLOADS[args.workload]
+    batch = wl["per_gpu_batch"] * n
+    g = _graph(args.workload, batch)
+    doc = _plan_doc(args.workload, n)
     if doc is None:
         prog, table, ratios, plan_name = api.single_device_program(g), {}, (1.0,), "single-device program (m=1)"
     else:
         prog, table = DistributedProgram.from_json(doc["program"]), table_from_plan(doc)
-        ratios, plan_name = tuple(doc["ratios"][0]), f"bert12_b{batch}.b200x{n}"
+        ratios, plan_name = tuple(doc["ratios"][0]), f"{wl['stem']}_b{batch}.b200x{n}"
     group = NcclGroup.from_torch_distributed() if world > 1 else LocalGroup(1)
     shapes = {nd.id: nd.shape for nd in g.sources()}
     ex = Executor(prog, n, table, shapes, group=group,
@@ -297,7 +321,7 @@ def main() -> None:
                      * (2 if m["accumulate"] else 1) for m in members)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
-    if n == 1 and os.path.exists(prof):
+    if n == 1 and args.workload == "bert" and os.path.exists(prof):
         with open(prof) as fh:
             tr = json.load(fh)
         traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]
@@ -317,7 +341,8 @@ def main() -> None:
 
     cb = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(args.cpu_steps, sample_batch=4)
+        cb = cpu_baseline(args.cpu_steps, sample_batch=4 if args.workload == "bert" else 2,
+                          workload=args.workload)
 
     if rank == 0:
         samples = batch
@@ -329,8 +354,7 @@ def main() -> None:
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "BERT-base GEMM skeleton (configs[2]): 12 layers, seq 128, hidden 768, "
-                                   "FFN 3072, train step fwd+bwd+sync+SGD",
+            "config": {"workload": wl["desc"],
                        "global_batch": batch, "seq_len": SEQ, "parallelism": f"hap-spmd{n}",
                        "plan": plan_name, "sm_caps": caps, "ratios": list(ratios),
                        "grad_sync": dict(sorted(ex.sync_choice.items())) or "n/a (m=1)",

@@ -155,6 +155,32 @@ class Op:
 
 # ---------------------------------------------------------------------------- executor
 
+def price_grad_sync(spec, ratios, weight: str, kdim: int, ndim: int, uses) -> str:
+    """HAP's SFB rule for one replicated [kdim, ndim] weight whose uses are
+    row-sharded matmuls ``(x_ref, y_ref, rows)``: all-reduce the partial dW
+    (plus the ratio-sharded dW GEMMs) against all-gathering x and dy and
+    rebuilding dW at full batch on every device — each priced with the
+    reference cost model's collective times (cost_model.comm_time) and the
+    slowest device's GEMM time.  Returns "sfb" or "all_reduce"."""
+    from .cost_model import ClusterSpec, comm_time
+
+    if not isinstance(spec, ClusterSpec):
+        spec = ClusterSpec.from_dict(spec)
+    row = tuple(ratios) if ratios else tuple(d.flops_per_second / spec.total_rate for d in spec.devices)
+    rates = [d.flops_per_second for d in spec.devices]
+    t_ar = comm_time(Instruction("all_reduce", weight, elements=kdim * ndim), row, spec)
+    t_sfb = 0.0
+    for x_ref, y_ref, rows in uses:
+        flops = 2 * rows * kdim * ndim
+        t_sfb += comm_time(Instruction("all_gather", x_ref, elements=rows * kdim), row, spec)
+        t_sfb += comm_time(Instruction("all_gather", y_ref, elements=rows * ndim), row, spec)
+        # SFB replicates the weight-gradient GEMM at full batch on every device;
+        # all-reduce keeps it sharded.
+        t_sfb += max(flops / rt for rt in rates)
+        t_ar += max(flops * b / rt for b, rt in zip(row, rates))
+    return "sfb" if t_sfb < t_ar else "all_reduce"
+
+
 class Executor:
     """Compiled executor of one distributed program on this process's devices."""
 
@@ -1091,30 +1117,13 @@ class Executor:
                 self.sfb[ins.output] = us
 
     def _price_sync(self, pins: Instruction, uses: list) -> str:
-        from .cost_model import ClusterSpec, comm_time
-
         spec = self.cfg.cluster
         if spec is None:
             return "all_reduce"
-        if not isinstance(spec, ClusterSpec):
-            spec = ClusterSpec.from_dict(spec)
-        row = self.cfg.ratios or tuple(d.flops_per_second / spec.total_rate for d in spec.devices)
-        rates = [d.flops_per_second for d in spec.devices]
         kdim, ndim = self.source_shapes[pins.ref]
-        ar = Instruction("all_reduce", pins.ref, elements=kdim * ndim)
-        t_ar = comm_time(ar, row, spec)
-        t_sfb = 0.0
-        for u in uses:
-            rows = sum(s[0] for s in self.shapes[u.operands[0]])
-            flops = 2 * rows * kdim * ndim
-            gx = Instruction("all_gather", u.operands[0].split("@")[0], elements=rows * kdim)
-            gy = Instruction("all_gather", u.ref, elements=rows * ndim)
-            t_sfb += comm_time(gx, row, spec) + comm_time(gy, row, spec)
-            # SFB replicates the weight-gradient GEMM at full batch on every device;
-            # all-reduce keeps it sharded.
-            t_sfb += max(flops / rt for rt in rates)
-            t_ar += max(flops * b / rt for b, rt in zip(row, rates))
-        return "sfb" if t_sfb < t_ar else "all_reduce"
+        use_rows = [(u.operands[0].split("@")[0], u.ref, sum(s[0] for s in self.shapes[u.operands[0]]))
+                    for u in uses]
+        return price_grad_sync(spec, self.cfg.ratios, pins.ref, kdim, ndim, use_rows)
 
     def _sfb_weight_grad(self, ins: Instruction, contrib):
         """dW = gather(x)^T . gather(dy), replicated (Id form) on every device."""

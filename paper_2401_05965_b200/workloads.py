@@ -71,6 +71,80 @@ def bert_doc(layers: int = 12, batch: int = 64, seq: int = 128, hidden: int = 76
     return {"nodes": nodes, "loss": "loss"}
 
 
+def moe_doc(experts: int = 8, tokens: int = 256, hidden: int = 768, ffn: int = 3072) -> dict:
+    """configs[3]/[4]: a mixture-of-experts FFN block (BERT-base widths).
+
+    The router's dispatch is the data loader's: expert e receives its own
+    token batch x_e [tokens, hidden] (a placeholder), runs a SiLU FFN
+    (W1_e, W2_e) and the per-expert outputs are summed into the loss.  With
+    few tokens per expert the weights dominate the activations, which is
+    where sufficient-factor broadcasting beats all-reducing the weight
+    gradients — the choice the executor prices with the cost model."""
+    nodes = []
+    losses = []
+    for e in range(experts):
+        p = f"e{e}_"
+        nodes.append(_n(p + "x", "Placeholder", [tokens, hidden]))
+        nodes.append(_n(p + "W1", "Parameter", [hidden, ffn]))
+        nodes.append(_n(p + "f1", "MatMul", [tokens, ffn], [p + "x", p + "W1"]))
+        nodes.append(_n(p + "s1", "ElemwiseUnary", [tokens, ffn], [p + "f1"], tag="sigmoid"))
+        nodes.append(_n(p + "g", "ElemwiseBinary", [tokens, ffn], [p + "f1", p + "s1"], tag="mul"))
+        nodes.append(_n(p + "W2", "Parameter", [ffn, hidden]))
+        nodes.append(_n(p + "y", "MatMul", [tokens, hidden], [p + "g", p + "W2"]))
+        nodes.append(_n(p + "l", "Reduce", [], [p + "y"], dims="all"))
+        losses.append(p + "l")
+    acc = losses[0]
+    for i, l in enumerate(losses[1:], 1):
+        out = "loss" if i == len(losses) - 1 else f"lsum{i}"
+        nodes.append(_n(out, "ElemwiseBinary", [], [acc, l], tag="add"))
+        acc = out
+    if len(losses) == 1:
+        nodes.append(_n("loss", "Identity", [], [acc]))
+    return {"nodes": nodes, "loss": "loss"}
+
+
+def moe_stack_doc(layers: int = 12, experts: int = 2, batch: int = 8, seq: int = 128, hidden: int = 768,
+                  ffn: int = 3072) -> dict:
+    """configs[4] (BERT-MoE FFN stack): per layer, `experts` SiLU FFN experts
+    (BERT-base widths) read the layer input and their outputs join the
+    residual stream, x_{l+1} = x_l + sum_e FFN_e(x_l).  Every expert sees
+    every token (a dense mixture: the reference IR has no routing op), and
+    with few tokens per GPU the weight gradients dwarf the activation factors
+    — the sufficient-factor-broadcasting regime.  Experts per layer stay at 2
+    because the planner's search grows combinatorially with independent
+    branches (4 experts exhaust its 200k-expansion budget)."""
+    tokens = batch * seq
+    nodes = [_n("x0", "Placeholder", [tokens, hidden])]
+    prev = "x0"
+    for layer in range(layers):
+        outs = []
+        for e in range(experts):
+            p = f"l{layer}_e{e}_"
+            nodes.append(_n(p + "W1", "Parameter", [hidden, ffn]))
+            nodes.append(_n(p + "f1", "MatMul", [tokens, ffn], [prev, p + "W1"]))
+            nodes.append(_n(p + "s1", "ElemwiseUnary", [tokens, ffn], [p + "f1"], tag="sigmoid"))
+            nodes.append(_n(p + "g", "ElemwiseBinary", [tokens, ffn], [p + "f1", p + "s1"], tag="mul"))
+            nodes.append(_n(p + "W2", "Parameter", [ffn, hidden]))
+            nodes.append(_n(p + "y", "MatMul", [tokens, hidden], [p + "g", p + "W2"]))
+            outs.append(p + "y")
+        acc = prev
+        for i, y in enumerate(outs):
+            out = f"l{layer}_x{i + 1}"
+            nodes.append(_n(out, "ElemwiseBinary", [tokens, hidden], [acc, y], tag="add"))
+            acc = out
+        prev = acc
+    nodes.append(_n("loss", "Reduce", [], [prev], dims="all"))
+    return {"nodes": nodes, "loss": "loss"}
+
+
+def moe_stack(layers: int = 12, experts: int = 2, batch: int = 8, seq: int = 128) -> Graph:
+    return graph_from_dict(moe_stack_doc(layers, experts, batch, seq))
+
+
+def moe(experts: int = 8, tokens: int = 256, hidden: int = 768, ffn: int = 3072) -> Graph:
+    return graph_from_dict(moe_doc(experts, tokens, hidden, ffn))
+
+
 def mlp(batch: int = 64, hidden: int = 1024, layers: int = 2) -> Graph:
     return graph_from_dict(mlp_doc(batch, hidden, layers))
 
@@ -128,7 +202,12 @@ def synthetic_inputs(g: Graph, seed: int, scaled: bool = True) -> dict:
     rng = np.random.default_rng(seed)
     # residual-branch output projections get the GPT-2 1/sqrt(2L) factor so a
     # deep skeleton without normalisation keeps O(1) activations.
-    depth = sum(1 for n in g.nodes if n.id.endswith("_Wo"))
+    # (BERT skeleton: one _Wo per layer; MoE stack: every expert's _W2 feeds
+    # the residual stream.)
+    branches = [n.id for n in g.nodes if n.id.endswith("_Wo")]
+    if not branches:
+        branches = [n.id for n in g.nodes if n.id.startswith("l") and n.id.endswith("_W2")]
+    depth = len(branches)
     out = {}
     for node in g.nodes:
         if node.op in ("Placeholder", "Parameter"):

@@ -125,6 +125,9 @@ def enumerated_cases(per_case: int = 10) -> None:
 
     names = ["matmul_reduce", "two_reduce_rows", "two_reduce_cols", "binary_add",
              "matmul_unary", "identity_after_reduce", "self_add", "rank1_mul"]
+    if args.moe:
+        moe_plans(bench=args.bench)
+        return
     clusters = {"homog2": ref_corpus.HOMOG2, "hetero2": ref_corpus.HETERO2,
                 "skew2": ref_corpus.SKEW2, "homog3": ref_corpus.HOMOG3}
     for gname in names:
@@ -249,11 +252,31 @@ def fd_gradients(gname: str, gdoc: dict, eps: float = 1e-5) -> None:
     np.savez_compressed(path, **out)
 
 
+def moe_plans(bench: bool) -> None:
+    """configs[4]: BERT-MoE stack (2 SiLU experts per layer, residual merge),
+    2 sequences of 128 tokens per GPU — the regime where the cost model picks
+    sufficient-factor broadcasting at 2 and 4 GPUs and all-reduce at 8."""
+    for n in (2, 4):
+        cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+        gdoc = workloads.moe_stack_doc(layers=2, batch=2, seq=64)
+        _dump(os.path.join(HERE, "graphs", "moe2_b2.json"), gdoc)
+        plan_case("moe2_b2", gdoc, f"b200x{n}", cdoc, scaled=True, seeds=(0,))
+    if bench:
+        for n in (2, 4, 8):
+            cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+            gdoc = workloads.moe_stack_doc(layers=12, batch=2 * n, seq=128)
+            plan_case(f"moe12_b{2 * n}", gdoc, f"b200x{n}", cdoc, values=False)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--bench", action="store_true", help="also plan the 12-layer bench graphs")
+    ap.add_argument("--moe", action="store_true", help="only the MoE-stack plans (configs[4])")
     args = ap.parse_args()
 
+    if args.moe:
+        moe_plans(bench=args.bench)
+        return
     clusters = {"homog2": ref_corpus.HOMOG2, "homog3": ref_corpus.HOMOG3,
                 "hetero2": ref_corpus.HETERO2, "skew2": ref_corpus.SKEW2}
     for cname, cdoc in clusters.items():

@@ -22,6 +22,8 @@ def load_json(*parts):
 def graph_doc(name: str) -> dict:
     if name.startswith("bert12_b"):
         return workloads.bert_doc(layers=12, batch=int(name[len("bert12_b"):]), seq=128)
+    if name.startswith("moe12_b"):
+        return workloads.moe_stack_doc(layers=12, batch=int(name[len("moe12_b"):]), seq=128)
     return load_json("graphs", f"{name}.json")
 
 

@@ -52,11 +52,16 @@ def main():
         g = goldens.graph(gname)
         shapes = {n.id: n.shape for n in g.sources()}
         program, m, table = O.load_plan(doc)
+        # Gradient sync: all-reduce for every gather implementation, plus
+        # sufficient-factor broadcasting through the P2P and send/recv gathers.
+        variants = [(g_, "all_reduce") for g_ in ("kernel", "padded", "sendrecv")]
+        variants += [("kernel", "sfb"), ("sendrecv", "sfb")]
         for dtype in ("fp32", "bf16"):
-            for gather in ("kernel", "padded", "sendrecv"):
+            for gather, sync in variants:
                 count += 1
                 ex = Executor(DistributedProgram.from_json(doc["program"]), m, table_from_plan(doc), shapes,
-                              group=group, config=ExecConfig(dtype=dtype, input_grads=True, gather=gather))
+                              group=group, config=ExecConfig(dtype=dtype, input_grads=True, gather=gather,
+                                                             grad_sync=sync))
                 ex.load(inputs)
                 ex.step()
                 torch.cuda.synchronize()
@@ -69,7 +74,7 @@ def main():
                     if ins.ref == program.loss and ins.kind == "reduce":
                         scale = max(scale, float(np.sqrt(sum(np.sum(np.square(v)) for v in env[ins.operands[0]]))))
                 if any(abs(a - float(b)) > RTOL[dtype] * scale for a, b in zip(losses, want)):
-                    failures.append(f"{name} {dtype} {gather}: losses {losses} vs {[float(v) for v in want]}")
+                    failures.append(f"{name} {dtype} {gather} {sync}: losses {losses} vs {[float(v) for v in want]}")
                 for ref, value in sg.items():
                     for r, forms in ex.gradient(ref).items():
                         for did, grad in forms:
@@ -85,7 +90,7 @@ def main():
                                 continue
                             err = float(np.max(np.abs(grad - value_r))) / max(float(np.max(np.abs(value))), 1e-3)
                             if err > RTOL[dtype]:
-                                failures.append(f"{name} {dtype} {gather}: grad {did}@{r} rel err {err:.3g}")
+                                failures.append(f"{name} {dtype} {gather} {sync}: grad {did}@{r} rel err {err:.3g}")
                 ex.group = None  # the communicator is shared across executors
     fl = [None] * world
     dist.all_gather_object(fl, failures)

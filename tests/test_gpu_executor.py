@@ -22,12 +22,12 @@ if not torch.cuda.is_available():  # pragma: no cover
 RTOL = {"bf16": 2e-2, "fp32": 1e-3}
 
 
-def _run(doc, g, inputs, dtype, lr=0.0):
+def _run(doc, g, inputs, dtype, lr=0.0, grad_sync="auto"):
     prog = DistributedProgram.from_json(doc["program"])
     m = int(doc["devices"])
     shapes = {n.id: n.shape for n in g.nodes if n.op in ("Placeholder", "Parameter")}
     ex = Executor(prog, m, table_from_plan(doc), shapes, group=LocalGroup(m),
-                  config=ExecConfig(dtype=dtype, lr=lr, input_grads=True))
+                  config=ExecConfig(dtype=dtype, lr=lr, input_grads=True, grad_sync=grad_sync))
     ex.load(inputs)
     ex.step()
     torch.cuda.synchronize()
@@ -111,6 +111,22 @@ def test_programs_with_collectives_match_reference(stem, dtype):
     ex = _run(doc, g, inputs, dtype)
     want = vals["seed0:losses"]
     _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
+    _check_grads(ex, g, inputs, dtype, doc)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", ["moe2_b2.b200x2", "moe2_b2.b200x4", "mlp.ratio12"])
+def test_sufficient_factor_broadcasting_matches_reference(case, dtype):
+    """Every replicated weight rebuilt from gathered factors (x, dy) gives the
+    reference gradient, as the all-reduce path does."""
+    gname, cname = case.split(".")
+    g = goldens.graph(gname)
+    vals = goldens.values(gname, cname)
+    doc = goldens.plan(gname, cname)
+    inputs = goldens.inputs(g, vals, goldens.seeds(vals)[0])
+    ex = _run(doc, g, inputs, dtype, grad_sync="sfb")
+    assert ex.sync_choice and set(ex.sync_choice.values()) == {"sfb"}, ex.sync_choice
+    assert ex.sfb_done == set(ex.sfb)
     _check_grads(ex, g, inputs, dtype, doc)
 
 

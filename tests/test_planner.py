@@ -27,8 +27,8 @@ def _plan_cases():
     cases = []
     for name in sorted(os.listdir(os.path.join(goldens.GOLDEN, "plans"))):
         gname, cname = name[:-5].rsplit(".", 1)
-        if gname.startswith("bert12") and not SLOW:
-            continue  # 75-170 s each; HAP_SLOW_TESTS=1 includes them
+        if gname.startswith(("bert12", "moe12")) and not SLOW:
+            continue  # 60-170 s each; HAP_SLOW_TESTS=1 includes them
         cases.append((gname, cname))
     return cases
 

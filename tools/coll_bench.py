@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--rows", default="4096,16384,65536,262144", help="comma-separated gathered row counts")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -49,7 +50,7 @@ def main():
     handles = [None] * world
     dist.all_gather_object(handles, bytes(h.raw))
     check(L.hap_symm_open(ctx, b"".join(handles)))
-    for rows in (4096, 16384, 65536, 262144):
+    for rows in [int(v) for v in args.rows.split(",")]:
         sizes = round_shards(rows, ratios)
         counts = [s * inner for s in sizes]
         send = torch.randn(counts[rank], device=dev).to(torch.bfloat16)
