@@ -231,8 +231,11 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 }
 
 // Epilogue modes: direct per-thread stores (any layout), TMA bulk store, TMA
-// bulk reduce-add (fp32 accumulate / split-K partials).
-enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2 };
+// bulk reduce-add (fp32 accumulate and fp32 split-K partials), and split-K
+// into bf16: each K split stores its fp32 partial tile into its own slice of
+// a workspace; split_reduce_kernel then sums the slices in split order and
+// rounds once into C (deterministic, and no bf16 double rounding).
+enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_WS = 3 };
 
 // Byte offset of 16-byte chunk c of row r in a TMA-swizzled staging box.
 template <int kRowBytes>
@@ -251,7 +254,7 @@ template <int BN, typename OutT>
 __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter, int half, int lane, int row0,
                                                   int col0, int M, int N, OutT* C, int64_t ldc, int mode,
                                                   int vec_ok, int accumulate, int splits,
-                                                  const CUtensorMap* tmC, uint8_t* buf) {
+                                                  const CUtensorMap* tmC, uint8_t* buf, uint32_t& box_seq) {
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16);
   const int first = col0 + half * (BN / 2);
   if (mode == EPI_DIRECT) {
@@ -284,7 +287,10 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
   const uint32_t buf0 = smem_u32(buf);
 #pragma unroll 1
   for (int b = 0; b < kBoxes; ++b) {
-    const uint32_t dst = buf0 + (b & 1) * 4096;
+    // the two staging buffers alternate across boxes AND units (a unit with
+    // an odd box count must not restart on the buffer its last box is still
+    // being stored from)
+    const uint32_t dst = buf0 + (box_seq++ & 1) * 4096;
     if (lane == 0) bulk_wait_read1();   // the buffer's previous box has been read out
     __syncwarp();
 #pragma unroll
@@ -325,6 +331,10 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
   }
 }
 
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ batched problems
 // One persistent launch serves up to kMaxProblems GEMMs of the same operand
 // orientation: either independent problems whose tiles share the launch
@@ -335,9 +345,12 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
 constexpr int kMaxProblems = 4;
 
 struct alignas(64) TcProblem {
-  CUtensorMap a, b, c;
+  CUtensorMap a, b, c;     // c: output map, or the fp32 workspace map (EPI_SPLIT_WS)
   void* C;
   int64_t ldc;
+  float* ws;               // EPI_SPLIT_WS: fp32 partials [splits][ws_rows][ws_ld]
+  int64_t ws_ld;
+  int ws_rows;             // rows per split slice (M rounded up to whole tiles)
   int M, N, K;
   int m_tiles, n_tiles, k_blocks;
   int splits, kb_per_split;
@@ -349,11 +362,27 @@ struct alignas(64) TcBatch {
   TcProblem p[kMaxProblems];
   int count;
   int sum_k;
+  int sum_kb;              // sum_k: K blocks of all problems (the concatenated K range)
   int total_units;
 };
 
+// Epilogue of one unit for one warp: drain the accumulator into C, or (split
+// K) into split `split`'s slice of the workspace.
+template <int BN, typename OutT>
+__device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
+                                              int lane, int row0, int col0, int split, uint8_t* buf,
+                                              uint32_t& box_seq) {
+  if (pr.epi_mode == EPI_SPLIT_WS) {
+    drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0, pr.M, pr.N, pr.ws,
+                                 pr.ws_ld, EPI_TMA_STORE, 1, 0, 1, &pr.c, buf, box_seq);
+    return;
+  }
+  drain_accumulator<BN, OutT>(tmem_acc, quarter, half, lane, row0, col0, pr.M, pr.N, static_cast<OutT*>(pr.C),
+                              pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, pr.splits, &pr.c, buf, box_seq);
+}
+
 struct Unit {
-  int prob, m0, n0, kb0, kb1;
+  int prob, split, m0, n0, kb0, kb1;
 };
 
 // Work unit u -> (problem, output tile, K-block range).  Grouped: units are
@@ -369,19 +398,26 @@ __device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
   const int t = local % tiles;
   Unit x;
   x.prob = p;
+  x.split = local / tiles;
   x.m0 = (t % pr.m_tiles) * ROWS;
   x.n0 = (t / pr.m_tiles) * BN;
   x.kb0 = (local / tiles) * pr.kb_per_split;
-  x.kb1 = min(pr.k_blocks, x.kb0 + pr.kb_per_split);
+  x.kb1 = min(bt.sum_k ? bt.sum_kb : pr.k_blocks, x.kb0 + pr.kb_per_split);
   return x;
 }
 
-// f(problem, k_block) for every K block a unit accumulates, in order.
+// f(problem, k_block) for every K block a unit accumulates, in order (a sum
+// walks its slice [kb0, kb1) of the problems' concatenated K blocks).
 template <typename F>
 __device__ __forceinline__ void for_each_kblock(const TcBatch& bt, const Unit& x, F&& f) {
   if (bt.sum_k) {
-    for (int q = 0; q < bt.count; ++q)
-      for (int kb = 0; kb < bt.p[q].k_blocks; ++kb) f(q, kb);
+    int base = 0;
+    for (int q = 0; q < bt.count; ++q) {
+      const int nk = bt.p[q].k_blocks;
+      const int lo = max(x.kb0 - base, 0), hi = min(x.kb1 - base, nk);
+      for (int kb = lo; kb < hi; ++kb) f(q, kb);
+      base += nk;
+    }
   } else {
     for (int kb = x.kb0; kb < x.kb1; ++kb) f(x.prob, kb);
   }
@@ -515,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const int quarter = warp & 3;              // TMEM lanes 32*quarter .. +31
     const int half = (warp - 4) >> 2;          // which half of the tile's columns
     uint8_t* buf = staging + (warp - 4) * 8192;
+    uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -522,9 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const TcProblem& pr = bt.p[x.prob];
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, pr.M,
-                                  pr.N, static_cast<OutT*>(pr.C), pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate,
-                                  pr.splits, &pr.c, buf);
+      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
+                              buf, box_seq);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
@@ -753,6 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int half = (warp - 4) >> 2;
     uint8_t* buf = staging + (warp - 4) * 8192;
+    uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
     const uint32_t leader_tempty = map_to_cta(tempty0, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -762,9 +799,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      drain_accumulator<BN, OutT>(tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, pr.M, pr.N,
-                                  static_cast<OutT*>(pr.C), pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate,
-                                  pr.splits, &pr.c, buf);
+      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
+                              buf, box_seq);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
@@ -878,50 +914,128 @@ hap_status launch_dispatch(bool pair, int bn, bool amn, bool bmn, const TcBatch&
 }
 
 // Tile shape of a batch: single-CTA 128 x BN or SM-pair 256 x BN
-// (cta_group::2), BN in {128, 256}, plus a split-K factor (fp32 output, one
-// problem).  Each candidate is scored by the fraction of the capped SMs kept
-// busy across the persistent rounds, times a per-shape efficiency (operand
-// bytes per MMA: the pair tile halves B traffic per SM; 128-wide tiles are
-// smem-bandwidth bound).
+// (cta_group::2), BN in {128, 192, 256}, plus a split-K factor when the tiles
+// alone cannot fill the SMs and the split's extra pass pays for itself.  Each
+// candidate is scored by the fraction of the capped SMs kept busy across the
+// persistent rounds, times a per-shape efficiency (operand bytes per MMA: the
+// pair tile halves B traffic per SM; 128-wide tiles are smem-bandwidth bound).
 struct Shape {
   int bn, splits, kb_per_split;
   bool pair;
 };
 
-Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool fp32_out,
-                   int cap, int allow_pair) {
+Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
+                   bool fp32_out, int cap, int allow_pair) {
   int64_t k_blocks = 0;
   for (int q = 0; q < (sum_k ? count : 1); ++q) k_blocks += (Ks[q] + BK - 1) / BK;
-  Shape best{256, 1, static_cast<int>(k_blocks), false};
-  double best_score = -1.0;
   struct Cand { bool pair; int bn; double weight; };
   const Cand cands[] = {{true, 256, 1.0}, {true, 192, 0.85}, {true, 128, 0.8}, {false, 256, 0.75},
                         {false, 128, 0.65}};
   int64_t min_m = Ms[0];
   for (int q = 0; q < count; ++q) min_m = std::min(min_m, Ms[q]);
+  // Best candidate without and with split-K, each by the fraction of the
+  // capped SMs kept busy across the persistent rounds times the shape's
+  // efficiency; est_us is a rough critical path (per-SM K-block time of a
+  // BN-wide tile at full MMA rate / efficiency, times the K blocks each SM walks).
+  struct Pick { Shape s; double score; double est_us; };
+  Pick plain{{256, 1, static_cast<int>(k_blocks), false}, -1.0, 1e30};
+  Pick split = plain;
   for (const Cand& c : cands) {
     if (c.pair && (!allow_pair || min_m < 256 || cap < 2)) continue;
     const int64_t rows = c.pair ? 256 : 128;
     const int64_t slots = c.pair ? cap / 2 : cap;
     int64_t tiles = 0;
     for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
-    int64_t splits = 1;
-    if (fp32_out && !sum_k && tiles < slots && k_blocks >= 8) {
-      splits = std::min<int64_t>(slots / tiles, k_blocks / 4);
-      if (splits < 1) splits = 1;
-    }
-    const int64_t kps = (k_blocks + splits - 1) / splits;
-    splits = (k_blocks + kps - 1) / kps;
-    const int64_t work = tiles * splits;
-    const int64_t rounds = (work + slots - 1) / slots;
-    double score = static_cast<double>(work) / static_cast<double>(rounds * slots) * c.weight;
-    if (splits > 1) score *= 0.97;  // partial-sum traffic
-    if (score > best_score + 1e-9) {
-      best_score = score;
-      best = {c.bn, static_cast<int>(splits), static_cast<int>(kps), c.pair};
+    const double t_kb = 0.26 * c.bn / 256.0 / c.weight;
+    for (int want_split = 0; want_split < 2; ++want_split) {
+      int64_t splits = 1;
+      if (want_split) {
+        if (!allow_split || tiles >= slots || k_blocks < 8) continue;
+        splits = std::max<int64_t>(1, std::min<int64_t>(slots / tiles, k_blocks / 4));
+      }
+      const int64_t kps = (k_blocks + splits - 1) / splits;
+      splits = (k_blocks + kps - 1) / kps;
+      if (want_split && splits < 2) continue;
+      const int64_t work = tiles * splits;
+      const int64_t rounds = (work + slots - 1) / slots;
+      const double score = static_cast<double>(work) / static_cast<double>(rounds * slots) * c.weight;
+      Pick& best = want_split ? split : plain;
+      const double s_adj = want_split ? score * 0.97 : score;   // partial-sum traffic
+      if (s_adj > best.score + 1e-9)
+        best = {{c.bn, static_cast<int>(splits), static_cast<int>(kps), c.pair}, s_adj,
+                static_cast<double>(rounds * kps) * t_kb};
     }
   }
-  return best;
+  // fp32 outputs: split partials reduce-add in L2, nearly free — the higher
+  // score wins.  bf16 outputs: the partial slices and their reduction pass
+  // add a serial tail (~5 us measured on B200), so split only when the
+  // shortened K walk saves more than that.
+  if (fp32_out) return split.score > plain.score ? split.s : plain.s;
+  constexpr double kSplitTailUs = 5.0;
+  if (split.score > 0 && split.est_us + kSplitTailUs < plain.est_us) return split.s;
+  return plain.score > 0 ? plain.s : split.s;
+}
+
+// C (+)= sum over s of ws[s] — the K splits' partial tiles added in split
+// order (fixed, so repeated launches give identical bits).  A thread owns 4
+// consecutive columns of a row; every split's load is issued before the sum.
+template <typename OutT>
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ ws, int splits,
+                                                           int64_t slice, int64_t ld, OutT* __restrict__ C,
+                                                           int64_t ldc, int M, int N, int accumulate, int vec) {
+  hap::pdl_enter();
+  const int64_t nq = (static_cast<int64_t>(N) + 3) / 4;
+  const int64_t total = static_cast<int64_t>(M) * nq;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / nq;
+    const int col = static_cast<int>(i - row * nq) * 4;
+    const float* src = ws + row * ld + col;
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+    constexpr int U = 8;
+    for (int s0 = 1; s0 < splits; s0 += U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + u < splits) v[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + u) * slice));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + u < splits) {
+          acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+        }
+    }
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    OutT* dst = C + row * ldc + col;
+    if (vec && col + 4 <= N) {
+      if constexpr (std::is_same<OutT, float>::value) {
+        float4 o = make_float4(a[0], a[1], a[2], a[3]);
+        if (accumulate) {
+          const float4 c = *reinterpret_cast<const float4*>(dst);
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        *reinterpret_cast<float4*>(dst) = o;
+      } else {
+        float f[4] = {a[0], a[1], a[2], a[3]};
+        if (accumulate) {
+          const uint2 c = *reinterpret_cast<const uint2*>(dst);
+          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
+          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
+          f[0] += lo.x; f[1] += lo.y; f[2] += hi.x; f[3] += hi.y;
+        }
+        __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&lo);
+        o.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(dst) = o;
+      }
+    } else {
+      for (int e = 0; e < 4 && col + e < N; ++e) {
+        float v = a[e];
+        if (accumulate) v += to_f32(dst[e]);
+        dst[e] = from_f32<OutT>(v);
+      }
+    }
+  }
 }
 
 }  // namespace tc
@@ -1007,6 +1121,15 @@ int tma_epilogue() {
   return mode;
 }
 
+// HAP_GEMM_SPLIT=0 disables split-K.
+int split_enabled() {
+  static int mode = [] {
+    const char* v = getenv("HAP_GEMM_SPLIT");
+    return v ? atoi(v) : 1;
+  }();
+  return mode;
+}
+
 int pair_mode() {
   static int mode = [] {
     const char* v = getenv("HAP_GEMM_PAIR");
@@ -1055,6 +1178,41 @@ extern "C" int hap_matmul_engine(const void* A, int64_t lda, int transA, const v
 
 namespace {
 
+// Split-K workspace, one per stream (launches on one stream are ordered, so
+// they can share it).  Grown only outside stream capture; a capturing launch
+// that would need more runs without splitting.
+struct SplitWorkspace {
+  float* ws = nullptr;
+  int64_t elems = 0;
+};
+
+bool split_workspace(cudaStream_t stream, int64_t elems, float** out) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, SplitWorkspace> table;
+  std::lock_guard<std::mutex> lock(mu);
+  SplitWorkspace& w = table[stream];
+  if (w.elems >= elems) {
+    *out = w.ws;
+    return true;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return false;   // the old buffer may be in use
+  cudaFree(w.ws);
+  w = SplitWorkspace{};
+  const int64_t n = std::max<int64_t>(elems, 1 << 22);
+  if (cudaMalloc(reinterpret_cast<void**>(&w.ws), n * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    w = SplitWorkspace{};
+    return false;
+  }
+  w.elems = n;
+  *out = w.ws;
+  return true;
+}
+
+inline int64_t ws_pitch(int64_t n) { return (n + 3) / 4 * 4; }   // 16-byte rows for the TMA map
+
 // Build and launch one tcgen05 batch (all problems tc-eligible, same
 // orientation, <= kMaxProblems).  sum_k: every problem adds into problem 0's
 // output (same C, M, N), accumulate taken from problem 0.
@@ -1068,7 +1226,30 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     Ks[q] = d[q].K;
   }
   const bool fp32 = out_dtype == HAP_F32;
-  const tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, fp32, cap, pair_mode());
+  const int nout = sum_k ? 1 : count;
+  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0, fp32, cap, pair_mode());
+  // split-K partial slices: splits x (M rounded up to whole tiles) x pitch(N)
+  // fp32 per output; without room for them (capture), no split
+  float* ws = nullptr;
+  auto slice_rows = [&](int q, const tc::Shape& sh) {
+    const int64_t r = sh.pair ? 256 : tc::BM;
+    return (Ms[q] + r - 1) / r * r;
+  };
+  auto problem_splits = [&](int q, const tc::Shape& sh) -> int64_t {
+    if (sum_k) return sh.splits;
+    const int64_t kb = (Ks[q] + tc::BK - 1) / tc::BK;
+    const int64_t kps = std::max<int64_t>(1, std::min<int64_t>(sh.kb_per_split, kb));
+    return (kb + kps - 1) / kps;
+  };
+  if (shp.splits > 1 && !fp32) {
+    int64_t need = 0;
+    for (int q = 0; q < nout; ++q) {
+      const int64_t sp = problem_splits(q, shp);
+      if (sp > 1) need += sp * slice_rows(q, shp) * ws_pitch(Ns[q]);
+    }
+    if (!split_workspace(stream, need, &ws))
+      shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, false, fp32, cap, pair_mode());
+  }
   const int rows = shp.pair ? 256 : tc::BM;
   const int b_box = shp.pair ? shp.bn / 2 : shp.bn;
   const bool amn = d[0].transA != 0, bmn = d[0].transB == 0;
@@ -1077,14 +1258,15 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   std::memset(&bt, 0, sizeof(bt));
   bt.count = count;
   bt.sum_k = sum_k;
+  for (int q = 0; q < count; ++q) bt.sum_kb += static_cast<int>((d[q].K + tc::BK - 1) / tc::BK);
   int units = 0;
+  int64_t ws_used = 0;
   for (int q = 0; q < count; ++q) {
     tc::TcProblem& pr = bt.p[q];
     const hap_gemm_desc& g = d[q];
     bool ok = g.transA ? tc::make_map(&pr.a, g.A, g.M, g.K, g.lda, tc::BK) : tc::make_map(&pr.a, g.A, g.K, g.M, g.lda, tc::BM);
     ok = ok && (g.transB ? tc::make_map(&pr.b, g.B, g.K, g.N, g.ldb, b_box) : tc::make_map(&pr.b, g.B, g.N, g.K, g.ldb, tc::BK));
     HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout");
-    const tc::TcProblem& owner = bt.p[0];
     const hap_gemm_desc& out = sum_k ? d[0] : g;
     pr.C = out.C;
     pr.ldc = out.ldc;
@@ -1094,34 +1276,62 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.m_tiles = static_cast<int>((out.M + rows - 1) / rows);
     pr.n_tiles = static_cast<int>((out.N + shp.bn - 1) / shp.bn);
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
-    // a sum walks every problem's K blocks; grouped problems may split K
-    // (same factor for all; problems with fewer K blocks get fewer splits)
-    if (!sum_k && shp.splits > 1) {
-      pr.kb_per_split = std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
-      pr.splits = (pr.k_blocks + pr.kb_per_split - 1) / pr.kb_per_split;
-    } else {
+    // grouped problems split K by the same factor (problems with fewer K
+    // blocks get fewer splits); a sum splits its concatenated K blocks
+    pr.splits = static_cast<int>(problem_splits(q, shp));
+    pr.kb_per_split = sum_k ? shp.kb_per_split : std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
+    if (pr.splits <= 1) {
       pr.splits = 1;
-      pr.kb_per_split = pr.k_blocks;
+      pr.kb_per_split = sum_k ? bt.sum_kb : pr.k_blocks;
     }
     pr.accumulate = out.accumulate;
     pr.vec_ok = ((reinterpret_cast<uintptr_t>(out.C) & 15) == 0) && ((out.ldc * osz) % 16 == 0);
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
-    // accumulation and split-K partials use TMA reduce-add; a bf16
-    // accumulate (read-modify-round) stays on per-thread stores.
+    // accumulation and fp32 split-K partials use TMA reduce-add (in L2); a
+    // bf16 accumulate (read-modify-round) stays on per-thread stores; bf16
+    // split K stores fp32 partial slices, summed in order by split_reduce.
     pr.epi_mode = tc::EPI_DIRECT;
-    if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
-        tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc, shp.bn))
+    if (!fp32 && pr.splits > 1 && (!sum_k || q == 0)) {
+      pr.ws = ws + ws_used;
+      pr.ws_ld = ws_pitch(out.N);
+      pr.ws_rows = static_cast<int>(slice_rows(q, shp));
+      ws_used += static_cast<int64_t>(pr.splits) * pr.ws_rows * pr.ws_ld;
+      HAP_CHECK_ARG(tc::make_map_c(&pr.c, pr.ws, HAP_F32, out.N, static_cast<int64_t>(pr.splits) * pr.ws_rows,
+                                   pr.ws_ld, shp.bn),
+                    "hap_matmul: workspace tensor map rejected");
+      pr.epi_mode = tc::EPI_SPLIT_WS;
+    } else if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
+               tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc, shp.bn)) {
       pr.epi_mode = (fp32 && (pr.accumulate || pr.splits > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
+    }
     pr.unit_begin = units;
     if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
-    (void)owner;
   }
   bt.total_units = units;
-  for (int q = 0; q < (sum_k ? 1 : count); ++q)  // split-K partials add into a zeroed output
-    if (bt.p[q].splits > 1 && !d[q].accumulate)
+  for (int q = 0; q < nout; ++q)  // fp32 split-K partials add into a zeroed output
+    if (fp32 && bt.p[q].splits > 1 && !d[q].accumulate)
       HAP_CUDA_TRY(cudaMemset2DAsync(d[q].C, d[q].ldc * osz, 0, d[q].N * osz, d[q].M, stream));
-  return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
-              : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+  hap_status st = fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
+                       : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+  if (st != HAP_OK) return st;
+  for (int q = 0; q < nout; ++q) {
+    const tc::TcProblem& pr = bt.p[q];
+    if (pr.epi_mode != tc::EPI_SPLIT_WS) continue;
+    const int64_t work = static_cast<int64_t>(pr.M) * ((pr.N + 3) / 4);
+    const int grid = capped_grid((work + 255) / 256, cap * 4);
+    const int64_t slice = static_cast<int64_t>(pr.ws_rows) * pr.ws_ld;
+    if (fp32)
+      launch_k(tc::split_reduce_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(pr.ws),
+               pr.splits, slice, pr.ws_ld, static_cast<float*>(pr.C), pr.ldc, pr.M, pr.N, pr.accumulate,
+               pr.vec_ok);
+    else
+      launch_k(tc::split_reduce_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
+               static_cast<const float*>(pr.ws), pr.splits, slice, pr.ws_ld, static_cast<__nv_bfloat16*>(pr.C),
+               pr.ldc, pr.M, pr.N, pr.accumulate, pr.vec_ok);
+    st = launch_status("split_reduce_kernel");
+    if (st != HAP_OK) return st;
+  }
+  return HAP_OK;
 }
 
 hap_status simt_one(const hap_gemm_desc& g, hap_dtype in_dtype, hap_dtype out_dtype, int sm_cap,

@@ -21,6 +21,7 @@
 //      device memory so CUDA-graph replays need no host bookkeeping.
 // Every CTA spins on flags another GPU writes, so the grid is one CTA per
 // (capped) SM, all resident; separate GPUs run the ranks, never one GPU.
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -297,14 +298,24 @@ extern "C" int64_t hap_symm_capacity(void* ctx) {
 
 namespace {
 
+// CTAs for a call moving `bytes`: each CTA keeps ~64 KB of NVLink reads in
+// flight (512 threads x 8 x 16 B), so small messages use few CTAs — cheaper
+// grid barriers, and SMs left to the compute stream when the call runs on a
+// side stream — and large ones one CTA per (capped) SM.
+inline int p2p_grid(int64_t bytes, int sm_cap) {
+  const int64_t want = std::max<int64_t>(4, (bytes + 65535) / 65536);
+  return capped_grid(want, sm_cap);
+}
+
 template <typename T>
 hap_status p2p_launch(void (*kern)(Peers, int, int, const T*, T*, int64_t, int64_t, int64_t, const int64_t*,
                                    const int64_t*),
                       Symm* s, const void* send, void* out, int64_t outer, int64_t inner, int64_t extent,
-                      const int64_t* dev_sizes, const int64_t* dev_offs, int sm_cap, cudaStream_t stream) {
+                      const int64_t* dev_sizes, const int64_t* dev_offs, int64_t bytes, int sm_cap,
+                      cudaStream_t stream) {
   Peers peers{};
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
-  const int grid = capped_grid(sm_count(), sm_cap);  // one resident CTA per (capped) SM
+  const int grid = p2p_grid(bytes, sm_cap);   // every CTA resident (they spin on peer flags)
   launch_k(kern, dim3(grid), dim3(kThreads), 0, stream, peers, s->rank, s->nranks, static_cast<const T*>(send),
            static_cast<T*>(out), outer, inner, extent, dev_sizes, dev_offs);
   return launch_status("p2p kernel");
@@ -321,11 +332,12 @@ extern "C" hap_status hap_p2p_all_gather_v(void* ctx, const void* send, void* re
   HAP_CHECK_ARG(max_chunk_elems * static_cast<int64_t>(dtype_size(dtype)) <= hap_symm_capacity(ctx),
                 "hap_p2p_all_gather_v: shard larger than the symmetric staging buffer");
   auto st = static_cast<cudaStream_t>(stream);
+  const int64_t bytes = max_chunk_elems * s->nranks * static_cast<int64_t>(dtype_size(dtype));
   if (dtype == HAP_BF16)
-    return p2p_launch<__nv_bfloat16>(p2p_all_gather_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent, dev_sizes,
-                      dev_offsets, sm_cap, st);
+    return p2p_launch<__nv_bfloat16>(p2p_all_gather_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent,
+                                     dev_sizes, dev_offsets, bytes, sm_cap, st);
   return p2p_launch<float>(p2p_all_gather_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes, dev_offsets,
-                    sm_cap, st);
+                           bytes, sm_cap, st);
 }
 
 extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype,
@@ -337,9 +349,10 @@ extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void
   HAP_CHECK_ARG(outer * extent * inner * static_cast<int64_t>(dtype_size(dtype)) <= hap_symm_capacity(ctx),
                 "hap_p2p_reduce_scatter_v: tensor larger than the symmetric staging buffer");
   auto st = static_cast<cudaStream_t>(stream);
+  const int64_t bytes = outer * extent * inner * static_cast<int64_t>(dtype_size(dtype));
   if (dtype == HAP_BF16)
-    return p2p_launch<__nv_bfloat16>(p2p_reduce_scatter_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent, dev_sizes,
-                      dev_offsets, sm_cap, st);
+    return p2p_launch<__nv_bfloat16>(p2p_reduce_scatter_kernel<__nv_bfloat16>, s, send, recv, outer, inner, extent,
+                                     dev_sizes, dev_offsets, bytes, sm_cap, st);
   return p2p_launch<float>(p2p_reduce_scatter_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes,
-                    dev_offsets, sm_cap, st);
+                           dev_offsets, bytes, sm_cap, st);
 }

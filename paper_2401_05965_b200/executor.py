@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -142,6 +143,8 @@ class ExecConfig:
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
     batch_gemms: bool = True          # merge runs of matmuls into batched launches
     fuse_elementwise: bool = True     # fuse swish / gate elementwise chains
+    overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
+                                      # during the forward), weight-gradient GEMMs at the end of backward
 
 
 @dataclass
@@ -223,7 +226,12 @@ class Executor:
         self._check_program()
         self._infer()
         self._allocate()
-        self._symm = None
+        self._symm: dict = {}            # stream tag -> peer-memory context
+        self._p2p_bytes: dict = {}       # stream tag -> largest staging need
+        self._emit_on = None             # stream the next ops are emitted on (None: self.stream)
+        self._sfb_full: dict = {}        # gathered SFB factors, keyed by source buffer
+        self._sfb_pending: list = []     # deferred SFB weight-gradient GEMMs
+        self._plan_sfb()
         self._compile_forward()
         self._compile_backward()
         if self.cfg.batch_gemms:
@@ -357,7 +365,19 @@ class Executor:
         self._ops.append(Op(fn, args, what or name, kernel))
 
     def _sptr(self):
-        return self.stream.cuda_stream
+        return (self._emit_on or self.stream).cuda_stream
+
+    def _comm(self):
+        """NCCL communicator of the stream being emitted on: collectives on
+        the side stream use their own communicator, so the two streams never
+        interleave operations on one communicator."""
+        g = self.group
+        return g.comm_grad if self._emit_on is not None and self._emit_on is self.comm_stream else g.comm
+
+    def _side(self):
+        if self.comm_stream is None:
+            self.comm_stream = torch.cuda.Stream(self.device)
+        return self.comm_stream
 
     def _copy(self, src: Buf, dst: Buf, cap: int, accumulate: int = 0, alpha: float = 1.0):
         n = src.numel if src.shape else 1
@@ -416,7 +436,7 @@ class Executor:
         r = g.rank
         s = src[r]
         target = dst[r] if (not accumulate and dst[r].dtype == s.dtype) else self._new(s.shape, s.dtype)
-        self._emit("hap_all_reduce", g.comm, s.ptr, target.ptr, s.numel if s.shape else 1, s.dtype,
+        self._emit("hap_all_reduce", self._comm(), s.ptr, target.ptr, s.numel if s.shape else 1, s.dtype,
                    self._sptr(), kernel=False)
         if target is not dst[r]:
             self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
@@ -453,12 +473,12 @@ class Executor:
         carr = _lib.i64_array(counts)
         self._keep(carr)
         if kind == "grouped_broadcast":
-            self._emit("hap_grouped_broadcast", g.comm, s.ptr, target.ptr, carr, s.dtype,
+            self._emit("hap_grouped_broadcast", self._comm(), s.ptr, target.ptr, carr, s.dtype,
                        self._sptr(), kernel=False)
         else:
             padded = self.cfg.gather == "padded"
             scratch = self._new((self.m * max(counts),), s.dtype) if padded else None
-            self._emit("hap_all_gather_v", g.comm, s.ptr, target.ptr, carr, s.dtype, int(padded),
+            self._emit("hap_all_gather_v", self._comm(), s.ptr, target.ptr, carr, s.dtype, int(padded),
                        scratch.ptr if scratch else None, self._sptr(), kernel=False)
         if not direct:
             # rank-ordered chunks [outer, size_k, inner] -> full [outer, E, inner]
@@ -511,7 +531,7 @@ class Executor:
         scratch = self._new((self.m * max(max(counts), 1),), s.dtype)
         carr = _lib.i64_array(counts)
         self._keep(carr)
-        self._emit("hap_reduce_scatter_v", g.comm, send.ptr, target.ptr, carr, s.dtype, scratch.ptr,
+        self._emit("hap_reduce_scatter_v", self._comm(), send.ptr, target.ptr, carr, s.dtype, scratch.ptr,
                    self._sptr(), kernel=False)
         if not direct:
             self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
@@ -551,7 +571,7 @@ class Executor:
         sarr, rarr = _lib.i64_array(send_counts), _lib.i64_array(recv_counts)
         self._keep(sarr)
         self._keep(rarr)
-        self._emit("hap_all_to_all_v", g.comm, send.ptr, sarr, recv.ptr, rarr, s.dtype, self._sptr(),
+        self._emit("hap_all_to_all_v", self._comm(), send.ptr, sarr, recv.ptr, rarr, s.dtype, self._sptr(),
                    kernel=False)
         roff = offsets(recv_counts)
         for k in range(self.m):
@@ -567,34 +587,39 @@ class Executor:
         r = self.group.rank
         dev = torch.tensor([list(sizes), offsets(sizes)[:-1]], dtype=torch.int64, device=self.device)
         self._keep(dev)
-        self._p2p_bytes = max(getattr(self, "_p2p_bytes", 0), arena_bytes)
+        # one context (staging arena + flag epochs) per stream: calls on one
+        # stream are ordered, calls on two streams must not share staging
+        tag = "side" if self._emit_on is not None else "main"
+        self._p2p_bytes[tag] = max(self._p2p_bytes.get(tag, 0), arena_bytes)
         fn_ptr = getattr(self.lib, fn)
         stream = self._sptr()
         cap = self.caps[r]
         sizes_ptr, offs_ptr = dev[0].data_ptr(), dev[1].data_ptr()
         if fn == "hap_p2p_all_gather_v":
             max_chunk = max(sizes) * outer * inner
-            args = lambda: (self._symm, send.ptr, recv.ptr, send.dtype, outer, inner, extent, sizes_ptr,  # noqa: E731
-                            offs_ptr, max_chunk, cap, stream)
+            args = lambda: (self._symm[tag], send.ptr, recv.ptr, send.dtype, outer, inner, extent,  # noqa: E731
+                            sizes_ptr, offs_ptr, max_chunk, cap, stream)
         else:
-            args = lambda: (self._symm, send.ptr, recv.ptr, send.dtype, outer, inner, extent, sizes_ptr,  # noqa: E731
-                            offs_ptr, cap, stream)
+            args = lambda: (self._symm[tag], send.ptr, recv.ptr, send.dtype, outer, inner, extent,  # noqa: E731
+                            sizes_ptr, offs_ptr, cap, stream)
         self._ops.append(Op(lambda: fn_ptr(*args()), (), fn, True))
 
     def _create_symm(self):
-        if not getattr(self, "_p2p_bytes", 0):
+        if not self._p2p_bytes:
             return
         import torch.distributed as dist
 
         g = self.group
-        ctx = ctypes.c_void_p()
-        check(self.lib.hap_symm_create(ctypes.byref(ctx), int(self._p2p_bytes), g.rank, g.m), "hap_symm_create")
-        handle = ctypes.create_string_buffer(64)
-        check(self.lib.hap_symm_handle(ctx, handle), "hap_symm_handle")
-        handles = [None] * g.m
-        dist.all_gather_object(handles, bytes(handle.raw))
-        check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
-        self._symm = ctx
+        for tag in sorted(self._p2p_bytes):   # same order on every rank
+            ctx = ctypes.c_void_p()
+            check(self.lib.hap_symm_create(ctypes.byref(ctx), int(self._p2p_bytes[tag]), g.rank, g.m),
+                  "hap_symm_create")
+            handle = ctypes.create_string_buffer(64)
+            check(self.lib.hap_symm_handle(ctx, handle), "hap_symm_handle")
+            handles = [None] * g.m
+            dist.all_gather_object(handles, bytes(handle.raw))
+            check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
+            self._symm[tag] = ctx
 
     def _batch_gemms(self, ops: list) -> list:
         """Merge runs of consecutive matmul launches into hap_matmul_batch
@@ -690,6 +715,13 @@ class Executor:
     def _compile_forward(self):
         self._ops = self.ops_fwd
         self._find_chains()
+        # activations that sufficient-factor broadcasting will gather: with a
+        # side stream, gather each as soon as it is produced
+        early = set()
+        if self._sfb_overlap() and os.environ.get("HAP_DBG_SFB_FWD", "1") == "1":
+            early = {u.operands[0] for uses in self.sfb.values() for u in uses}
+            for d in sorted(early & self.source_dids):
+                self._sfb_factor(d, {r: self.bufs[(d, r)] for r in self.group.local_ranks})
         skip: set = set()
         for idx, ins in enumerate(self.program.instrs):
             if idx in skip:
@@ -698,8 +730,13 @@ class Executor:
             if chain is not None:
                 self._forward_chain(chain)
                 skip.update(chain["members"][1:])
-                continue
-            self._forward_instr(ins)
+                outs = [self.program.instrs[i].output for i in chain["members"]]
+            else:
+                self._forward_instr(ins)
+                outs = [ins.output]
+            for d in outs:
+                if d in early and d not in self.source_dids:
+                    self._sfb_factor(d, {r: self.bufs[(d, r)] for r in self.group.local_ranks})
         self._loss_closure()
 
     def _find_chains(self):
@@ -874,7 +911,6 @@ class Executor:
             self._emit("hap_fill", gb.ptr, gb.dtype, seed_val, max(1, gb.numel), self._sptr())
         written.add(seed_did)
 
-        self._plan_sfb()
         self._grad_ready_at: dict = {}
         self.overlapped: set = set()
         self._count_contributions(seed_did)
@@ -901,6 +937,7 @@ class Executor:
             for d in ins.operands:
                 if d in self.source_dids:
                     self._grad_ready_at[d] = len(self._ops)
+        self._emit_sfb_pending()
         self._overlap_grad_sync()
         self._finish_update(written)
 
@@ -1125,23 +1162,68 @@ class Executor:
                     for u in uses]
         return price_grad_sync(spec, self.cfg.ratios, pins.ref, kdim, ndim, use_rows)
 
+    def _sfb_overlap(self) -> bool:
+        return bool(self.sfb) and isinstance(self.group, NcclGroup) and self.cfg.overlap_sfb \
+            and self.group.comm_grad is not None
+
+    def _sfb_factor(self, did: str, bufs: dict) -> dict:
+        """Row-gathered copy of an SFB factor (an activation or an output
+        gradient), made once per source buffer and shared by every weight
+        that uses it (both experts of a layer read the same input).  With a
+        side stream the gather is issued there, ordered after the factor's
+        producer by an event, and overlaps the compute stream."""
+        L = self.group.local_ranks
+        key = tuple(bufs[r].ptr for r in L)
+        if os.environ.get("HAP_DBG_SFB_DEDUPE", "1") != "1":
+            key = (did, len(self._ops), id(self._ops))
+        if key in self._sfb_full:
+            return self._sfb_full[key]
+        rows = sum(s[0] for s in self.shapes[did])
+        full = {r: self._new((rows,) + tuple(self.shapes[did][0][1:]), bufs[r].dtype) for r in L}
+        if self._sfb_overlap():
+            side = self._side()
+            ready = torch.cuda.Event()
+            self._keep(ready)
+            self._ops.append(Op(ready.record, (self.stream,), "event.record", False))
+            self._ops.append(Op(side.wait_event, (ready,), "stream.wait_event", False))
+            self._emit_on = side
+            try:
+                self._coll_all_gather(bufs, self.shapes[did], full, 0, 0, "all_gather")
+            finally:
+                self._emit_on = None
+        else:
+            self._coll_all_gather(bufs, self.shapes[did], full, 0, 0, "all_gather")
+        self._sfb_full[key] = full
+        return full
+
     def _sfb_weight_grad(self, ins: Instruction, contrib):
         """dW = gather(x)^T . gather(dy), replicated (Id form) on every device."""
         L = self.group.local_ranks
         w = ins.operands[1]
         xdid, ydid = ins.operands[0], ins.output
-        xfull = {r: self._new((sum(s[0] for s in self.shapes[xdid]),) + self.shapes[xdid][0][1:],
-                              self.bufs[(xdid, r)].dtype) for r in L}
-        yfull = {r: self._new((sum(s[0] for s in self.shapes[ydid]),) + self.shapes[ydid][0][1:],
-                              self.grads[(ydid, r)].dtype) for r in L}
-        self._coll_all_gather({r: self.bufs[(xdid, r)] for r in L}, self.shapes[xdid], xfull, 0, 0,
-                              "all_gather")
-        self._coll_all_gather({r: self.grads[(ydid, r)] for r in L}, self.shapes[ydid], yfull, 0, 0,
-                              "all_gather")
+        xfull = self._sfb_factor(xdid, {r: self.bufs[(xdid, r)] for r in L})
+        yfull = self._sfb_factor(ydid, {r: self.grads[(ydid, r)] for r in L})
         acc = contrib(w)
         self.sfb_done.add(w)
+        if self._sfb_overlap():
+            self._sfb_pending.append((xfull, yfull, w, acc))
+            return
         for r in L:
             self._gemm(xfull[r], True, yfull[r], False, self._grad(w, r), self.caps[r], acc)
+
+    def _emit_sfb_pending(self):
+        """The deferred SFB weight-gradient GEMMs, after one wait for the side
+        stream's gathers; consecutive, so launch batching can group them."""
+        if not self._sfb_pending:
+            return
+        done = torch.cuda.Event()
+        self._keep(done)
+        self._ops.append(Op(done.record, (self._side(),), "event.record", False))
+        self._ops.append(Op(self.stream.wait_event, (done,), "stream.wait_event", False))
+        for xfull, yfull, w, acc in self._sfb_pending:
+            for r in self.group.local_ranks:
+                self._gemm(xfull[r], True, yfull[r], False, self._grad(w, r), self.caps[r], acc)
+        self._sfb_pending = []
 
     def _overlap_grad_sync(self):
         """NCCL groups: all-reduce each replicated parameter's gradient on a
@@ -1165,7 +1247,7 @@ class Executor:
             plan.append((self._grad_ready_at[f.output], f.output))
         if not plan:
             return
-        self.comm_stream = torch.cuda.Stream(self.device)
+        self._side()
         r = g.rank
         ops = self.ops_bwd
         for pos, did in sorted(plan, reverse=True):
@@ -1376,7 +1458,8 @@ class Executor:
     def close(self):
         if getattr(self, "_symm", None):
             torch.cuda.synchronize(self.device)
-            check(self.lib.hap_symm_destroy(self._symm), "hap_symm_destroy")
-            self._symm = None
+            for ctx in self._symm.values():
+                check(self.lib.hap_symm_destroy(ctx), "hap_symm_destroy")
+            self._symm = {}
         if self.group is not None:
             self.group.close()

@@ -56,12 +56,15 @@ def main():
         # sufficient-factor broadcasting through the P2P and send/recv gathers.
         variants = [(g_, "all_reduce") for g_ in ("kernel", "padded", "sendrecv")]
         variants += [("kernel", "sfb"), ("sendrecv", "sfb")]
+        if os.environ.get("HAP_PARITY_VARIANTS"):
+            variants = [tuple(v.split(":")) for v in os.environ["HAP_PARITY_VARIANTS"].split(",")]
+        overlap = os.environ.get("HAP_PARITY_OVERLAP", "1") == "1"
         for dtype in ("fp32", "bf16"):
             for gather, sync in variants:
                 count += 1
                 ex = Executor(DistributedProgram.from_json(doc["program"]), m, table_from_plan(doc), shapes,
                               group=group, config=ExecConfig(dtype=dtype, input_grads=True, gather=gather,
-                                                             grad_sync=sync))
+                                                             grad_sync=sync, overlap_sfb=overlap))
                 ex.load(inputs)
                 ex.step()
                 torch.cuda.synchronize()

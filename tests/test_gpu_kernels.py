@@ -221,3 +221,68 @@ def test_matmul_batch_grouped_and_summed(ta, tb, out):
     torch.cuda.synchronize()
     want = base + sum(ref_mm(x, ta, y, tb) for x, y in zip(As, Bs))
     assert rel_err(c, want) < (1e-5 if out == torch.float32 else 1.2e-2)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 768, 3072), (256, 3072, 768), (200, 520, 4096), (128, 96, 2048),
+                                   (512, 1000, 1536)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+@pytest.mark.parametrize("acc", [0, 1])
+def test_split_k_into_bf16_output(M, N, K, ta, tb, acc):
+    """Few output tiles, long K: the K range is split across SMs, partial sums
+    meet in the fp32 workspace and the last split rounds them into the bf16
+    output.  Repeated launches check that the workspace and its counters are
+    left clean; a capped grid checks the persistent schedule."""
+    torch.manual_seed(M + N + K + ta + tb + acc)
+    a = torch.randn((K, M) if ta else (M, K), device=DEV).to(torch.bfloat16)
+    b = torch.randn((N, K) if tb else (K, N), device=DEV).to(torch.bfloat16)
+    want = ref_mm(a, ta, b, tb)
+    for cap in (0, 0, 23):
+        c = torch.randn(M, N, device=DEV).to(torch.bfloat16)
+        base = c.float().clone()
+        gemm(a, ta, b, tb, c, accumulate=acc, sm_cap=cap)
+        assert rel_err(c, want + base if acc else want) < 8e-3, cap
+
+
+def test_split_k_bf16_sum_and_graph_replay():
+    """A K-concatenated sum (dx = dq.Wq^T + dk.Wk^T + dv.Wv^T at few tokens)
+    splits its combined K range; the same launches replay from a CUDA graph."""
+    torch.manual_seed(5)
+    M, N, K = 256, 768, 768
+    As = [torch.randn(M, K, device=DEV).to(torch.bfloat16) for _ in range(3)]
+    Bs = [torch.randn(N, K, device=DEV).to(torch.bfloat16) for _ in range(3)]
+    c = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    descs = (_lib.GemmDesc * 3)(*[_desc(x, 0, y, 1, c) for x, y in zip(As, Bs)])
+    want = sum(ref_mm(x, 0, y, 1) for x, y in zip(As, Bs))
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        check(L.hap_matmul_batch(descs, 3, 1, BF16, BF16, 0, stream.cuda_stream))
+    stream.synchronize()
+    assert rel_err(c, want) < 8e-3
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        check(L.hap_matmul_batch(descs, 3, 1, BF16, BF16, 0, stream.cuda_stream))
+    for _ in range(3):
+        c.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert rel_err(c, want) < 8e-3
+
+
+@pytest.mark.parametrize("cap", [0, 8])
+@pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("K", [256, 200, 4096])
+def test_matmul_batch_grouped_mixed_shapes(out, K, cap):
+    """Grouped problems of different M x N in one launch (the weight
+    gradients of a layer rebuilt from gathered factors: dW = X^T . dY).  A
+    small SM cap makes every CTA drain many tiles in a row (epilogue staging
+    buffers alternate across tiles with an odd box count, 192-wide tiles)."""
+    torch.manual_seed(K)
+    shapes = [(3072, 768), (768, 3072), (768, 768), (768, 768)]
+    As = [torch.randn(K, M, device=DEV).to(torch.bfloat16) for M, _ in shapes]
+    Bs = [torch.randn(K, N, device=DEV).to(torch.bfloat16) for _, N in shapes]
+    Cs = [torch.full((M, N), 7.0, device=DEV, dtype=out) for M, N in shapes]
+    descs = (_lib.GemmDesc * 4)(*[_desc(a, 1, b, 0, c) for a, b, c in zip(As, Bs, Cs)])
+    check(L.hap_matmul_batch(descs, 4, 0, BF16, _dt(Cs[0]), cap, S))
+    torch.cuda.synchronize()
+    for a, b, c in zip(As, Bs, Cs):
+        assert rel_err(c, ref_mm(a, 1, b, 0)) < (1e-5 if out == torch.float32 else 8e-3)

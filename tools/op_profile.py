@@ -2,6 +2,7 @@
 launches bracketed by CUDA events on the executor stream.  Aggregates by op
 (and GEMM shape) and compares the sum with the CUDA-graph step time."""
 import collections
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -10,7 +11,11 @@ import torch  # noqa: E402
 from paper_2401_05965_b200 import api, workloads  # noqa: E402
 from paper_2401_05965_b200.executor import ExecConfig, Executor, LocalGroup  # noqa: E402
 
-g = workloads.bert(layers=12, batch=64, seq=128)
+# HAP_PROFILE_WORKLOAD=moe profiles the BERT-MoE stack (2 sequences) instead.
+if os.environ.get("HAP_PROFILE_WORKLOAD") == "moe":
+    g = workloads.moe_stack(layers=12, batch=2, seq=128)
+else:
+    g = workloads.bert(layers=12, batch=64, seq=128)
 ex = Executor(api.single_device_program(g), 1, {}, {n.id: n.shape for n in g.sources()}, group=LocalGroup(1),
               config=ExecConfig(dtype="bf16", lr=1e-11))
 ex.load(workloads.synthetic_inputs(g, 0, scaled=True))

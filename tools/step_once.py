@@ -1,5 +1,6 @@
 """Build the bench executor (N=1) and run a few eager training steps — a
 small target for `ncu` (per-kernel counters of one step)."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -9,7 +10,10 @@ from paper_2401_05965_b200 import api, workloads  # noqa: E402
 from paper_2401_05965_b200.executor import ExecConfig, Executor, LocalGroup  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-g = workloads.bert(layers=12, batch=64, seq=128)
+if os.environ.get("HAP_PROFILE_WORKLOAD") == "moe":
+    g = workloads.moe_stack(layers=12, batch=2, seq=128)
+else:
+    g = workloads.bert(layers=12, batch=64, seq=128)
 ex = Executor(api.single_device_program(g), 1, {}, {n.id: n.shape for n in g.sources()}, group=LocalGroup(1),
               config=ExecConfig(dtype="bf16", lr=1e-11))
 ex.load(workloads.synthetic_inputs(g, 0, scaled=True))
