@@ -145,6 +145,7 @@ class ExecConfig:
     fuse_elementwise: bool = True     # fuse swish / gate elementwise chains
     overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
                                       # during the forward), weight-gradient GEMMs at the end of backward
+    bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
 
 
 @dataclass
@@ -914,6 +915,7 @@ class Executor:
         self._grad_ready_at: dict = {}
         self.overlapped: set = set()
         self._count_contributions(seed_did)
+        self._flat_grads()
         index = {id(ins): i for i, ins in enumerate(self.program.instrs)}
         handled: set = set()
         for ins in reversed(self.program.instrs):
@@ -1225,41 +1227,90 @@ class Executor:
                 self._gemm(xfull[r], True, yfull[r], False, self._grad(w, r), self.caps[r], acc)
         self._sfb_pending = []
 
-    def _overlap_grad_sync(self):
-        """NCCL groups: all-reduce each replicated parameter's gradient on a
-        side stream as soon as its last contribution is enqueued, so the
-        transfer overlaps the remaining backward kernels; the compute stream
-        joins the side stream before the update."""
-        g = self.group
-        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None:
-            return
+    def _synced_params(self) -> list:
+        """Parameter (and, with input_grads, placeholder) tensors realised in
+        one replicated form whose gradient is all-reduced (not SFB)."""
         forms: dict = {}
         for ins in self.program.instrs:
             if ins.kind.startswith("parameter") or (self.cfg.input_grads and ins.kind.startswith("placeholder")):
                 forms.setdefault(ins.ref, []).append(ins)
-        plan = []
-        for ref, fs in forms.items():
-            f = fs[0]
-            if len(fs) != 1 or f.kind not in ("parameter", "placeholder") or f.output in self.sfb_done:
-                continue
-            if f.output not in self._grad_ready_at:
-                continue
-            plan.append((self._grad_ready_at[f.output], f.output))
-        if not plan:
+        return [fs[0] for fs in forms.values()
+                if len(fs) == 1 and fs[0].kind in ("parameter", "placeholder") and fs[0].output not in self.sfb]
+
+    def _flat_grads(self):
+        """NCCL groups: lay the all-reduced gradients out back to back in one
+        fp32 buffer, in the order the backward pass completes them, so that
+        neighbouring gradients sync as one bucket (one large all-reduce runs
+        at NCCL's bandwidth; dozens of small ones pay its latency each)."""
+        g = self.group
+        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None:
             return
-        self._side()
+        first_use: dict = {}
+        for i, ins in enumerate(self.program.instrs):
+            for d in ins.operands:
+                first_use.setdefault(d, i)
+        params = [f for f in self._synced_params() if self._n_contrib.get(f.output, 0) > 0]
+        # a gradient is complete once the adjoint of its first consumer ran
+        params.sort(key=lambda f: -first_use.get(f.output, -1))
         r = g.rank
+        offs, total = [], 0
+        for f in params:
+            offs.append(total)
+            total += (int(math.prod(self.shapes[f.output][r])) + 63) // 64 * 64   # 256-byte aligned
+        if not total:
+            return
+        flat = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self._keep(flat)
+        self.bytes_allocated += total * 4
+        self._flat = (flat, {f.output: (o, int(math.prod(self.shapes[f.output][r]))) for f, o in zip(params, offs)})
+        for f, o in zip(params, offs):
+            shape = tuple(self.shapes[f.output][r])
+            self.grads[(f.output, r)] = Buf(flat.narrow(0, o, max(1, int(math.prod(shape)))), F32, shape)
+
+    def _overlap_grad_sync(self):
+        """NCCL groups: all-reduce the replicated parameters' gradients on a
+        side stream, bucket by bucket of the flat gradient buffer, as soon as
+        the last gradient of a bucket is enqueued, so the transfers overlap
+        the remaining backward kernels; the compute stream joins the side
+        stream before the update."""
+        g = self.group
+        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None or not hasattr(self, "_flat"):
+            return
+        flat, place = self._flat
+        ready = {f.output: self._grad_ready_at[f.output] for f in self._synced_params()
+                 if f.output in place and f.output in self._grad_ready_at}
+        if not ready:
+            return
+        # buckets: runs of the flat layout of about bucket_bytes
+        order = sorted(ready, key=lambda d: place[d][0])
+        buckets, cur = [], []
+        for d in order:
+            cur.append(d)
+            lo = place[cur[0]][0]
+            hi = place[d][0] + place[d][1]
+            if (hi - lo) * 4 >= self.cfg.bucket_bytes:
+                buckets.append(cur)
+                cur = []
+        if cur:
+            buckets.append(cur)
+        self._side()
         ops = self.ops_bwd
-        for pos, did in sorted(plan, reverse=True):
-            gb = self.grads[(did, r)]
+        plan = []
+        for members in buckets:
+            lo = place[members[0]][0]
+            hi = place[members[-1]][0] + place[members[-1]][1]
+            plan.append((max(ready[d] for d in members), lo, hi, members))
+        self.grad_buckets = [(hi - lo) * 4 for _, lo, hi, _ in plan]
+        for pos, lo, hi, members in sorted(plan, key=lambda t: -t[0]):
             ev = torch.cuda.Event()
             self._keep(ev)
+            ptr = flat.data_ptr() + lo * 4
             inserted = [Op(ev.record, (self.stream,), "event.record", False),
                         Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False),
-                        Op(self.lib.hap_all_reduce, (g.comm_grad, gb.ptr, gb.ptr, gb.numel, gb.dtype,
+                        Op(self.lib.hap_all_reduce, (g.comm_grad, ptr, ptr, hi - lo, F32,
                                                      self.comm_stream.cuda_stream), "hap_all_reduce", False)]
             ops[pos:pos] = inserted
-            self.overlapped.add(did)
+            self.overlapped.update(members)
         done = torch.cuda.Event()
         self._keep(done)
         ops.append(Op(done.record, (self.comm_stream,), "event.record", False))

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rows", default="4096,16384,65536,262144", help="comma-separated gathered row counts")
+    ap.add_argument("--ar-elems", default="", help="comma-separated fp32 all-reduce sizes (elements)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -78,19 +79,63 @@ def main():
             else:
                 assert torch.equal(out, ref), name
             dist.barrier()
+            # 10 calls per CUDA graph: device time per call, no host launch cost
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+                for _ in range(10):
+                    fn()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            with torch.cuda.stream(stream):
+                graph.replay()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, args.reps // 10)
             e0.record(stream)
-            for _ in range(args.reps):
-                fn()
+            with torch.cuda.stream(stream):
+                for _ in range(reps):
+                    graph.replay()
             e1.record(stream)
             torch.cuda.synchronize(dev)
-            t = torch.tensor([e0.elapsed_time(e1) / args.reps], device=dev)
+            del graph
+            t = torch.tensor([e0.elapsed_time(e1) / (reps * 10)], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             rb = torch.tensor([recv_bytes], device=dev, dtype=torch.float64)
             dist.all_reduce(rb, op=dist.ReduceOp.MAX)
             results.append({"op": "all_gather", "impl": name, "rows": rows, "shard_rows": sizes,
                             "ms": ms, "recv_GBps_max_rank": float(rb.item()) / (ms * 1e-3) / 1e9})
+    # NCCL all-reduce (fp32, in place) — the gradient synchronisation
+    for elems in [int(v) for v in args.ar_elems.split(",") if v]:
+        buf = torch.randn(elems, device=dev)
+        fn = lambda: L.hap_all_reduce(group.comm, buf.data_ptr(), buf.data_ptr(), elems, 0,  # noqa: E731
+                                      stream.cuda_stream)
+        for _ in range(3):
+            check(fn(), "all_reduce")
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+            for _ in range(10):
+                fn()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, args.reps // 10)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        del graph
+        t = torch.tensor([e0.elapsed_time(e1) / (reps * 10)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # bus bandwidth convention: 2 (n-1)/n x bytes / time
+        results.append({"op": "all_reduce", "impl": "nccl", "rows": elems, "shard_rows": [],
+                        "ms": ms, "recv_GBps_max_rank": 2 * (world - 1) / world * elems * 4 / (ms * 1e-3) / 1e9})
     if rank == 0:
         for r in results:
             print(f"{r['op']:10s} {r['impl']:14s} rows={r['rows']:7d} {r['ms'] * 1e3:9.1f} us "
