@@ -84,53 +84,104 @@ def _plan_doc(workload: str, n: int) -> dict | None:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    An NVML polling thread (every 5 ms, plus one sample on entry and one on
+    exit, so even a short timed region has samples); the nvidia-smi CSV loop
+    of the profiling recipe is the fallback when NVML is unavailable.  The
+    device is addressed by PCI bus id, so CUDA_VISIBLE_DEVICES remapping
+    cannot point the sampler at another GPU."""
 
-    def __init__(self, index: int):
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.proc = None
+        self.period = period_s
+        self.samples = []          # (sm_mhz, reasons)
+        self.sm_max = None
+        self._stop = None
+        self._thread = None
+        self._nvml = None
+        self._handle = None
+        self._smi = None
+
+    def _sample(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._handle, nv.NVML_CLOCK_SM)
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._handle)
+        self.samples.append((float(sm), {name for name, attr in self.REASONS if mask & getattr(nv, attr)}))
+
+    def _loop(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001 - a failed sample is just missing
+                pass
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self._nvml = nv
+            self._handle = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(self._handle, nv.NVML_CLOCK_SM))
+            self._sample()
+            self._stop = threading.Event()
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+        except Exception:  # noqa: BLE001 - fall back to the nvidia-smi loop
+            self._nvml = None
+            try:
+                self._smi = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.index}",
+                     "--query-gpu=index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self._smi = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+        if self._smi is not None:
+            self._smi.terminate()
+            try:
+                out, _ = self._smi.communicate(timeout=5)
             except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+                self._smi.kill()
+                out, _ = self._smi.communicate()
+            for ln in out.splitlines():
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm, smax = float(parts[1]), float(parts[2])
+                except ValueError:
+                    continue
+                self.sm_max = max(self.sm_max or 0.0, smax)
+                self.samples.append((sm, {name for (name, _), flag in zip(self.REASONS, parts[3:7])
+                                          if flag.lower() == "active"}))
 
     def summary(self) -> dict:
-        sm, smax, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = max(smax, float(parts[2]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, parts[5:9]):
-                if flag.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = set().union(*[r for _, r in self.samples]) if self.samples else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.sm_max,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def cpu_baseline(steps: int, sample_batch: int, workload: str = "bert") -> dict:
@@ -176,7 +227,7 @@ def run_reference_arm(args, rank: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bert", choices=sorted(WORKLOADS))

@@ -79,7 +79,31 @@ typedef struct {
   int64_t ldc;
   int64_t M, N, K;
   int accumulate;
+  /* Fused epilogue (bf16 output, tcgen05 path; zero = plain C (+)= A.B).
+   * The elementwise instructions that follow a matmul in the reference
+   * program (interpreter.py:141-148) or the adjoint contributions the
+   * executor would otherwise run as separate kernels, applied to the
+   * accumulator tile before it leaves the SM, with the rounding of the
+   * unfused sequence (every stored tensor rounded to bf16 where the unfused
+   * kernels store it):
+   *   HAP_EPI_ADD       C = A.B + R                       (R may equal C)
+   *   HAP_EPI_ADD2      C = A.B;  Y = C + R               (residual add)
+   *   HAP_EPI_SWISH     C = A.B;  Y = f(C);  Z = C * Y    (f = epi_tag)
+   *   HAP_EPI_SWISH_BWD dz = A.B (not stored);
+   *                     C (+)= dz*R2 + (dz*R)*f'(R, R2)   (R = x, R2 = f(x))
+   */
+  int epi;
+  int epi_tag;
+  const void* R;
+  int64_t ldr;
+  const void* R2;
+  int64_t ldr2;
+  void* Y;
+  int64_t ldy;
+  void* Z;
+  int64_t ldz;
 } hap_gemm_desc;
+enum { HAP_EPI_NONE = 0, HAP_EPI_ADD = 1, HAP_EPI_ADD2 = 2, HAP_EPI_SWISH = 3, HAP_EPI_SWISH_BWD = 4 };
 hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
                             hap_dtype out_dtype, int sm_cap, void* stream);
 /* Which engine hap_matmul would use for these arguments (no launch). */

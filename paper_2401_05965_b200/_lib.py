@@ -28,7 +28,12 @@ class GemmDesc(ctypes.Structure):
     """hap_gemm_desc (include/hap_b200.h)."""
     _fields_ = [("A", c_void_p), ("lda", c_int64), ("transA", c_int), ("B", c_void_p), ("ldb", c_int64),
                 ("transB", c_int), ("C", c_void_p), ("ldc", c_int64), ("M", c_int64), ("N", c_int64),
-                ("K", c_int64), ("accumulate", c_int)]
+                ("K", c_int64), ("accumulate", c_int), ("epi", c_int), ("epi_tag", c_int), ("R", c_void_p),
+                ("ldr", c_int64), ("R2", c_void_p), ("ldr2", c_int64), ("Y", c_void_p), ("ldy", c_int64),
+                ("Z", c_void_p), ("ldz", c_int64)]
+
+
+EPI_NONE, EPI_ADD, EPI_ADD2, EPI_SWISH, EPI_SWISH_BWD = range(5)
 
 
 # name -> (restype, argtypes); must cover every function include/hap_b200.h declares.

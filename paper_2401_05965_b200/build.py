@@ -52,7 +52,7 @@ def _compile(src: str, flags: list[str], force: bool) -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     inc, lib = nccl_paths()
-    flags = [f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}"]
+    flags = [f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}"] + os.environ.get("HAP_NVCC_FLAGS", "").split()
     if verbose:
         flags += ["-Xptxas", "-v"]
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))

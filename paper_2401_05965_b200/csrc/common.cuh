@@ -112,6 +112,32 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
   return __float2bfloat16_rn(v);
 }
 
+// Elementwise unary functions (interpreter.py:141-143), shared by the
+// elementwise kernels and the GEMM's fused epilogues so both round alike.
+__device__ __forceinline__ float unary_fwd(int tag, float x) {
+  switch (tag) {
+    case HAP_EXP: return __expf(x);
+    case HAP_NEG: return -x;
+    case HAP_RELU: return fmaxf(x, 0.f);
+    case HAP_SIGMOID: return __frcp_rn(1.f + __expf(-x));   // rcp.rn: one MUFU + refinement, no IEEE divide
+    default: return tanhf(x);
+  }
+}
+
+template <int TAG>
+__device__ __forceinline__ float unary_fwd_t(float x) { return unary_fwd(TAG, x); }
+
+// d/dx f at x, given y = f(x).
+__device__ __forceinline__ float unary_deriv(int tag, float x, float y) {
+  switch (tag) {
+    case HAP_EXP: return y;
+    case HAP_NEG: return -1.f;
+    case HAP_RELU: return x > 0.f ? 1.f : 0.f;
+    case HAP_SIGMOID: return y * (1.f - y);
+    default: return 1.f - y * y;
+  }
+}
+
 inline size_t dtype_size(hap_dtype t) { return t == HAP_BF16 ? 2 : 4; }
 
 }  // namespace hap

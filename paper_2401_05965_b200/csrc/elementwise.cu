@@ -17,27 +17,6 @@ namespace {
 constexpr int kBlock = 1024;
 constexpr int kUnroll = 2;   // independent 16-byte vectors in flight per thread
 
-__device__ __forceinline__ float unary_fwd(int tag, float x) {
-  switch (tag) {
-    case HAP_EXP: return __expf(x);
-    case HAP_NEG: return -x;
-    case HAP_RELU: return fmaxf(x, 0.f);
-    case HAP_SIGMOID: return 1.f / (1.f + __expf(-x));
-    default: return tanhf(x);
-  }
-}
-
-// d/dx f at x, given y = f(x).
-__device__ __forceinline__ float unary_deriv(int tag, float x, float y) {
-  switch (tag) {
-    case HAP_EXP: return y;
-    case HAP_NEG: return -1.f;
-    case HAP_RELU: return x > 0.f ? 1.f : 0.f;
-    case HAP_SIGMOID: return y * (1.f - y);
-    default: return 1.f - y * y;
-  }
-}
-
 // Vector of 8 elements loaded/stored as one 16-byte (bf16) or two 16-byte (fp32) accesses.
 template <typename T> struct Vec8;
 template <> struct Vec8<__nv_bfloat16> {

@@ -49,7 +49,7 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kBarrierBytes = 256;
+  static constexpr int kBarrierBytes = 512;
   static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + kBarrierBytes + 1024;
 };
 
@@ -236,6 +236,9 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 // a workspace; split_reduce_kernel then sums the slices in split order and
 // rounds once into C (deterministic, and no bf16 double rounding).
 enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_WS = 3 };
+// fused elementwise ops of the epilogue (hap_gemm_desc.epi)
+enum { EPI_OP_NONE = HAP_EPI_NONE, EPI_OP_ADD = HAP_EPI_ADD, EPI_OP_ADD2 = HAP_EPI_ADD2,
+       EPI_OP_SWISH = HAP_EPI_SWISH, EPI_OP_SWISH_BWD = HAP_EPI_SWISH_BWD };
 
 // Byte offset of 16-byte chunk c of row r in a TMA-swizzled staging box.
 template <int kRowBytes>
@@ -356,6 +359,12 @@ struct alignas(64) TcProblem {
   int splits, kb_per_split;
   int unit_begin;
   int epi_mode, accumulate, vec_ok;
+  // fused epilogue (hap_gemm_desc.epi): two extra bf16 tensor maps with C's
+  // box geometry, loaded into / stored from the staging boxes by TMA:
+  //   ADD: e1 = R (in)   ADD2: e1 = R (in), e2 = Y (out)
+  //   SWISH: e1 = Y, e2 = Z (out)   SWISH_BWD: e1 = R = x, e2 = R2 = f(x) (in)
+  int epi, epi_tag;
+  CUtensorMap e1, e2;
 };
 
 struct alignas(64) TcBatch {
@@ -366,12 +375,205 @@ struct alignas(64) TcBatch {
   int total_units;
 };
 
+__device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// 8 consecutive fp32 accumulator columns of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[e]);
+}
+
+__device__ __forceinline__ void lds_bf16x8(uint32_t at, float (&v)[8]) {
+  uint32_t q[4];
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]) : "r"(at));
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q[e]));
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+
+__device__ __forceinline__ void sts_bf16x8(uint32_t at, const float (&v)[8]) {
+  uint32_t p[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+    p[e] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]));
+}
+
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// Fused epilogues (hap_gemm_desc.epi, bf16 outputs).  The warp drains its
+// 32 rows x BN/2 columns in chunks of 32 columns (one tcgen05.ld each); every
+// tensor a chunk touches — outputs (C, Y, Z) and inputs (R, x, f(x)) — is a
+// 32 x 32 bf16 box (64-byte rows, SWIZZLE_64B) in the warp's 8 KB staging area
+// (4 slots of 2 KB).  Inputs are TMA-loaded into the slot their output will
+// occupy and overwritten in place; outputs leave by TMA store, one bulk group
+// per chunk.  Ops with <= 2 slots per chunk double-buffer: the next chunk's
+// inputs are loaded into the other slot pair while this chunk computes.
+// Rounding follows the unfused kernels: C is rounded to bf16 first and the
+// elementwise results are computed from the rounded value (elementwise.cu
+// swish_fwd / binary / swish_bwd).
+constexpr int kFusedW = 32;                  // columns per fused box
+constexpr int kFusedBox = 32 * kFusedW * 2;  // bytes per fused box
+
+// The elementwise op of one 32-column chunk: r = accumulator columns of the
+// lane's row; s0..s2 = the chunk's staging slots (inputs in place, outputs).
+template <int EPI, int TAG>
+__device__ __forceinline__ void fused_chunk(const uint32_t (&r)[32], int lane, uint32_t s0, uint32_t s1,
+                                            uint32_t s2) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {   // 8 columns: 16-byte chunk j of the lane's 64-byte row
+    const uint32_t off = swz_offset<64>(lane, j);
+    float c[8], x[8], o0[8], o1[8], o2[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c[e] = __uint_as_float(r[8 * j + e]);
+    if constexpr (EPI == EPI_OP_ADD) {
+      lds_bf16x8(s0 + off, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o0[e] = c[e] + x[e];
+    } else if constexpr (EPI == EPI_OP_ADD2) {
+      lds_bf16x8(s1 + off, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        o0[e] = c[e];
+        o1[e] = bf16_round(c[e]) + x[e];
+      }
+    } else if constexpr (EPI == EPI_OP_SWISH) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float cv = bf16_round(c[e]);
+        const float yv = bf16_round(unary_fwd_t<TAG>(cv));
+        o0[e] = cv;
+        o1[e] = yv;
+        o2[e] = cv * yv;
+      }
+    } else {   // EPI_OP_SWISH_BWD: C = dz*y + (dz*x)*f'(x, y), dz = rounded accumulator
+      float y[8];
+      lds_bf16x8(s0 + off, x);
+      lds_bf16x8(s1 + off, y);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float gz = bf16_round(c[e]);
+        const float dy = bf16_round(gz * x[e]);
+        o0[e] = gz * y[e] + bf16_round(dy * unary_deriv(TAG, x[e], y[e]));
+      }
+    }
+    sts_bf16x8(s0 + off, o0);
+    if constexpr (EPI == EPI_OP_ADD2 || EPI == EPI_OP_SWISH) sts_bf16x8(s1 + off, o1);
+    if constexpr (EPI == EPI_OP_SWISH) sts_bf16x8(s2 + off, o2);
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half, int lane,
+                                            int row0, int col0, uint8_t* buf, uint32_t ld_bar0, uint32_t& ld_phase) {
+  constexpr int kChunks = (BN / 2) / kFusedW;
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
+  const int first = col0 + half * (BN / 2);
+  const int epi = pr.epi;
+  const int n_in = epi == EPI_OP_SWISH_BWD ? 2 : ((epi == EPI_OP_ADD || epi == EPI_OP_ADD2) ? 1 : 0);
+  const bool dbl = epi != EPI_OP_SWISH;   // <= 2 slots per chunk: two slot pairs alternate
+  const uint32_t buf0 = smem_u32(buf);
+  // slot of input i / output o in slot set `set`
+  auto slot = [&](int set, int k) -> uint32_t { return buf0 + (dbl ? set * 2 + k : k) * kFusedBox; };
+  auto in_slot = [&](int set, int i) -> uint32_t { return slot(set, epi == EPI_OP_ADD2 ? 1 : i); };
+  auto issue_loads = [&](int chunk) {   // lane 0
+    const int set = dbl ? (chunk & 1) : 0;
+    const uint32_t bar = ld_bar0 + 8 * set;
+    mbar_expect_tx(bar, n_in * kFusedBox);
+    const int x0 = first + chunk * kFusedW;
+    tma_load_2d(in_slot(set, 0), &pr.e1, bar, x0, row0);
+    if (n_in == 2) tma_load_2d(in_slot(set, 1), &pr.e2, bar, x0, row0);
+  };
+  if (lane == 0) {
+    bulk_wait_read0();   // the previous unit's stores have read the staging slots
+    if (n_in) issue_loads(0);
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int ch = 0; ch < kChunks; ++ch) {
+    const int set = dbl ? (ch & 1) : 0;
+    if (lane == 0) {
+      if (dbl) {
+        // the other pair was last stored from by chunk ch-1: once read out,
+        // prefetch chunk ch+1's inputs into it
+        if (ch + 1 < kChunks) {
+          bulk_wait_read0();
+          if (n_in) issue_loads(ch + 1);
+        }
+      } else {
+        bulk_wait_read0();
+      }
+    }
+    uint32_t r[32];
+    tmem_ld32(lane_base + ch * kFusedW, r);
+    if (n_in) {
+      mbar_wait(ld_bar0 + 8 * set, (ld_phase >> set) & 1);
+      ld_phase ^= 1u << set;
+    }
+    __syncwarp();
+    const uint32_t s0 = slot(set, 0), s1 = slot(set, 1), s2 = slot(set, 2);
+    // one dispatch per chunk: the 32 columns run a loop specialised on (op, f)
+#define HAP_FUSED_CASE(EPI, TAG) fused_chunk<EPI, TAG>(r, lane, s0, s1, s2)
+    if (epi == EPI_OP_ADD) HAP_FUSED_CASE(EPI_OP_ADD, 0);
+    else if (epi == EPI_OP_ADD2) HAP_FUSED_CASE(EPI_OP_ADD2, 0);
+    else if (epi == EPI_OP_SWISH) {
+      switch (pr.epi_tag) {
+        case HAP_SIGMOID: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_SIGMOID); break;
+        case HAP_EXP: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_EXP); break;
+        case HAP_NEG: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_NEG); break;
+        case HAP_RELU: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_RELU); break;
+        default: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_TANH); break;
+      }
+    } else {
+      switch (pr.epi_tag) {
+        case HAP_SIGMOID: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_SIGMOID); break;
+        case HAP_EXP: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_EXP); break;
+        case HAP_NEG: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_NEG); break;
+        case HAP_RELU: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_RELU); break;
+        default: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_TANH); break;
+      }
+    }
+#undef HAP_FUSED_CASE
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const int x0 = first + ch * kFusedW;
+      tma_store_2d(&pr.c, slot(set, 0), x0, row0);
+      if (epi == EPI_OP_ADD2) tma_store_2d(&pr.e2, slot(set, 1), x0, row0);
+      if (epi == EPI_OP_SWISH) {
+        tma_store_2d(&pr.e1, slot(set, 1), x0, row0);
+        tma_store_2d(&pr.e2, slot(set, 2), x0, row0);
+      }
+      bulk_commit();
+    }
+  }
+  // a following unit may be unfused: its staging boxes overlap these slots
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+}
+
 // Epilogue of one unit for one warp: drain the accumulator into C, or (split
 // K) into split `split`'s slice of the workspace.
 template <int BN, typename OutT>
 __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
                                               int lane, int row0, int col0, int split, uint8_t* buf,
-                                              uint32_t& box_seq) {
+                                              uint32_t& box_seq, uint32_t ld_bar, uint32_t& ld_phase) {
+  if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
+    if (pr.epi != EPI_OP_NONE) {
+      drain_fused<BN>(pr, tmem_acc, quarter, half, lane, row0, col0, buf, ld_bar, ld_phase);
+      return;
+    }
+  }
   if (pr.epi_mode == EPI_SPLIT_WS) {
     drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0, pr.M, pr.N, pr.ws,
                                  pr.ws_ld, EPI_TMA_STORE, 1, 0, 1, &pr.c, buf, box_seq);
@@ -455,6 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, kEpiWarps * 32);
     }
+    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -552,6 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const int half = (warp - 4) >> 2;          // which half of the tile's columns
     uint8_t* buf = staging + (warp - 4) * 8192;
     uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
+    const uint32_t ld_bar = smem_u32(bars + 2 * G::kStages + 6 + 2 * (warp - 4));   // fused-epilogue input loads
+    uint32_t ld_phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -560,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq);
+                              buf, box_seq, ld_bar, ld_phase);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
@@ -597,7 +802,7 @@ struct Cfg2 {
   static constexpr int kBBytes = kHalfLoaded * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 256 + 1024;
+  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 512 + 1024;
 };
 
 
@@ -692,6 +897,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
     }
+    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -790,6 +996,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = (warp - 4) >> 2;
     uint8_t* buf = staging + (warp - 4) * 8192;
     uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
+    const uint32_t ld_bar = smem_u32(bars + 2 * G::kStages + 6 + 2 * (warp - 4));   // fused-epilogue input loads
+    uint32_t ld_phase = 0;
     const uint32_t leader_tempty = map_to_cta(tempty0, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -800,7 +1008,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq);
+                              buf, box_seq, ld_bar, ld_phase);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
@@ -850,12 +1058,13 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, i
 }
 
 // Output tensor map for the TMA epilogue: boxes of 128 bytes x 32 rows.
-bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld, int bn) {
+bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld, int bn,
+                int box_w = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int es = dt == HAP_BF16 ? 2 : 4;
   const int wide = 128 / es;                               // must match drain_accumulator's W
-  const int w = ((bn / 2) % wide == 0) ? wide : wide / 2;
+  const int w = box_w ? box_w : (((bn / 2) % wide == 0) ? wide : wide / 2);
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * es};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(w), 32};
@@ -926,8 +1135,13 @@ struct Shape {
 
 Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
                    bool fp32_out, int cap, int allow_pair) {
+  // K blocks a unit walks: the concatenated K of a sum, else the largest
+  // problem's (grouped problems with less K simply walk fewer blocks)
   int64_t k_blocks = 0;
-  for (int q = 0; q < (sum_k ? count : 1); ++q) k_blocks += (Ks[q] + BK - 1) / BK;
+  for (int q = 0; q < count; ++q) {
+    const int64_t kb = (Ks[q] + BK - 1) / BK;
+    k_blocks = sum_k ? k_blocks + kb : std::max(k_blocks, kb);
+  }
   struct Cand { bool pair; int bn; double weight; };
   const Cand cands[] = {{true, 256, 1.0}, {true, 192, 0.85}, {true, 128, 0.8}, {false, 256, 0.75},
                         {false, 128, 0.65}};
@@ -1227,7 +1441,12 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   }
   const bool fp32 = out_dtype == HAP_F32;
   const int nout = sum_k ? 1 : count;
-  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0, fp32, cap, pair_mode());
+  bool fused = false;
+  for (int q = 0; q < nout; ++q) fused = fused || d[q].epi != HAP_EPI_NONE;
+  HAP_CHECK_ARG(!fused || !fp32, "hap_matmul: fused epilogues need a bf16 output");
+  // a fused epilogue runs once per output tile: no split K
+  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && !fused, fp32, cap,
+                                   pair_mode());
   // split-K partial slices: splits x (M rounded up to whole tiles) x pitch(N)
   // fp32 per output; without room for them (capture), no split
   float* ws = nullptr;
@@ -1291,7 +1510,48 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     // bf16 accumulate (read-modify-round) stays on per-thread stores; bf16
     // split K stores fp32 partial slices, summed in order by split_reduce.
     pr.epi_mode = tc::EPI_DIRECT;
-    if (!fp32 && pr.splits > 1 && (!sum_k || q == 0)) {
+    pr.epi = (!sum_k || q == 0) ? out.epi : HAP_EPI_NONE;
+    pr.epi_tag = out.epi_tag;
+    // bf16 accumulate (read-modify-round) on the TMA path: C = A.B + C
+    int epi = pr.epi;
+    const void* R = out.R;
+    int64_t ldr = out.ldr;
+    if (epi == HAP_EPI_NONE && !fp32 && out.accumulate && pr.splits <= 1 && pr.vec_ok && tma_epilogue()) {
+      epi = HAP_EPI_ADD;
+      R = out.C;
+      ldr = out.ldc;
+    }
+    pr.epi = epi;
+    if (epi != HAP_EPI_NONE) {
+      HAP_CHECK_ARG(pr.splits <= 1 && pr.vec_ok && tma_epilogue(),
+                    "hap_matmul: fused epilogue needs a 16-byte pitched output and the TMA epilogue");
+      HAP_CHECK_ARG(epi >= HAP_EPI_ADD && epi <= HAP_EPI_SWISH_BWD, "hap_matmul: unknown epilogue op");
+      if (epi == HAP_EPI_ADD && out.accumulate) {
+        HAP_CHECK_ARG(R == nullptr || R == out.C,
+                      "hap_matmul: HAP_EPI_ADD with accumulate adds C itself (R must be C or null)");
+        R = out.C;
+        ldr = out.ldc;
+      }
+      HAP_CHECK_ARG(epi != HAP_EPI_SWISH_BWD || !out.accumulate,
+                    "hap_matmul: the fused swish adjoint writes C (no accumulate)");
+      auto map = [&](CUtensorMap* m, const void* ptr, int64_t ld, const char* what) -> bool {
+        if (ptr == nullptr ||
+            !tc::make_map_c(m, const_cast<void*>(ptr), HAP_BF16, out.N, out.M, ld, shp.bn, tc::kFusedW)) {
+          set_error(std::string("hap_matmul: fused epilogue tensor ") + what +
+                    " is null or not 16-byte aligned / pitched");
+          return false;
+        }
+        return true;
+      };
+      bool ok = map(&pr.c, out.C, out.ldc, "C");
+      if (epi == HAP_EPI_ADD) ok = ok && map(&pr.e1, R, ldr, "R");
+      if (epi == HAP_EPI_ADD2) ok = ok && map(&pr.e1, R, ldr, "R") && map(&pr.e2, out.Y, out.ldy, "Y");
+      if (epi == HAP_EPI_SWISH) ok = ok && map(&pr.e1, out.Y, out.ldy, "Y") && map(&pr.e2, out.Z, out.ldz, "Z");
+      if (epi == HAP_EPI_SWISH_BWD) ok = ok && map(&pr.e1, R, ldr, "R") && map(&pr.e2, out.R2, out.ldr2, "R2");
+      if (!ok) return HAP_ERR_ARG;
+      pr.accumulate = 0;
+      pr.epi_mode = tc::EPI_TMA_STORE;
+    } else if (!fp32 && pr.splits > 1 && (!sum_k || q == 0)) {
       pr.ws = ws + ws_used;
       pr.ws_ld = ws_pitch(out.N);
       pr.ws_rows = static_cast<int>(slice_rows(q, shp));
@@ -1406,6 +1666,10 @@ extern "C" hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, in
     hap_gemm_desc g = descs[q];
     if (sum_k && q > 0) g.accumulate = 1;
     hap_status st;
+    HAP_CHECK_ARG(g.epi == HAP_EPI_NONE || (g.M > 0 && g.N > 0 && g.K > 0 &&
+                                            tc_eligible(g.A, g.lda, g.transA, g.B, g.ldb, g.transB, g.M, g.N,
+                                                        g.K, in_dtype)),
+                  "hap_matmul: fused epilogues run on the tcgen05 path only (bf16, 16-byte pitched operands)");
     if (degenerate(g, out_dtype, stream, &st)) {
       if (st != HAP_OK) return st;
       continue;
@@ -1423,6 +1687,8 @@ extern "C" hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, in
 extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const void* B, int64_t ldb, int transB,
                                  void* C, int64_t ldc, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype,
                                  hap_dtype out_dtype, int accumulate, int sm_cap, void* stream) {
-  hap_gemm_desc g{A, lda, transA, B, ldb, transB, C, ldc, M, N, K, accumulate};
+  hap_gemm_desc g{};
+  g.A = A; g.lda = lda; g.transA = transA; g.B = B; g.ldb = ldb; g.transB = transB;
+  g.C = C; g.ldc = ldc; g.M = M; g.N = N; g.K = K; g.accumulate = accumulate;
   return hap_matmul_batch(&g, 1, 0, in_dtype, out_dtype, sm_cap, stream);
 }

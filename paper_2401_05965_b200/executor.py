@@ -143,6 +143,12 @@ class ExecConfig:
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
     batch_gemms: bool = True          # merge runs of matmuls into batched launches
     fuse_elementwise: bool = True     # fuse swish / gate elementwise chains
+    fuse_epilogue: bool = True        # fold elementwise work into the producing GEMM's epilogue (bf16
+                                      # outputs): residual adds, deferred gradient copies, the swish
+                                      # adjoint after the dz GEMM
+    fuse_swish_fwd: bool = False      # also y = f(x), z = x*y after the x GEMM (three outputs per tile:
+                                      # measured slower than GEMM + swish kernel with 8 KB of staging
+                                      # per epilogue warp, profiles/r01f_fused_epilogues.md)
     overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
                                       # during the forward), weight-gradient GEMMs at the end of backward
     bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
@@ -404,7 +410,12 @@ class Executor:
         self._copy(buf, out, cap)
         return out
 
-    def _gemm(self, a: Buf, trans_a: bool, b: Buf, trans_b: bool, c: Buf, cap: int, accumulate: int):
+    def _gemm(self, a: Buf, trans_a: bool, b: Buf, trans_b: bool, c: Buf, cap: int, accumulate: int,
+              addend: Buf | None = None):
+        """C (+)= op(A).op(B) as one hap_matmul_batch launch of a single
+        descriptor (later passes may merge descriptors into batches or fold
+        elementwise work into the descriptor's epilogue).  ``addend``: C =
+        A.B + addend (a deferred gradient copy, see _compile_backward)."""
         am, ak = (a.shape[1], a.shape[0]) if trans_a else a.shape
         bk, bn = (b.shape[1], b.shape[0]) if trans_b else b.shape
         if ak != bk or tuple(c.shape) != (am, bn):
@@ -413,12 +424,58 @@ class Executor:
         in_dt = BF16 if (a.dtype == BF16 and b.dtype == BF16) else F32
         a = self._as(a, in_dt, cap)
         b = self._as(b, in_dt, cap)
-        self._emit("hap_matmul", a.ptr, a.shape[1], int(trans_a), b.ptr, b.shape[1], int(trans_b),
-                   c.ptr, c.shape[1], am, bn, ak, in_dt, c.dtype, accumulate, cap, self._sptr())
-        self._ops[-1].gemm = dict(A=a.ptr, lda=a.shape[1], transA=int(trans_a), B=b.ptr, ldb=b.shape[1],
-                                  transB=int(trans_b), C=c.ptr, ldc=c.shape[1], M=am, N=bn, K=ak,
-                                  accumulate=accumulate, in_dt=in_dt, out_dt=c.dtype, cap=cap,
-                                  stream=self._sptr())
+        g = dict(A=a.ptr, lda=a.shape[1], transA=int(trans_a), B=b.ptr, ldb=b.shape[1],
+                 transB=int(trans_b), C=c.ptr, ldc=c.shape[1], M=am, N=bn, K=ak,
+                 accumulate=accumulate, in_dt=in_dt, out_dt=c.dtype, cap=cap,
+                 stream=self._sptr(), epi=_lib.EPI_NONE, epi_tag=0, R=None, ldr=0, R2=None, ldr2=0,
+                 Y=None, ldy=0, Z=None, ldz=0)
+        if addend is not None:
+            g.update(epi=_lib.EPI_ADD, R=addend.ptr, ldr=addend.shape[1], accumulate=0)
+        desc = (_lib.GemmDesc * 1)()
+        self._ops.append(Op(self.lib.hap_matmul_batch, (desc, 1, 0, in_dt, c.dtype, cap, self._sptr()),
+                            "hap_matmul", True, g))
+        self._sync_desc(self._ops[-1])
+
+    @staticmethod
+    def _fill_desc(d, g: dict):
+        for k in ("A", "lda", "transA", "B", "ldb", "transB", "C", "ldc", "M", "N", "K", "accumulate", "epi",
+                  "epi_tag", "R", "ldr", "R2", "ldr2", "Y", "ldy", "Z", "ldz"):
+            setattr(d, k, g[k])
+
+    def _sync_desc(self, op: Op):
+        """Write a single-GEMM op's record into its launch descriptor."""
+        self._fill_desc(op.args[0][0], op.gemm)
+
+    def _gemm_fusable(self, g: dict) -> bool:
+        """The GEMM can take a fused epilogue: tcgen05 path, bf16 output,
+        16-byte pitched buffers, one plain descriptor."""
+        if not self.cfg.fuse_epilogue or g is None or g.get("members") or g["out_dt"] != BF16:
+            return False
+        if g["epi"] != _lib.EPI_NONE or g["ldc"] % 8 or g["C"] % 16:
+            return False
+        return self.lib.hap_matmul_engine(g["A"], g["lda"], g["transA"], g["B"], g["ldb"], g["transB"], g["M"],
+                                          g["N"], g["K"], g["in_dt"]) == _lib.GEMM_TCGEN05
+
+    def _producer_gemm(self, ptr: int, window: int = 8):
+        """The recent single-GEMM op that wrote ``ptr`` (its C), if only GEMMs
+        that do not read ``ptr`` (and stream events) were emitted after it."""
+        for op in reversed(self._ops[-window:]):
+            g = op.gemm
+            if g is None:
+                if op.what in ("event.record", "stream.wait_event"):
+                    continue
+                return None
+            if g["C"] == ptr and not g.get("members"):
+                return op
+            if ptr in (g["A"], g["B"], g["R"], g["R2"], g["C"], g["Y"], g["Z"]):
+                return None
+        return None
+
+    @staticmethod
+    def _fusable_buf(*bufs) -> bool:
+        shape = tuple(bufs[0].shape)
+        return all(b.dtype == BF16 and len(b.shape) == 2 and tuple(b.shape) == shape and b.shape[1] % 8 == 0
+                   and b.ptr % 16 == 0 for b in bufs)
 
     # ------------------------------------------------------------------ collectives
     # Every collective maps per-device source buffers to per-device outputs with
@@ -645,10 +702,13 @@ class Executor:
 
     def _group_run(self, run: list) -> list:
         def reads(g):
-            r = {g["A"], g["B"]}
+            r = {g["A"], g["B"]} | ({g["R"], g["R2"]} - {None})
             if g["accumulate"]:
                 r.add(g["C"])
             return r
+
+        def writes(g):
+            return {g["C"], g["Y"], g["Z"]} - {None}
 
         def compatible(a, b):
             keys = ("transA", "transB", "in_dt", "out_dt", "cap", "stream")
@@ -671,19 +731,23 @@ class Executor:
                     continue
                 same_out = gj["C"] == g0["C"]
                 if same_out:
+                    # a K-concatenated sum: later terms plain accumulates; the
+                    # first term's epilogue (at most an addend) applies to the sum
                     if not (gj["accumulate"] and (gj["M"], gj["N"], gj["ldc"]) == (g0["M"], g0["N"], g0["ldc"])):
+                        continue
+                    if gj["epi"] != _lib.EPI_NONE or g0["epi"] not in (_lib.EPI_NONE, _lib.EPI_ADD):
                         continue
                     if len(members) > 1 and not sum_k:
                         continue
-                elif sum_k or any(run[m].gemm["C"] in reads(gj) for m in members) or \
-                        any(gj["C"] in reads(run[m].gemm) for m in members):
+                elif sum_k or any(writes(run[m].gemm) & (reads(gj) | writes(gj)) for m in members) or \
+                        any(writes(gj) & reads(run[m].gemm) for m in members):
                     continue
                 # the ops skipped over (not in the group, not yet placed) must not conflict
                 between = [k for k in range(i + 1, j) if not placed[k] and k not in members]
                 conflict = False
                 for k in between:
                     gk = run[k].gemm
-                    if gk["C"] in reads(gj) or gj["C"] in reads(gk) or gk["C"] == gj["C"]:
+                    if writes(gk) & reads(gj) or writes(gj) & reads(gk) or writes(gk) & writes(gj):
                         conflict = True
                         break
                 if conflict:
@@ -699,9 +763,7 @@ class Executor:
                 continue
             descs = (_lib.GemmDesc * len(members))()
             for slot, m in enumerate(members):
-                g = run[m].gemm
-                descs[slot] = _lib.GemmDesc(g["A"], g["lda"], g["transA"], g["B"], g["ldb"], g["transB"], g["C"],
-                                            g["ldc"], g["M"], g["N"], g["K"], g["accumulate"])
+                self._fill_desc(descs[slot], run[m].gemm)
             self._keep(descs)
             result.append(Op(self.lib.hap_matmul_batch, (descs, len(members), int(sum_k), g0["in_dt"],
                                                          g0["out_dt"], g0["cap"], g0["stream"]),
@@ -807,6 +869,13 @@ class Executor:
         for r in L:
             if c["kind"] == "swish":
                 x, y, z = B(c["x"], r), B(c["y"], r), B(c["z"], r)
+                op = self._producer_gemm(x.ptr) if self.cfg.fuse_swish_fwd else None
+                if op is not None and op.gemm["accumulate"] == 0 and self._gemm_fusable(op.gemm) \
+                        and self._fusable_buf(x, y, z):
+                    op.gemm.update(epi=_lib.EPI_SWISH, epi_tag=_lib.UNARY_TAGS[c["u"].tag], Y=y.ptr,
+                                   ldy=y.shape[1], Z=z.ptr, ldz=z.shape[1])
+                    self._sync_desc(op)
+                    continue
                 self._emit("hap_swish_fwd", _lib.UNARY_TAGS[c["u"].tag], x.ptr, y.ptr, z.ptr, x.dtype, x.numel,
                            self.caps[r], self._sptr())
             else:
@@ -832,6 +901,16 @@ class Executor:
         elif k == "elemwise_binary":
             for r in L:
                 a, b = src[0][r], src[1][r]
+                if ins.tag == "add" and ins.operands[0] != ins.operands[1] and self._fusable_buf(a, b, out[r]):
+                    # out = C + R folded into the epilogue of the GEMM that produced C
+                    op, other = self._producer_gemm(b.ptr), a
+                    if op is None:
+                        op, other = self._producer_gemm(a.ptr), b
+                    if op is not None and op.gemm["accumulate"] == 0 and self._gemm_fusable(op.gemm):
+                        op.gemm.update(epi=_lib.EPI_ADD2, R=other.ptr, ldr=other.shape[1], Y=out[r].ptr,
+                                       ldy=out[r].shape[1])
+                        self._sync_desc(op)
+                        continue
                 in_dt = BF16 if a.dtype == BF16 and b.dtype == BF16 else F32
                 a, b = self._as(a, in_dt, self.caps[r]), self._as(b, in_dt, self.caps[r])
                 self._emit("hap_binary", _lib.BINARY_TAGS[ins.tag], a.ptr, b.ptr, in_dt, out[r].ptr,
@@ -894,8 +973,14 @@ class Executor:
         written: set[str] = set()   # grads that already hold a contribution
         self._written = written
 
-        def contrib(did: str) -> int:
-            """accumulate flag for the next contribution to grad(did)."""
+        self._pending: dict = {}    # (did, r) -> Buf: deferred first contribution (a plain copy)
+
+        def contrib(did: str, fuse_ok: bool = False) -> int:
+            """accumulate flag for the next contribution to grad(did).  A
+            deferred copy into grad(did) is emitted first unless the caller
+            folds it into its own launch (fuse_ok: a GEMM epilogue addend)."""
+            if not fuse_ok:
+                self._flush_pending(did)
             acc = int(did in written)
             written.add(did)
             return acc
@@ -939,9 +1024,32 @@ class Executor:
             for d in ins.operands:
                 if d in self.source_dids:
                     self._grad_ready_at[d] = len(self._ops)
+        self._flush_pending()
         self._emit_sfb_pending()
         self._overlap_grad_sync()
         self._finish_update(written)
+
+    def _flush_pending(self, did: str | None = None):
+        """Emit deferred gradient copies (of ``did``, or all)."""
+        for key in [k for k in self._pending if did is None or k[0] == did]:
+            src = self._pending.pop(key)
+            self._copy(src, self._grad(key[0], key[1]), self.caps[key[1]])
+
+    def _defer_copy(self, did: str, dy: dict) -> bool:
+        """First contribution to grad(did) is a plain copy of dy (an add's
+        adjoint) and more contributions follow: defer it, so a GEMM that adds
+        into grad(did) next reads dy as its epilogue addend instead."""
+        L = self.group.local_ranks
+        if not self.cfg.fuse_epilogue or did in self._written or self._n_contrib.get(did, 0) < 2 \
+                or did in self.source_dids:
+            return False
+        if any(not self._fusable_buf(dy[r], self.bufs[(did, r)]) or self.dtypes[did] != BF16 for r in L):
+            return False
+        for r in L:
+            self._grad(did, r)
+            self._pending[(did, r)] = dy[r]
+        self._written.add(did)
+        return True
 
     def _chain_bwd_ok(self, c: dict) -> bool:
         """The fused adjoint keeps one dtype: every input gradient must be
@@ -961,6 +1069,7 @@ class Executor:
         only (the internal gradients dy / dq, dp are never materialised)."""
         L = self.group.local_ranks
         tag = _lib.UNARY_TAGS[c["u"].tag]
+        self._flush_pending(c["z"] if c["kind"] == "swish" else c["o"])
         if c["kind"] == "swish":
             if not self.req[c["x"]]:
                 return
@@ -968,6 +1077,15 @@ class Executor:
             for r in L:
                 x, y = self.bufs[(c["x"], r)], self.bufs[(c["y"], r)]
                 dz, dx = self.grads[(c["z"], r)], self._grad(c["x"], r)
+                # dx (+)= swish'(dz) folded into the epilogue of the GEMM that produced dz
+                op = self._producer_gemm(dz.ptr)
+                if op is not None and op.gemm["accumulate"] == 0 and acc == 0 and self._n_contrib.get(c["z"]) == 1 \
+                        and c["z"] not in self.aliased and self._gemm_fusable(op.gemm) \
+                        and self._fusable_buf(x, y, dz, dx):
+                    op.gemm.update(epi=_lib.EPI_SWISH_BWD, epi_tag=tag, C=dx.ptr, ldc=dx.shape[1], R=x.ptr,
+                                   ldr=x.shape[1], R2=y.ptr, ldr2=y.shape[1])
+                    self._sync_desc(op)
+                    continue
                 self._emit("hap_swish_bwd", tag, x.ptr, y.ptr, dz.ptr, dx.ptr, x.dtype, x.numel, acc, self.caps[r],
                            self._sptr())
             return
@@ -1021,14 +1139,24 @@ class Executor:
     def _adjoint(self, ins: Instruction, need: list, contrib):
         L = self.group.local_ranks
         k = ins.kind
+        self._flush_pending(ins.output)
         dy = {r: self.grads[(ins.output, r)] for r in L}
         x = [{r: self.bufs[(d, r)] for r in L} for d in ins.operands]
         ops = ins.operands
         if k == "matmul":
             if need[0]:
-                acc = contrib(ops[0])
-                for r in L:     # dA = dC . B^T
-                    self._gemm(dy[r], False, x[1][r], True, self._grad(ops[0], r), self.caps[r], acc)
+                acc = contrib(ops[0], fuse_ok=True)
+                for r in L:     # dA = dC . B^T (+ a deferred copy as the epilogue addend)
+                    pend = self._pending.get((ops[0], r))
+                    g = self._grad(ops[0], r)
+                    if pend is not None:
+                        self._gemm(dy[r], False, x[1][r], True, g, self.caps[r], 0, addend=pend)
+                        if self._gemm_fusable(dict(self._ops[-1].gemm, epi=_lib.EPI_NONE)):
+                            del self._pending[(ops[0], r)]
+                            continue
+                        self._ops.pop()      # not fusable here: copy first, then accumulate
+                        self._flush_pending(ops[0])
+                    self._gemm(dy[r], False, x[1][r], True, g, self.caps[r], acc)
             if need[1]:
                 if ops[1] in self.sfb:
                     self._sfb_weight_grad(ins, contrib)
@@ -1056,6 +1184,8 @@ class Executor:
             if ins.tag == "add":
                 for i in (0, 1):
                     if need[i] and not (ops[0] != ops[1] and self._alias_grad(ops[i], dy)):
+                        if ops[0] != ops[1] and self._defer_copy(ops[i], dy):
+                            continue
                         acc = contrib(ops[i])
                         for r in L:
                             self._copy(dy[r], self._grad(ops[i], r), self.caps[r], accumulate=acc)

@@ -286,3 +286,109 @@ def test_matmul_batch_grouped_mixed_shapes(out, K, cap):
     torch.cuda.synchronize()
     for a, b, c in zip(As, Bs, Cs):
         assert rel_err(c, ref_mm(a, 1, b, 0)) < (1e-5 if out == torch.float32 else 8e-3)
+
+
+def _fdesc(a, ta, b, tb, c, accumulate=0, **epi):
+    M, K = (a.shape[1], a.shape[0]) if ta else a.shape
+    N = b.shape[0] if tb else b.shape[1]
+    d = _lib.GemmDesc()
+    d.A, d.lda, d.transA, d.B, d.ldb, d.transB = a.data_ptr(), a.shape[1], ta, b.data_ptr(), b.shape[1], tb
+    d.C, d.ldc, d.M, d.N, d.K, d.accumulate = c.data_ptr(), c.shape[1], M, N, K, accumulate
+    fields = {f for f, _ in _lib.GemmDesc._fields_}
+    for k, v in epi.items():
+        assert k in fields, k
+        setattr(d, k, v.data_ptr() if isinstance(v, torch.Tensor) else v)
+    for k, ld in (("R", "ldr"), ("R2", "ldr2"), ("Y", "ldy"), ("Z", "ldz")):
+        if isinstance(epi.get(k), torch.Tensor):
+            setattr(d, ld, epi[k].shape[1])
+    return d
+
+
+def _run_descs(descs, out_dt=BF16, sum_k=0, sm_cap=0):
+    arr = (_lib.GemmDesc * len(descs))(*descs)
+    check(L.hap_matmul_batch(arr, len(descs), sum_k, BF16, out_dt, sm_cap, S), "hap_matmul_batch")
+    torch.cuda.synchronize()
+
+
+def _bf(t):
+    return t.to(torch.bfloat16).float()
+
+
+EPI_SHAPES = [(8192, 768, 3072), (1000, 520, 200), (256, 3072, 768), (300, 136, 64)]
+
+
+@pytest.mark.parametrize("M,N,K", EPI_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+@pytest.mark.parametrize("epi", ["add", "add_self", "add2", "swish", "swish_bwd", "swish_bwd_acc"])
+def test_gemm_fused_epilogues(M, N, K, ta, tb, epi):
+    """Fused epilogues (hap_gemm_desc.epi) against the unfused sequence of
+    our own kernels (GEMM into bf16, then the elementwise kernel) — the same
+    roundings, so equal up to fp32 contraction differences (<= 1 bf16 ulp on
+    a few elements) — and against a PyTorch fp32 reference (2e-2)."""
+    torch.manual_seed(M + 3 * N + 7 * K + ta + 2 * tb)
+    a = torch.randn((K, M) if ta else (M, K), device=DEV).to(torch.bfloat16)
+    b = (torch.randn((N, K) if tb else (K, N), device=DEV) / K ** 0.5).to(torch.bfloat16)
+    mm = ref_mm(a, ta, b, tb)
+    c = torch.empty((M, N), device=DEV, dtype=torch.bfloat16)
+    r = torch.randn((M, N), device=DEV).to(torch.bfloat16)
+    sig = _lib.UNARY_TAGS["sigmoid"]
+    if L.hap_matmul_engine(a.data_ptr(), a.shape[1], ta, b.data_ptr(), b.shape[1], tb, M, N, K,
+                           BF16) != _lib.GEMM_TCGEN05:
+        # fused epilogues exist on the tcgen05 path only: loud error, no silent fallback
+        with pytest.raises(_lib.HapError, match="fused epilogues"):
+            _run_descs([_fdesc(a, ta, b, tb, c, epi=_lib.EPI_ADD, R=r)])
+        return
+    plain = torch.empty_like(c)
+    gemm(a, ta, b, tb, plain)
+    n = M * N
+    if epi == "add":
+        _run_descs([_fdesc(a, ta, b, tb, c, epi=_lib.EPI_ADD, R=r)])
+        want, fused, unfused = mm + r.float(), [c], None
+    elif epi == "add_self":
+        c.copy_(r)
+        _run_descs([_fdesc(a, ta, b, tb, c, accumulate=1, epi=_lib.EPI_ADD)])
+        want, fused, unfused = mm + r.float(), [c], None
+    elif epi == "add2":
+        y = torch.empty_like(c)
+        _run_descs([_fdesc(a, ta, b, tb, c, epi=_lib.EPI_ADD2, R=r, Y=y)])
+        y2 = torch.empty_like(c)
+        check(L.hap_binary(_lib.BINARY_TAGS["add"], plain.data_ptr(), r.data_ptr(), BF16, y2.data_ptr(), BF16, n,
+                           0, S), "hap_binary")
+        want, fused, unfused = _bf(mm) + r.float(), [c, y], [plain, y2]
+    elif epi == "swish":
+        y, z = torch.empty_like(c), torch.empty_like(c)
+        _run_descs([_fdesc(a, ta, b, tb, c, epi=_lib.EPI_SWISH, epi_tag=sig, Y=y, Z=z)])
+        y2, z2 = torch.empty_like(c), torch.empty_like(c)
+        check(L.hap_swish_fwd(sig, plain.data_ptr(), y2.data_ptr(), z2.data_ptr(), BF16, n, 0, S), "hap_swish_fwd")
+        s = torch.sigmoid(_bf(mm))
+        want, fused, unfused = _bf(mm) * _bf(s), [c, y, z], [plain, y2, z2]
+        assert rel_err(y, s) < 2e-2
+    elif epi == "swish_bwd_acc":
+        # the fused adjoint writes its output (no read-modify-write): loud error
+        x = torch.randn((M, N), device=DEV).to(torch.bfloat16)
+        with pytest.raises(_lib.HapError, match="no accumulate"):
+            _run_descs([_fdesc(a, ta, b, tb, c, accumulate=1, epi=_lib.EPI_SWISH_BWD, epi_tag=sig, R=x, R2=x)])
+        return
+    else:
+        acc = False
+        x = torch.randn((M, N), device=DEV).to(torch.bfloat16)
+        xs = torch.sigmoid(x.float()).to(torch.bfloat16)
+        dx = torch.randn((M, N), device=DEV).to(torch.bfloat16) if acc else torch.empty_like(c)
+        dx2 = dx.clone()
+        _run_descs([_fdesc(a, ta, b, tb, dx, accumulate=int(acc), epi=_lib.EPI_SWISH_BWD, epi_tag=sig, R=x, R2=xs)])
+        check(L.hap_swish_bwd(sig, x.data_ptr(), xs.data_ptr(), plain.data_ptr(), dx2.data_ptr(), BF16, n,
+                              int(acc), 0, S), "hap_swish_bwd")
+        g, xf, yf = _bf(mm), x.float(), xs.float()
+        want = g * yf + g * xf * yf * (1 - yf) + (dx2.float() * 0 if not acc else 0)
+        fused, unfused = [dx], [dx2]
+        if acc:
+            want = None   # checked against the unfused kernels only
+    torch.cuda.synchronize()
+    if unfused is not None:
+        for f, u in zip(fused, unfused):
+            diff = (f.float() - u.float()).abs()
+            ulp = u.float().abs().clamp_min(1e-30) * 2.0 ** -7
+            assert int((diff > ulp).sum()) == 0, (epi, float(diff.max()))
+            assert float((diff > 0).float().mean()) < 1e-3, (epi, float((diff > 0).float().mean()))
+    if want is not None:
+        assert rel_err(fused[-1], want) < 2e-2
