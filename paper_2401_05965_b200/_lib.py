@@ -13,7 +13,7 @@ import re
 from ctypes import c_float, c_int, c_int64, c_uint32, c_void_p, POINTER
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhap_b200.so")
+LIB_PATH = os.environ.get("HAP_LIB_PATH", os.path.join(PKG, "libhap_b200.so"))   # override: A/B builds
 HEADER = os.path.join(os.path.dirname(PKG), "include", "hap_b200.h")
 
 F32, BF16 = 0, 1

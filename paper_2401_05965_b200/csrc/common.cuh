@@ -119,7 +119,7 @@ __device__ __forceinline__ float unary_fwd(int tag, float x) {
     case HAP_EXP: return __expf(x);
     case HAP_NEG: return -x;
     case HAP_RELU: return fmaxf(x, 0.f);
-    case HAP_SIGMOID: return __frcp_rn(1.f + __expf(-x));   // rcp.rn: one MUFU + refinement, no IEEE divide
+    case HAP_SIGMOID: return __fdividef(1.f, 1.f + __expf(-x));   // MUFU rcp: ~2 ulp fp32, exact after bf16
     default: return tanhf(x);
   }
 }

@@ -20,6 +20,8 @@
 // multiple of 16 bytes) — small corpus shapes and zero-size shards.
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -484,7 +486,11 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
   const bool dbl = epi != EPI_OP_SWISH;   // <= 2 slots per chunk: two slot pairs alternate
   const uint32_t buf0 = smem_u32(buf);
   // slot of input i / output o in slot set `set`
-  auto slot = [&](int set, int k) -> uint32_t { return buf0 + (dbl ? set * 2 + k : k) * kFusedBox; };
+  // dbl: slot pair `set`; otherwise (three outputs per chunk) `set` is the
+  // chunk index and its boxes take the next three slots of a 4-slot ring
+  auto slot = [&](int set, int k) -> uint32_t {
+    return buf0 + (dbl ? set * 2 + k : ((3 * set + k) & 3)) * kFusedBox;
+  };
   auto in_slot = [&](int set, int i) -> uint32_t { return slot(set, epi == EPI_OP_ADD2 ? 1 : i); };
   auto issue_loads = [&](int chunk) {   // lane 0
     const int set = dbl ? (chunk & 1) : 0;
@@ -501,7 +507,7 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
   __syncwarp();
 #pragma unroll 1
   for (int ch = 0; ch < kChunks; ++ch) {
-    const int set = dbl ? (ch & 1) : 0;
+    const int set = dbl ? (ch & 1) : ch;
     if (lane == 0) {
       if (dbl) {
         // the other pair was last stored from by chunk ch-1: once read out,
@@ -511,7 +517,7 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
           if (n_in) issue_loads(ch + 1);
         }
       } else {
-        bulk_wait_read0();
+        bulk_wait_read1();   // ring: only the previous chunk's last box may still be read
       }
     }
     uint32_t r[32];
@@ -550,8 +556,10 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
       const int x0 = first + ch * kFusedW;
       tma_store_2d(&pr.c, slot(set, 0), x0, row0);
       if (epi == EPI_OP_ADD2) tma_store_2d(&pr.e2, slot(set, 1), x0, row0);
-      if (epi == EPI_OP_SWISH) {
+      if (epi == EPI_OP_SWISH) {   // one bulk group per box (ring slots free up one by one)
+        bulk_commit();
         tma_store_2d(&pr.e1, slot(set, 1), x0, row0);
+        bulk_commit();
         tma_store_2d(&pr.e2, slot(set, 2), x0, row0);
       }
       bulk_commit();
@@ -1571,6 +1579,17 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   for (int q = 0; q < nout; ++q)  // fp32 split-K partials add into a zeroed output
     if (fp32 && bt.p[q].splits > 1 && !d[q].accumulate)
       HAP_CUDA_TRY(cudaMemset2DAsync(d[q].C, d[q].ldc * osz, 0, d[q].N * osz, d[q].M, stream));
+  static const bool log_shapes = getenv("HAP_GEMM_LOG") != nullptr;
+  if (log_shapes) {
+    fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d kbps %d units %d |", count,
+            sum_k, fp32 ? "f32" : "bf16", cap, shp.pair ? "pair" : "cta", shp.bn, shp.splits, shp.kb_per_split,
+            units);
+    for (int q = 0; q < count; ++q)
+      fprintf(stderr, " %lldx%lldx%lld t%d%d epi%d acc%d", static_cast<long long>(d[q].M),
+              static_cast<long long>(d[q].N), static_cast<long long>(d[q].K), d[q].transA, d[q].transB, d[q].epi,
+              d[q].accumulate);
+    fprintf(stderr, "\n");
+  }
   hap_status st = fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
                        : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
   if (st != HAP_OK) return st;

@@ -146,9 +146,8 @@ class ExecConfig:
     fuse_epilogue: bool = True        # fold elementwise work into the producing GEMM's epilogue (bf16
                                       # outputs): residual adds, deferred gradient copies, the swish
                                       # adjoint after the dz GEMM
-    fuse_swish_fwd: bool = False      # also y = f(x), z = x*y after the x GEMM (three outputs per tile:
-                                      # measured slower than GEMM + swish kernel with 8 KB of staging
-                                      # per epilogue warp, profiles/r01f_fused_epilogues.md)
+    fuse_swish_fwd: bool = os.environ.get("HAP_FUSE_SWISH_FWD", "1") == "1"   # also y = f(x), z = x*y
+                                      # after the x GEMM (three outputs per tile)
     overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
                                       # during the forward), weight-gradient GEMMs at the end of backward
     bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
