@@ -184,23 +184,32 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
-def cpu_baseline(steps: int, sample_batch: int, workload: str = "bert") -> dict:
+def cpu_baseline(steps: int, sample_batch: int, workload: str = "bert", budget_s: float = 30.0) -> dict:
     """Reference CPU path (the oracle port of the reference interpreter plus
-    its adjoint, float64 numpy) on a bounded sample of the same workload."""
-    import numpy as np
-    from threadpoolctl import threadpool_info
+    its adjoint, float64 numpy) on a bounded sample of the same workload:
+    up to ``steps`` train steps, stopping once ``budget_s`` seconds of CPU
+    work are measured, with every host core given to the BLAS pool (torchrun
+    sets OMP_NUM_THREADS=1 per rank)."""
+    import numpy as np  # noqa: F401
+    from threadpoolctl import threadpool_info, threadpool_limits
 
     from oracle import interpreter_np as O
     from paper_2401_05965_b200 import api, workloads
 
+    threadpool_limits(limits=os.cpu_count() or 1)
     g = _graph(workload, sample_batch)
     prog = O.Program(api.single_device_program(g).to_json())
     inputs = workloads.synthetic_inputs(g, 0, scaled=True)
     shapes = {n.id: n.shape for n in g.nodes}
     O.train_step(prog, 1, inputs, {}, shapes, lr=1e-3)  # warm
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < max(1, steps):
         O.train_step(prog, 1, inputs, {}, shapes, lr=1e-3)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    steps = done
     dt = (time.perf_counter() - t0) / steps
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     return {"value": sample_batch / dt, "unit": "samples/s", "cores": threads, "kind": "port",

@@ -211,6 +211,37 @@ __device__ __forceinline__ void red_row_chunk(float* dst, const uint32_t (&r)[32
 }
 
 
+// stream-K helpers: a cut tile's fp32 partial, column-major [BN][128] per CTA
+// (the TMEM lane = row is the fast index), so a warp's 32 lanes move one
+// column as one coalesced 128-byte access.
+__device__ __forceinline__ void add_partial(uint32_t (&r)[32], const float* p) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __ldcg(p + i * 128);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) + v[i]);
+}
+template <int BN>
+__device__ __forceinline__ void write_partial(uint32_t tmem_acc, int quarter, int half, int lane, float* part) {
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
+  float* col0 = part + (half * (BN / 2)) * 128 + quarter * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t r[32];
+    tmem_ld32(lane_base + c * 32, r);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) __stcg(col0 + (c * 32 + i) * 128, __uint_as_float(r[i]));
+  }
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -259,7 +290,8 @@ template <int BN, typename OutT>
 __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter, int half, int lane, int row0,
                                                   int col0, int M, int N, OutT* C, int64_t ldc, int mode,
                                                   int vec_ok, int accumulate, int splits,
-                                                  const CUtensorMap* tmC, uint8_t* buf, uint32_t& box_seq) {
+                                                  const CUtensorMap* tmC, uint8_t* buf, uint32_t& box_seq,
+                                                  const float* prow = nullptr) {
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16);
   const int first = col0 + half * (BN / 2);
   if (mode == EPI_DIRECT) {
@@ -302,6 +334,7 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
     for (int k = 0; k < W / 32; ++k) {
       uint32_t r[32];
       tmem_ld32(lane_base + half * (BN / 2) + b * W + k * 32, r);
+      if (prow) add_partial(r, prow + (b * W + k * 32) * 128);
       if constexpr (std::is_same<OutT, float>::value) {
         static_assert(W % 32 == 0 || W == 16, "fp32 box width");
 #pragma unroll
@@ -375,6 +408,18 @@ struct alignas(64) TcBatch {
   int sum_k;
   int sum_kb;              // sum_k: K blocks of all problems (the concatenated K range)
   int total_units;
+  // stream-K (SM-pair kernel, one problem): pair p walks K-block iterations
+  // [p*I/P, (p+1)*I/P) of the I = tiles x k_blocks iteration space, so every
+  // pair gets the same MMA work whatever the tile count; a tile cut by a range
+  // boundary is finished by the pair holding its first K blocks, after adding
+  // the fp32 partial of its last K blocks that the next pair wrote to slot
+  // (boundary index) of the workspace.
+  int sk;                  // 0: data-parallel units
+  int sk_kb;               // K blocks per tile
+  int sk_pairs;            // P
+  long long sk_iters;      // I
+  float* sk_ws;            // [P + 1][2 CTAs][128][BN] fp32 partial tiles
+  unsigned* sk_flags;      // [P + 1][2 CTAs][8 epilogue warps]: partial written
 };
 
 __device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
@@ -477,7 +522,8 @@ __device__ __forceinline__ void fused_chunk(const uint32_t (&r)[32], int lane, u
 
 template <int BN>
 __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half, int lane,
-                                            int row0, int col0, uint8_t* buf, uint32_t ld_bar0, uint32_t& ld_phase) {
+                                            int row0, int col0, uint8_t* buf, uint32_t ld_bar0, uint32_t& ld_phase,
+                                            const float* prow) {
   constexpr int kChunks = (BN / 2) / kFusedW;
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
   const int first = col0 + half * (BN / 2);
@@ -522,6 +568,7 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
     }
     uint32_t r[32];
     tmem_ld32(lane_base + ch * kFusedW, r);
+    if (prow) add_partial(r, prow + ch * kFusedW * 128);
     if (n_in) {
       mbar_wait(ld_bar0 + 8 * set, (ld_phase >> set) & 1);
       ld_phase ^= 1u << set;
@@ -575,10 +622,14 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
 template <int BN, typename OutT>
 __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
                                               int lane, int row0, int col0, int split, uint8_t* buf,
-                                              uint32_t& box_seq, uint32_t ld_bar, uint32_t& ld_phase) {
+                                              uint32_t& box_seq, uint32_t ld_bar, uint32_t& ld_phase,
+                                              const float* part) {
+  // part: stream-K partial of this CTA's 128 x BN share (column-major), added to
+  // the accumulator before anything is rounded
+  const float* prow = part ? part + (half * (BN / 2)) * 128 + quarter * 32 + lane : nullptr;
   if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
     if (pr.epi != EPI_OP_NONE) {
-      drain_fused<BN>(pr, tmem_acc, quarter, half, lane, row0, col0, buf, ld_bar, ld_phase);
+      drain_fused<BN>(pr, tmem_acc, quarter, half, lane, row0, col0, buf, ld_bar, ld_phase, prow);
       return;
     }
   }
@@ -588,11 +639,13 @@ __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem
     return;
   }
   drain_accumulator<BN, OutT>(tmem_acc, quarter, half, lane, row0, col0, pr.M, pr.N, static_cast<OutT*>(pr.C),
-                              pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, pr.splits, &pr.c, buf, box_seq);
+                              pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, pr.splits, &pr.c, buf, box_seq, prow);
 }
 
 struct Unit {
   int prob, split, m0, n0, kb0, kb1;
+  int sk_kind;   // 0: whole tile; 1: a tile's last K blocks (write partial); 2: its first (finish it)
+  int sk_slot;   // workspace slot of a cut tile
 };
 
 // Work unit u -> (problem, output tile, K-block range).  Grouped: units are
@@ -615,6 +668,50 @@ __device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
   x.kb1 = min(bt.sum_k ? bt.sum_kb : pr.k_blocks, x.kb0 + pr.kb_per_split);
   return x;
 }
+
+// The units one SM pair walks, in order: every num_pairs-th data-parallel
+// unit, or (stream-K) the pieces of its iteration range.  Producer, MMA issuer
+// and epilogue each run their own cursor and see the same sequence.
+template <int BN>
+struct PairCursor {
+  long long it = 0, end = 0;
+  int u = 0, step = 1, pair = 0;
+  __device__ PairCursor(const TcBatch& bt, int pair_, int num_pairs) : pair(pair_) {
+    if (bt.sk) {
+      it = static_cast<long long>(pair) * bt.sk_iters / bt.sk_pairs;
+      end = static_cast<long long>(pair + 1) * bt.sk_iters / bt.sk_pairs;
+    } else {
+      u = pair;
+      step = num_pairs;
+    }
+  }
+  __device__ bool next(const TcBatch& bt, Unit& x) {
+    if (!bt.sk) {
+      if (u >= bt.total_units) return false;
+      x = decode_unit<256, BN>(bt, u);
+      x.sk_kind = 0;
+      x.sk_slot = 0;
+      u += step;
+      return true;
+    }
+    if (it >= end) return false;
+    const TcProblem& pr = bt.p[0];
+    const int kb = bt.sk_kb;
+    const int tile = static_cast<int>(it / kb);
+    const int kb0 = static_cast<int>(it - static_cast<long long>(tile) * kb);
+    const int kb1 = static_cast<int>(min(static_cast<long long>(kb), kb0 + (end - it)));
+    x.prob = 0;
+    x.split = 0;
+    x.m0 = (tile % pr.m_tiles) * 256;
+    x.n0 = (tile / pr.m_tiles) * BN;
+    x.kb0 = kb0;
+    x.kb1 = kb1;
+    x.sk_kind = (kb0 == 0 && kb1 == kb) ? 0 : (kb1 == kb ? 1 : 2);
+    x.sk_slot = x.sk_kind == 1 ? pair : pair + 1;
+    it += kb1 - kb0;
+    return true;
+  }
+};
 
 // f(problem, k_block) for every K block a unit accumulates, in order (a sum
 // walks its slice [kb0, kb1) of the problems' concatenated K blocks).
@@ -773,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq, ld_bar, ld_phase);
+                              buf, box_seq, ld_bar, ld_phase, nullptr);
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
@@ -888,7 +985,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
-  const int num_units = bt.total_units;
 
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < bt.count; ++q) {
@@ -924,8 +1020,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < num_units; u += num_pairs) {
-        const Unit x = decode_unit<256, BN>(bt, u);
+      PairCursor<BN> cur(bt, pair, num_pairs);
+      Unit x;
+      while (cur.next(bt, x)) {
         const int m0 = x.m0 + 128 * static_cast<int>(rank);
         const int n0 = x.n0 + HB * static_cast<int>(rank);
         for_each_kblock(bt, x, [&](int q, int kb) {
@@ -968,8 +1065,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = pair; u < num_units; u += num_pairs) {
-        const Unit x = decode_unit<256, BN>(bt, u);
+      PairCursor<BN> cur(bt, pair, num_pairs);
+      Unit x;
+      while (cur.next(bt, x)) {
         mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -1009,14 +1107,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty = map_to_cta(tempty0, 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < num_units; u += num_pairs) {
-      const Unit x = decode_unit<256, BN>(bt, u);
+    PairCursor<BN> cur(bt, pair, num_pairs);
+    Unit x;
+    while (cur.next(bt, x)) {
       const TcProblem& pr = bt.p[x.prob];
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq, ld_bar, ld_phase);
+      // stream-K: this CTA's 128 x BN share of a cut tile's partial
+      float* part = nullptr;
+      unsigned* flag = nullptr;
+      if (x.sk_kind) {
+        part = bt.sk_ws + (static_cast<size_t>(x.sk_slot) * 2 + rank) * 128 * BN;
+        flag = bt.sk_flags + (static_cast<size_t>(x.sk_slot) * 2 + rank) * kEpiWarps + (warp - 4);
+      }
+      if (x.sk_kind == 1) {
+        write_partial<BN>(tmem_base + acc * BN, quarter, half, lane, part);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(flag, 1u);
+      } else {
+        if (x.sk_kind == 2) {
+          if (lane == 0)
+            while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+          __syncwarp();
+        }
+        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
+                                buf, box_seq, ld_bar, ld_phase, x.sk_kind == 2 ? part : nullptr);
+        if (x.sk_kind == 2 && lane == 0) *flag = 0u;   // consumed: ready for the next launch
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
@@ -1352,6 +1471,14 @@ int split_enabled() {
   return mode;
 }
 
+// HAP_GEMM_SK=1 enables stream-K (read per call, so tests can toggle it).
+// Off by default: measured on the bench shapes (profiles/r01f_stream_k.md) the
+// cut tiles' partial write + read costs more than the idle pairs it fills.
+int sk_enabled() {
+  const char* v = getenv("HAP_GEMM_SK");
+  return v ? atoi(v) : 0;
+}
+
 int pair_mode() {
   static int mode = [] {
     const char* v = getenv("HAP_GEMM_PAIR");
@@ -1430,6 +1557,37 @@ bool split_workspace(cudaStream_t stream, int64_t elems, float** out) {
   }
   w.elems = n;
   *out = w.ws;
+  return true;
+}
+
+// Stream-K partial tiles and flags, one set per stream (launches on a stream
+// are ordered; every flag is reset by the pair that consumes it).  Sized for
+// the largest grid (74 SM pairs + 1 slot, 256-wide tiles); allocated outside
+// stream capture only.
+bool sk_workspace(cudaStream_t stream, float** ws, unsigned** flags) {
+  struct SkWs {
+    float* ws = nullptr;
+    unsigned* flags = nullptr;
+  };
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, SkWs> table;
+  std::lock_guard<std::mutex> lock(mu);
+  SkWs& w = table[stream];
+  if (!w.ws) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    const size_t slots = 148 / 2 + 1;
+    if (cudaMalloc(reinterpret_cast<void**>(&w.ws), slots * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&w.flags), slots * 2 * tc::kEpiWarps * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(w.flags, 0, slots * 2 * tc::kEpiWarps * sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(w.ws);
+      w = SkWs{};
+      return false;
+    }
+  }
+  *ws = w.ws;
+  *flags = w.flags;
   return true;
 }
 
@@ -1576,14 +1734,37 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
   }
   bt.total_units = units;
+  // stream-K: one problem on SM pairs whose data-parallel rounds would leave
+  // pairs idle (tile counts are products of 2s and 3s, the pair count 74 is
+  // 2 x 37: the last round is rarely full).  Every pair gets the same number
+  // of K-block iterations; needs at least one whole tile per pair.
+  if (count == 1 && !sum_k && shp.pair && bt.p[0].splits == 1 && bt.p[0].epi_mode == tc::EPI_TMA_STORE &&
+      sk_enabled()) {
+    const int P = std::max(1, cap / 2);
+    const int64_t T = static_cast<int64_t>(bt.p[0].m_tiles) * bt.p[0].n_tiles;
+    const int64_t rounds = (T + P - 1) / P;
+    const double eff = static_cast<double>(T) / static_cast<double>(rounds * P);
+    float* skws = nullptr;
+    unsigned* skflags = nullptr;
+    // long tiles only: every cut costs an extra partial write / read and epilogue
+    if (T >= P && eff < 0.93 && bt.p[0].k_blocks >= 16 && sk_workspace(stream, &skws, &skflags)) {
+      bt.sk = 1;
+      bt.sk_kb = bt.p[0].k_blocks;
+      bt.sk_pairs = P;
+      bt.sk_iters = T * bt.p[0].k_blocks;
+      bt.sk_ws = skws;
+      bt.sk_flags = skflags;
+      bt.total_units = P;
+    }
+  }
   for (int q = 0; q < nout; ++q)  // fp32 split-K partials add into a zeroed output
     if (fp32 && bt.p[q].splits > 1 && !d[q].accumulate)
       HAP_CUDA_TRY(cudaMemset2DAsync(d[q].C, d[q].ldc * osz, 0, d[q].N * osz, d[q].M, stream));
   static const bool log_shapes = getenv("HAP_GEMM_LOG") != nullptr;
   if (log_shapes) {
-    fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d kbps %d units %d |", count,
-            sum_k, fp32 ? "f32" : "bf16", cap, shp.pair ? "pair" : "cta", shp.bn, shp.splits, shp.kb_per_split,
-            units);
+    fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d kbps %d units %d sk %d |",
+            count, sum_k, fp32 ? "f32" : "bf16", cap, shp.pair ? "pair" : "cta", shp.bn, shp.splits,
+            shp.kb_per_split, units, bt.sk);
     for (int q = 0; q < count; ++q)
       fprintf(stderr, " %lldx%lldx%lld t%d%d epi%d acc%d", static_cast<long long>(d[q].M),
               static_cast<long long>(d[q].N), static_cast<long long>(d[q].K), d[q].transA, d[q].transB, d[q].epi,

@@ -392,3 +392,46 @@ def test_gemm_fused_epilogues(M, N, K, ta, tb, epi):
             assert float((diff > 0).float().mean()) < 1e-3, (epi, float((diff > 0).float().mean()))
     if want is not None:
         assert rel_err(fused[-1], want) < 2e-2
+
+
+@pytest.mark.parametrize("cap", [0, 104, 88, 20])
+@pytest.mark.parametrize("M,N,K", [(8192, 768, 3072), (8192, 3072, 1536), (2048, 1000, 1040)])
+def test_stream_k_gemm_repeated_and_graph(M, N, K, cap, monkeypatch):
+    """Shapes whose data-parallel rounds leave SM pairs idle run stream-K
+    (equal K-block ranges per pair, cut tiles finished from an fp32 partial):
+    results match the fp32 reference, stay identical over repeated launches
+    (the partial flags reset themselves) and under CUDA-graph replay."""
+    monkeypatch.setenv("HAP_GEMM_SK", "1")   # opt-in path (off by default)
+    torch.manual_seed(M + N + K + cap)
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = (torch.randn(K, N, device=DEV) / K ** 0.5).to(torch.bfloat16)
+    r = torch.randn(M, N, device=DEV).to(torch.bfloat16)
+    want = ref_mm(a, 0, b, 0)
+    outs = []
+    for _ in range(3):
+        c = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+        gemm(a, 0, b, 0, c, sm_cap=cap)
+        outs.append(c)
+    assert rel_err(outs[0], want) < 8e-3
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    y = torch.empty_like(r)
+    c = torch.empty_like(r)
+    _run_descs([_fdesc(a, 0, b, 0, c, epi=_lib.EPI_ADD2, R=r, Y=y)], sm_cap=cap)
+    assert torch.equal(c, outs[0])
+    assert rel_err(y, want + r.float()) < 2e-2
+    # graph replay on a side stream
+    s = torch.cuda.Stream()
+    cg = torch.zeros(M, N, device=DEV, dtype=torch.bfloat16)
+    with torch.cuda.stream(s):
+        check(L.hap_matmul(a.data_ptr(), K, 0, b.data_ptr(), N, 0, cg.data_ptr(), N, M, N, K, BF16, BF16, 0, cap,
+                           s.cuda_stream), "warm")
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        check(L.hap_matmul(a.data_ptr(), K, 0, b.data_ptr(), N, 0, cg.data_ptr(), N, M, N, K, BF16, BF16, 0, cap,
+                           s.cuda_stream), "capture")
+    for _ in range(3):
+        cg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(cg, outs[0])

@@ -1,1 +1,3 @@
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:gemm_tc2 -c 1 -o gpurun_out/fused_swish2 python tools/fused_dbg.py 8192 3072 768 0 swish > gpurun_out/ncu_fused.log 2>&1; tail -1 gpurun_out/ncu_fused.log
+python tools/gemm_bench.py 2>&1 | head -6
+echo nosk; HAP_GEMM_SK=0 python tools/gemm_bench.py 2>&1 | head -6
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "stream_k or fused" 2>&1 | tail -1
