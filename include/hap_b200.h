@@ -106,6 +106,12 @@ typedef struct {
 enum { HAP_EPI_NONE = 0, HAP_EPI_ADD = 1, HAP_EPI_ADD2 = 2, HAP_EPI_SWISH = 3, HAP_EPI_SWISH_BWD = 4 };
 hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
                             hap_dtype out_dtype, int sm_cap, void* stream);
+/* Autotune: time every tile shape / split-K candidate of this batch (outputs
+ * written to scratch buffers, inputs only read; not during stream capture)
+ * and use the fastest for every later hap_matmul_batch / hap_matmul launch
+ * with the same extents, orientation, epilogue, output type and SM cap. */
+hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
+                           hap_dtype out_dtype, int sm_cap, void* stream);
 /* Which engine hap_matmul would use for these arguments (no launch). */
 int hap_matmul_engine(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                       int transB, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype);

@@ -44,6 +44,7 @@ SIGNATURES = {
     "hap_matmul": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, _P, c_int64, c_int64, c_int64,
                            c_int64, c_int, c_int, c_int, c_int, _P]),
     "hap_matmul_batch": (c_int, [POINTER(GemmDesc), c_int, c_int, c_int, c_int, c_int, _P]),
+    "hap_matmul_tune": (c_int, [POINTER(GemmDesc), c_int, c_int, c_int, c_int, c_int, _P]),
     "hap_matmul_engine": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, c_int64, c_int64, c_int64,
                                   c_int]),
     "hap_unary": (c_int, [c_int, _P, c_int, _P, c_int, c_int64, c_int, _P]),

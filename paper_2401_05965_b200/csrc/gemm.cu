@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <vector>
 #include <unordered_map>
 
@@ -1317,6 +1318,39 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
   return plain.score > 0 ? plain.s : split.s;
 }
 
+// Every tile shape / split choose_shape considers (the autotuner times them).
+void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k,
+                      bool allow_split, int cap, int allow_pair, std::vector<Shape>& out) {
+  int64_t k_blocks = 0;
+  for (int q = 0; q < count; ++q) {
+    const int64_t kb = (Ks[q] + BK - 1) / BK;
+    k_blocks = sum_k ? k_blocks + kb : std::max(k_blocks, kb);
+  }
+  int64_t min_m = Ms[0];
+  for (int q = 0; q < count; ++q) min_m = std::min(min_m, Ms[q]);
+  const struct { bool pair; int bn; } cs[] = {{true, 256}, {true, 192}, {true, 128}, {false, 256}, {false, 128}};
+  for (const auto& c : cs) {
+    if (c.pair && (!allow_pair || min_m < 256 || cap < 2)) continue;
+    const int64_t rows = c.pair ? 256 : 128;
+    const int64_t slots = c.pair ? cap / 2 : cap;
+    int64_t tiles = 0;
+    for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
+    out.push_back({c.bn, 1, static_cast<int>(k_blocks), c.pair});
+    if (!allow_split || tiles >= slots || k_blocks < 8) continue;
+    const int64_t top = std::max<int64_t>(1, std::min<int64_t>(slots / tiles, k_blocks / 4));
+    for (int64_t want : {int64_t(2), top}) {
+      if (want < 2 || want > top) continue;
+      const int64_t kps = (k_blocks + want - 1) / want;
+      const int64_t splits = (k_blocks + kps - 1) / kps;
+      if (splits < 2) continue;
+      Shape sh{c.bn, static_cast<int>(splits), static_cast<int>(kps), c.pair};
+      bool dup = false;
+      for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits);
+      if (!dup) out.push_back(sh);
+    }
+  }
+}
+
 // C (+)= sum over s of ws[s] — the K splits' partial tiles added in split
 // order (fixed, so repeated launches give identical bits).  A thread owns 4
 // consecutive columns of a row; every split's load is issued before the sum.
@@ -1593,11 +1627,34 @@ bool sk_workspace(cudaStream_t stream, float** ws, unsigned** flags) {
 
 inline int64_t ws_pitch(int64_t n) { return (n + 3) / 4 * 4; }   // 16-byte rows for the TMA map
 
+// Autotuned shapes (hap_matmul_tune), keyed by everything that decides the
+// shape: problem extents, orientation, epilogue, output type, SM cap.
+std::mutex& tune_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+std::unordered_map<std::string, tc::Shape>& tune_cache() {
+  static std::unordered_map<std::string, tc::Shape> cache;
+  return cache;
+}
+std::string tune_key(const hap_gemm_desc* d, int count, int sum_k, bool fp32, int cap) {
+  std::string k = std::to_string(count) + "/" + std::to_string(sum_k) + "/" + (fp32 ? "f" : "b") + "/" +
+                  std::to_string(cap);
+  for (int q = 0; q < count; ++q) {
+    const hap_gemm_desc& g = d[q];
+    k += "|" + std::to_string(g.M) + "x" + std::to_string(g.N) + "x" + std::to_string(g.K) + ":" +
+         std::to_string(g.transA) + std::to_string(g.transB) + ":" + std::to_string(g.epi) + ":" +
+         std::to_string(g.accumulate) + ":" + std::to_string(g.lda) + "," + std::to_string(g.ldb) + "," +
+         std::to_string(g.ldc);
+  }
+  return k;
+}
+
 // Build and launch one tcgen05 batch (all problems tc-eligible, same
 // orientation, <= kMaxProblems).  sum_k: every problem adds into problem 0's
 // output (same C, M, N), accumulate taken from problem 0.
 hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_dtype, int sm_cap,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, const tc::Shape* force = nullptr) {
   const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
   int64_t Ms[tc::kMaxProblems], Ns[tc::kMaxProblems], Ks[tc::kMaxProblems];
   for (int q = 0; q < count; ++q) {
@@ -1613,6 +1670,13 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   // a fused epilogue runs once per output tile: no split K
   tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && !fused, fp32, cap,
                                    pair_mode());
+  if (force) {
+    shp = *force;
+  } else {
+    std::lock_guard<std::mutex> lock(tune_mutex());
+    auto it = tune_cache().find(tune_key(d, count, sum_k, fp32, cap));
+    if (it != tune_cache().end()) shp = it->second;
+  }
   // split-K partial slices: splits x (M rounded up to whole tiles) x pitch(N)
   // fp32 per output; without room for them (capture), no split
   float* ws = nullptr;
@@ -1823,6 +1887,110 @@ bool degenerate(const hap_gemm_desc& g, hap_dtype out_dtype, cudaStream_t stream
 }
 
 }  // namespace
+
+// Time every candidate tile shape / split of this batch on `stream` (outputs
+// redirected to scratch buffers, inputs only read) and remember the fastest
+// for later launches of the same signature.  Not during stream capture.
+extern "C" hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
+                                      hap_dtype out_dtype, int sm_cap, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  HAP_CHECK_ARG(descs && count >= 0, "hap_matmul_tune: bad arguments");
+  if (count == 0 || count > tc::kMaxProblems) return HAP_OK;
+  for (int q = 0; q < count; ++q) {
+    const hap_gemm_desc& g = descs[q];
+    if (!(g.M > 0 && g.N > 0 && g.K > 0 && g.transA == descs[0].transA && g.transB == descs[0].transB &&
+          tc_eligible(g.A, g.lda, g.transA, g.B, g.ldb, g.transB, g.M, g.N, g.K, in_dtype)))
+      return HAP_OK;   // runs on the SIMT path or one by one: nothing to tune
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HAP_CUDA_TRY(cudaStreamIsCapturing(stream, &cs));
+  HAP_CHECK_ARG(cs == cudaStreamCaptureStatusNone, "hap_matmul_tune: not during stream capture");
+  const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
+  const bool fp32 = out_dtype == HAP_F32;
+  const int nout = sum_k ? 1 : count;
+  bool fused = false;
+  for (int q = 0; q < nout; ++q) fused = fused || descs[q].epi != HAP_EPI_NONE;
+  int64_t Ms[tc::kMaxProblems], Ns[tc::kMaxProblems], Ks[tc::kMaxProblems];
+  for (int q = 0; q < count; ++q) {
+    Ms[q] = descs[q].M;
+    Ns[q] = descs[q].N;
+    Ks[q] = descs[q].K;
+  }
+  std::vector<tc::Shape> cands;
+  tc::candidate_shapes(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && !fused, cap, pair_mode(), cands);
+  if (cands.size() < 2) return HAP_OK;
+  // scratch outputs: every written tensor of the batch
+  const size_t osz = dtype_size(out_dtype);
+  std::vector<void*> scratch;
+  hap_gemm_desc t[tc::kMaxProblems];
+  auto scratch_like = [&](int64_t rows, int64_t ld, size_t es) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, static_cast<size_t>(rows) * ld * es) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    scratch.push_back(p);
+    return p;
+  };
+  bool ok = true;
+  for (int q = 0; q < count && ok; ++q) {
+    t[q] = descs[q];
+    if (sum_k && q > 0) {
+      t[q].C = t[0].C;
+      continue;
+    }
+    const void* origC = descs[q].C;
+    t[q].C = scratch_like(descs[q].M, descs[q].ldc, osz);
+    ok = t[q].C != nullptr;
+    if (descs[q].epi == HAP_EPI_ADD && descs[q].accumulate) {
+      t[q].R = origC;   // the addend stays the real (read-only) C
+      t[q].ldr = descs[q].ldc;
+      t[q].accumulate = 0;
+    }
+    if (ok && descs[q].Y) ok = (t[q].Y = scratch_like(descs[q].M, descs[q].ldy, 2)) != nullptr;
+    if (ok && descs[q].Z) ok = (t[q].Z = scratch_like(descs[q].M, descs[q].ldz, 2)) != nullptr;
+  }
+  hap_status result = HAP_OK;
+  if (ok) {
+    cudaEvent_t e0, e1;
+    HAP_CUDA_TRY(cudaEventCreate(&e0));
+    HAP_CUDA_TRY(cudaEventCreate(&e1));
+    float best_ms = 1e30f;
+    tc::Shape best = cands[0];
+    for (const tc::Shape& c : cands) {
+      bool good = true;
+      for (int w = 0; w < 2 && good; ++w) good = tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c) == HAP_OK;
+      if (!good) {
+        cudaGetLastError();
+        continue;
+      }
+      constexpr int kReps = 5;
+      cudaEventRecord(e0, stream);
+      for (int r = 0; r < kReps; ++r) tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c);
+      cudaEventRecord(e1, stream);
+      if (cudaEventSynchronize(e1) != cudaSuccess) {
+        result = HAP_ERR_CUDA;
+        set_error("hap_matmul_tune: a candidate launch failed");
+        break;
+      }
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best_ms) {
+        best_ms = ms;
+        best = c;
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (result == HAP_OK) {
+      std::lock_guard<std::mutex> lock(tune_mutex());
+      tune_cache()[tune_key(descs, count, sum_k, fp32, cap)] = best;
+    }
+  }
+  cudaStreamSynchronize(stream);
+  for (void* p : scratch) cudaFree(p);
+  return result;
+}
 
 extern "C" hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
                                        hap_dtype out_dtype, int sm_cap, void* stream_) {

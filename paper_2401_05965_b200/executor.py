@@ -151,6 +151,8 @@ class ExecConfig:
     overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
                                       # during the forward), weight-gradient GEMMs at the end of backward
     bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
+    autotune: bool = os.environ.get("HAP_AUTOTUNE", "1") == "1"   # time each GEMM signature's tile shapes /
+                                      # split-K once at compile time (hap_matmul_tune) and keep the fastest
 
 
 @dataclass
@@ -243,7 +245,28 @@ class Executor:
         if self.cfg.batch_gemms:
             self.ops_fwd[:] = self._batch_gemms(self.ops_fwd)
             self.ops_bwd[:] = self._batch_gemms(self.ops_bwd)
+        if self.cfg.autotune and self.wdt == BF16:
+            self._autotune()
         self._create_symm()
+
+    def _autotune(self):
+        """One hap_matmul_tune per distinct GEMM launch signature (layers
+        repeat shapes): the library times every tile shape / split of the
+        batch on scratch outputs and uses the fastest from then on."""
+        seen = set()
+        for op in self.ops_fwd + self.ops_bwd:
+            if op.gemm is None:
+                continue
+            descs, count, sum_k, in_dt, out_dt, cap, stream = op.args
+            key = (count, sum_k, in_dt, out_dt, cap) + tuple(
+                (d.M, d.N, d.K, d.transA, d.transB, d.epi, d.accumulate, d.lda, d.ldb, d.ldc)
+                for d in descs[:count])
+            if key in seen:
+                continue
+            seen.add(key)
+            check(self.lib.hap_matmul_tune(descs, count, sum_k, in_dt, out_dt, cap, stream), "hap_matmul_tune")
+        torch.cuda.synchronize(self.device)
+        self.tuned_signatures = len(seen)
 
     # ------------------------------------------------------------------ analysis
     def _sizes(self, ref: str, axis: int) -> list[int]:

@@ -435,3 +435,37 @@ def test_stream_k_gemm_repeated_and_graph(M, N, K, cap, monkeypatch):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(cg, outs[0])
+
+
+@pytest.mark.parametrize("case", ["bf16", "f32_acc", "add_acc", "sum_k", "swish"])
+def test_matmul_tune_keeps_outputs_and_results(case):
+    """hap_matmul_tune times candidate shapes on scratch outputs: the real
+    outputs are untouched by tuning, and launches after tuning (with the
+    chosen shape) still match the fp32 reference."""
+    torch.manual_seed(5)
+    M, N, K = 4096, 1536, 1024
+    a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+    b = (torch.randn(K, N, device=DEV) / K ** 0.5).to(torch.bfloat16)
+    want = ref_mm(a, 0, b, 0)
+    out_dt = F32 if case == "f32_acc" else BF16
+    c = torch.randn(M, N, device=DEV).to(torch.float32 if case == "f32_acc" else torch.bfloat16)
+    base = c.clone()
+    if case == "bf16":
+        descs = [_fdesc(a, 0, b, 0, c)]
+    elif case in ("f32_acc", "add_acc"):
+        descs = [_fdesc(a, 0, b, 0, c, accumulate=1, **({"epi": _lib.EPI_ADD} if case == "add_acc" else {}))]
+        want = want + base.float()
+    elif case == "sum_k":
+        a2 = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+        descs = [_fdesc(a, 0, b, 0, c), _fdesc(a2, 0, b, 0, c, accumulate=1)]
+        want = want + ref_mm(a2, 0, b, 0)
+    else:
+        y, z = torch.empty_like(c), torch.empty_like(c)
+        descs = [_fdesc(a, 0, b, 0, c, epi=_lib.EPI_SWISH, epi_tag=_lib.UNARY_TAGS["sigmoid"], Y=y, Z=z)]
+    arr = (_lib.GemmDesc * len(descs))(*descs)
+    check(L.hap_matmul_tune(arr, len(descs), int(case == "sum_k"), BF16, out_dt, 0, S), "hap_matmul_tune")
+    torch.cuda.synchronize()
+    assert torch.equal(c, base)   # tuning wrote only scratch
+    check(L.hap_matmul_batch(arr, len(descs), int(case == "sum_k"), BF16, out_dt, 0, S), "hap_matmul_batch")
+    torch.cuda.synchronize()
+    assert rel_err(c, want) < (1e-5 if case == "f32_acc" else 1.2e-2)
