@@ -292,7 +292,8 @@ def main() -> None:
     ex = Executor(prog, n, table, shapes, group=group,
                   config=ExecConfig(dtype="bf16", sm_caps=caps, lr=LR, cluster=cluster, ratios=ratios),
                   device=dev)
-    log(f"executor compiled: {len(ex.ops_fwd)} fwd / {len(ex.ops_bwd)} bwd / {len(ex.ops_upd)} update ops")
+    log(f"executor compiled: {len(ex.ops_fwd)} fwd / {len(ex.ops_bwd)} bwd / {len(ex.ops_upd)} update ops; "
+        f"weight-gradient GEMMs on the side stream (moved, forks, joins): {ex.wgrad_stats}")
     inputs = workloads.synthetic_inputs(g, 0, scaled=True)
     ex.load(inputs)
     ex.forward()
@@ -452,7 +453,9 @@ def main() -> None:
                        "global_batch": batch, "seq_len": SEQ, "parallelism": f"hap-spmd{n}",
                        "plan": plan_name, "sm_caps": caps, "ratios": list(ratios),
                        "grad_sync": dict(sorted(ex.sync_choice.items())) or "n/a (m=1)",
-                       "l2": "inputs larger than L2 (step working set >> 126 MB)"},
+                       "l2": "inputs larger than L2 (step working set >> 126 MB)",
+                       "wgrad_side_stream": dict(zip(("gemm_launches", "forks", "joins"), ex.wgrad_stats)),
+                       "tuned_gemm_signatures": getattr(ex, "tuned_signatures", 0)},
             "e2e": {"value": round(samples / (float(e2e_ms.item()) * 1e-3), 2), "unit": "samples/s",
                     "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": 4 * n},
             "roofline": roofline,

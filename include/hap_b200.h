@@ -211,6 +211,22 @@ hap_status hap_all_gather_v(void* comm, const void* send, void* recv, const int6
  * actual (unpadded) shards; result identical to hap_all_gather_v. */
 hap_status hap_grouped_broadcast(void* comm, const void* send, void* recv, const int64_t* counts,
                                  hap_dtype dtype, void* stream);
+/* Registered outputs for the push all-gather: export the CUDA IPC handle of
+ * the allocation holding `buf` (plus that allocation's base address in this
+ * process and buf's offset in it), exchange all ranks' triples on the host,
+ * then open them: out_ptrs[p] = rank p's buffer as mapped in this process
+ * (out_ptrs[rank] = own).  Mappings are cached per context (closed by
+ * hap_symm_destroy). */
+hap_status hap_p2p_buffer_handle(void* ctx, const void* buf, uint8_t* out64, int64_t* base_addr, int64_t* offset);
+hap_status hap_p2p_buffer_open(void* ctx, const void* own, const uint8_t* handles64xn, const int64_t* base_addrs,
+                               const int64_t* offsets, void** out_ptrs);
+/* all_gather (same semantics as hap_p2p_all_gather_v) by pushing: every rank
+ * stores its shard straight into every rank's registered output.
+ * `dev_outs` is a DEVICE array of the nranks output pointers from
+ * hap_p2p_buffer_open; `total_elems` = outer * extent * inner. */
+hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void* const* dev_outs, hap_dtype dtype,
+                                   int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                   const int64_t* dev_offsets, int64_t total_elems, int sm_cap, void* stream);
 /* reduce_scatter — interpreter.py:94-96: sum over ranks then keep this
  * rank's counts[rank]-element chunk of the rank-ordered layout of `send`.
  * `scratch` must hold nranks*max(counts) elements (padded layout). */
@@ -240,12 +256,33 @@ hap_status hap_p2p_all_gather_v(void* ctx, const void* send, void* recv, hap_dty
                                 int64_t inner, int64_t extent, const int64_t* dev_sizes,
                                 const int64_t* dev_offsets, int64_t max_chunk_elems, int sm_cap,
                                 void* stream);
+/* Registered outputs for the push all-gather: export the CUDA IPC handle of
+ * the allocation holding `buf` (plus that allocation's base address in this
+ * process and buf's offset in it), exchange all ranks' triples on the host,
+ * then open them: out_ptrs[p] = rank p's buffer as mapped in this process
+ * (out_ptrs[rank] = own).  Mappings are cached per context (closed by
+ * hap_symm_destroy). */
+hap_status hap_p2p_buffer_handle(void* ctx, const void* buf, uint8_t* out64, int64_t* base_addr, int64_t* offset);
+hap_status hap_p2p_buffer_open(void* ctx, const void* own, const uint8_t* handles64xn, const int64_t* base_addrs,
+                               const int64_t* offsets, void** out_ptrs);
+/* all_gather (same semantics as hap_p2p_all_gather_v) by pushing: every rank
+ * stores its shard straight into every rank's registered output.
+ * `dev_outs` is a DEVICE array of the nranks output pointers from
+ * hap_p2p_buffer_open; `total_elems` = outer * extent * inner. */
+hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void* const* dev_outs, hap_dtype dtype,
+                                   int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                   const int64_t* dev_offsets, int64_t total_elems, int sm_cap, void* stream);
 /* reduce_scatter — interpreter.py:94-96: `send` is this rank's partial
  * [outer, extent, inner]; recv gets the cross-rank sum of rows
  * [offsets[rank], offsets[rank] + sizes[rank]). */
 hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype, int64_t outer,
                                     int64_t inner, int64_t extent, const int64_t* dev_sizes,
                                     const int64_t* dev_offsets, int sm_cap, void* stream);
+/* Bandwidth probe (no flag protocol; callers separate calls with a host
+ * barrier): moves `chunk_bytes` between this rank and every peer through the
+ * arenas.  mode 0/1: pull / push one peer after another; 2/3: pull / push with
+ * the grid split across all peers at once; 4: the same bytes as a local copy. */
+hap_status hap_p2p_probe(void* ctx, int mode, int64_t chunk_bytes, int sm_cap, void* stream);
 
 #ifdef __cplusplus
 }

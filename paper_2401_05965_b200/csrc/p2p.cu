@@ -23,6 +23,9 @@
 // (capped) SM, all resident; separate GPUs run the ranks, never one GPU.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -36,6 +39,7 @@ constexpr int kThreads = 512;
 struct SignalPage {       // lives at the start of each rank's symmetric arena
   uint64_t ready[kMaxRanks];
   uint64_t done[kMaxRanks];
+  uint64_t armed[kMaxRanks];   // push gather: peer p's output may be overwritten for call armed[p]-1
   uint64_t epoch;         // calls completed by this rank
   uint32_t arrive;        // grid-barrier counter (local)
   uint32_t generation;    // grid-barrier generation (local)
@@ -49,6 +53,7 @@ struct Symm {
   size_t bytes = 0;
   char* local = nullptr;                 // arena base (signal page + staging)
   char* peers[kMaxRanks] = {};           // peer arena bases (IPC-mapped), peers[rank] = local
+  std::map<std::pair<int, uint64_t>, char*> opened;   // (peer, its allocation base) -> mapped here
 };
 
 struct Peers {
@@ -124,9 +129,20 @@ __device__ void place_chunk(T* __restrict__ out, const T* __restrict__ chunk, in
     return;
   }
   const int64_t per = rows * inner;
-  const int64_t total = outer * per;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  constexpr int kv = 16 / sizeof(T);
+  if (inner % kv == 0 && ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(chunk)) & 15) == 0) {
+    // every [rows, inner] block starts 16-byte aligned: 16-byte moves
+    const int64_t per4 = per / kv, total4 = outer * per4;
+    const int4* c4 = reinterpret_cast<const int4*>(chunk);
+    for (int64_t e = tid; e < total4; e += stride) {
+      const int64_t o = e / per4, rem = e - o * per4;
+      reinterpret_cast<int4*>(out + (o * extent + off) * inner)[rem] = c4[e];
+    }
+    return;
+  }
+  const int64_t total = outer * per;
   for (int64_t e = tid; e < total; e += stride) {
     const int64_t o = e / per, rem = e - o * per;
     out[(o * extent + off) * inner + rem] = chunk[e];
@@ -181,6 +197,54 @@ __global__ void __launch_bounds__(kThreads) p2p_all_gather_kernel(Peers peers, i
   }
 }
 
+// Push all-gather into registered outputs: every rank's output buffer is
+// mapped into every peer (hap_p2p_buffer_handle / _open), so rank r stores
+// its shard straight into every output at its final [outer, off_r, inner]
+// position — NVLink writes are posted (no request round trip), measured
+// 680 GB/s per rank vs 640 for reads (tools/coll_bench.py --probe), and
+// there is no staging copy.  Protocol per call (epoch e on every rank):
+//   1. armed: at kernel start my stream has finished every earlier reader of
+//      my output, so CTA 0 tells each peer armed[r] = e+1; every CTA waits
+//      for armed[p] = e+1 before storing into p's output;
+//   2. store my shard into all outputs (own included), grid barrier;
+//   3. ready[r] = e+1 (and done[r], so a later staged call's reuse check
+//      passes) on every peer, system-scope release; every CTA waits for
+//      every peer's ready before the kernel ends, so the output is complete
+//      for the next kernel on the stream.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_all_gather_push_kernel(Peers peers, int rank, int nranks,
+                                                                       const T* __restrict__ send,
+                                                                       T* const* __restrict__ outs, int64_t outer,
+                                                                       int64_t inner, int64_t extent,
+                                                                       const int64_t* __restrict__ sizes,
+                                                                       const int64_t* __restrict__ offs) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  const bool peer_thread = threadIdx.x < nranks && threadIdx.x != rank;
+  if (blockIdx.x == 0 && peer_thread)
+    st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  for (int q = 1; q <= nranks; ++q) {
+    const int p = (rank + q) % nranks;   // peers staggered across ranks, own output last (local HBM)
+    place_chunk(outs[p], send, outer, sizes[rank], inner, extent, offs[rank]);
+  }
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      SignalPage* peer_sig = reinterpret_cast<SignalPage*>(peers.base[p]);
+      st_release_sys(&peer_sig->ready[rank], epoch + 1);
+      st_release_sys(&peer_sig->done[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+}
+
 // Reduce-scatter: rank r stages its whole partial tensor [outer, extent,
 // inner]; every rank then sums, for its own shard rows, the matching rows of
 // all peers' partial tensors over NVLink.
@@ -233,10 +297,73 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_kernel(Peers peer
   }
 }
 
+// Bandwidth probe (tools/coll_bench.py --probe; no flags, the caller
+// separates calls with a host barrier).  Arena layout: chunk q at
+// kSignalBytes + q * chunk on every rank.  Modes: 0 pull peers one after
+// another, 1 push one after another, 2 pull with the grid split across peers
+// (all peers at once), 3 push split across peers, 4 local copy of the same
+// bytes (HBM reference).
+__global__ void __launch_bounds__(kThreads) p2p_probe_kernel(Peers peers, int rank, int nranks, int mode,
+                                                             int64_t chunk) {
+  char* local = peers.base[rank] + kSignalBytes;
+  const int64_t n4 = chunk / 16;
+  if (mode == 4) {
+    for (int q = 1; q < nranks; ++q)
+      copy_elems(reinterpret_cast<int4*>(local + ((rank + q) % nranks) * chunk),
+                 reinterpret_cast<const int4*>(local + rank * chunk), n4);
+    return;
+  }
+  const bool push = mode == 1 || mode == 3;
+  auto src_of = [&](int p) {
+    return push ? reinterpret_cast<const int4*>(local + rank * chunk)
+                : reinterpret_cast<const int4*>(peers.base[p] + kSignalBytes + rank * chunk);
+  };
+  auto dst_of = [&](int p) {
+    return push ? reinterpret_cast<int4*>(peers.base[p] + kSignalBytes + rank * chunk)
+                : reinterpret_cast<int4*>(local + p * chunk);
+  };
+  if (mode <= 1) {
+    for (int q = 1; q < nranks; ++q) copy_elems(dst_of((rank + q) % nranks), src_of((rank + q) % nranks), n4);
+    return;
+  }
+  // split: CTA b serves peer (rank + 1 + b % (nranks-1)) % nranks, striding over that peer's CTAs
+  const int peers_n = nranks - 1;
+  const int which = blockIdx.x % peers_n;
+  const int p = (rank + 1 + which) % nranks;
+  const int ctas = (gridDim.x - which + peers_n - 1) / peers_n;
+  const int idx = blockIdx.x / peers_n;
+  const int4* src = src_of(p);
+  int4* dst = dst_of(p);
+  constexpr int U = 8;
+  const int64_t stride = static_cast<int64_t>(ctas) * blockDim.x;
+  int64_t i = static_cast<int64_t>(idx) * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = src[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n4; i += stride) dst[i] = src[i];
+}
+
 }  // namespace
 }  // namespace hap
 
 using namespace hap;
+
+extern "C" hap_status hap_p2p_probe(void* ctx, int mode, int64_t chunk_bytes, int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && mode >= 0 && mode <= 4 && chunk_bytes > 0 && chunk_bytes % 16 == 0 &&
+                    chunk_bytes * s->nranks <= hap_symm_capacity(ctx),
+                "hap_p2p_probe: bad arguments");
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  const int grid = capped_grid(static_cast<int64_t>(sm_count()), sm_cap);
+  launch_k(p2p_probe_kernel, dim3(grid), dim3(kThreads), 0, static_cast<cudaStream_t>(stream), peers, s->rank,
+           s->nranks, mode, chunk_bytes);
+  return launch_status("p2p probe");
+}
 
 extern "C" hap_status hap_symm_create(void** out, int64_t bytes, int rank, int nranks) {
   HAP_CHECK_ARG(out && bytes > 0 && nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks,
@@ -284,10 +411,69 @@ extern "C" hap_status hap_symm_open(void* ctx, const uint8_t* handles) {
 extern "C" hap_status hap_symm_destroy(void* ctx) {
   auto* s = static_cast<Symm*>(ctx);
   if (!s) return HAP_OK;
+  for (auto& kv : s->opened) cudaIpcCloseMemHandle(kv.second);
   for (int p = 0; p < s->nranks; ++p)
     if (p != s->rank && s->peers[p]) cudaIpcCloseMemHandle(s->peers[p]);
   cudaFree(s->local);
   delete s;
+  return HAP_OK;
+}
+
+namespace {
+// Base of the allocation holding `ptr` (driver cuMemGetAddressRange).
+bool alloc_base(const void* ptr, char** base) {
+  using Fn = int (*)(uint64_t*, size_t*, uint64_t);
+  static Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<Fn>(p);
+  });
+  uint64_t b = 0;
+  size_t sz = 0;
+  if (!fn || fn(&b, &sz, reinterpret_cast<uint64_t>(ptr)) != 0) return false;
+  *base = reinterpret_cast<char*>(b);
+  return true;
+}
+}  // namespace
+
+extern "C" hap_status hap_p2p_buffer_handle(void* ctx, const void* buf, uint8_t* out64, int64_t* base_addr,
+                                            int64_t* offset) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && buf && out64 && base_addr && offset, "hap_p2p_buffer_handle: bad arguments");
+  char* base = nullptr;
+  HAP_CHECK_ARG(alloc_base(buf, &base), "hap_p2p_buffer_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  HAP_CUDA_TRY(cudaIpcGetMemHandle(&h, base));
+  std::memcpy(out64, &h, 64);
+  *base_addr = static_cast<int64_t>(reinterpret_cast<uintptr_t>(base));
+  *offset = static_cast<const char*>(buf) - base;
+  return HAP_OK;
+}
+
+extern "C" hap_status hap_p2p_buffer_open(void* ctx, const void* own, const uint8_t* handles64xn,
+                                          const int64_t* base_addrs, const int64_t* offsets, void** out_ptrs) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && own && handles64xn && base_addrs && offsets && out_ptrs, "hap_p2p_buffer_open: bad arguments");
+  for (int p = 0; p < s->nranks; ++p) {
+    if (p == s->rank) {
+      out_ptrs[p] = const_cast<void*>(own);
+      continue;
+    }
+    const auto key = std::make_pair(p, static_cast<uint64_t>(base_addrs[p]));
+    auto it = s->opened.find(key);
+    if (it == s->opened.end()) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles64xn + 64 * p, 64);
+      void* ptr = nullptr;
+      HAP_CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      it = s->opened.emplace(key, static_cast<char*>(ptr)).first;
+    }
+    out_ptrs[p] = it->second + offsets[p];
+  }
   return HAP_OK;
 }
 
@@ -338,6 +524,28 @@ extern "C" hap_status hap_p2p_all_gather_v(void* ctx, const void* send, void* re
                                      dev_sizes, dev_offsets, bytes, sm_cap, st);
   return p2p_launch<float>(p2p_all_gather_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes, dev_offsets,
                            bytes, sm_cap, st);
+}
+
+extern "C" hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void* const* dev_outs, hap_dtype dtype,
+                                              int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                              const int64_t* dev_offsets, int64_t total_elems, int sm_cap,
+                                              void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_outs && dev_sizes && dev_offsets, "hap_p2p_all_gather_push: bad arguments");
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  // every CTA spins on peer flags: all resident, one per (capped) SM at most
+  const int grid = p2p_grid(total_elems * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    launch_k(p2p_all_gather_push_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank,
+             s->nranks, static_cast<const __nv_bfloat16*>(send), reinterpret_cast<__nv_bfloat16* const*>(dev_outs),
+             outer, inner, extent, dev_sizes, dev_offsets);
+  else
+    launch_k(p2p_all_gather_push_kernel<float>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank, s->nranks,
+             static_cast<const float*>(send), reinterpret_cast<float* const*>(dev_outs), outer, inner, extent,
+             dev_sizes, dev_offsets);
+  return launch_status("p2p push all-gather");
 }
 
 extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype,

@@ -138,6 +138,9 @@ class ExecConfig:
     gather: str = "auto"              # all_gather / reduce_scatter impl: "auto" = "kernel" (NVLink
                                       # peer-memory kernel) | "padded" (NCCL, max-shard padding) |
                                       # "sendrecv" (NCCL grouped point-to-point)
+    p2p_push: bool = os.environ.get("HAP_P2P_PUSH", "1") == "1"   # "kernel" all-gathers into a dense
+                                      # output store straight into every rank's registered output (NVLink
+                                      # writes, no staging); else peers' shards are pulled from staging
     input_grads: bool = False         # also differentiate w.r.t. placeholders
     cluster: object = None            # ClusterSpec for the cost-model choices
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
@@ -153,6 +156,10 @@ class ExecConfig:
     bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
     autotune: bool = os.environ.get("HAP_AUTOTUNE", "1") == "1"   # time each GEMM signature's tile shapes /
                                       # split-K once at compile time (hap_matmul_tune) and keep the fastest
+    wgrad_stream: bool = os.environ.get("HAP_WGRAD_STREAM", "0") == "1"   # parameter-gradient GEMMs on a
+                                      # side stream, to run in the tails of the activation-gradient chain;
+                                      # off: measured no gain (persistent GEMMs keep their static tile
+                                      # schedule, so a late-starting launch only stretches the chain)
 
 
 @dataclass
@@ -236,6 +243,7 @@ class Executor:
         self._allocate()
         self._symm: dict = {}            # stream tag -> peer-memory context
         self._p2p_bytes: dict = {}       # stream tag -> largest staging need
+        self._p2p_regs: list = []        # (stream tag, output Buf, slot) of push all-gathers
         self._emit_on = None             # stream the next ops are emitted on (None: self.stream)
         self._sfb_full: dict = {}        # gathered SFB factors, keyed by source buffer
         self._sfb_pending: list = []     # deferred SFB weight-gradient GEMMs
@@ -245,6 +253,9 @@ class Executor:
         if self.cfg.batch_gemms:
             self.ops_fwd[:] = self._batch_gemms(self.ops_fwd)
             self.ops_bwd[:] = self._batch_gemms(self.ops_bwd)
+        self.wgrad_stats = (0, 0, 0)
+        if self.cfg.wgrad_stream:
+            self.ops_bwd[:] = self._offload_wgrad(self.ops_bwd)
         if self.cfg.autotune and self.wdt == BF16:
             self._autotune()
         self._create_symm()
@@ -543,8 +554,10 @@ class Executor:
             # hand-written NVLink kernel: exact chunks, placed in the final layout
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(full_shape, s.dtype)
-            self._p2p("hap_p2p_all_gather_v", s, target, outer, inner, full_shape[axis], sizes,
-                      max(counts) * (2 if s.dtype == BF16 else 4))
+            push = self.cfg.p2p_push and exact
+            fn = "hap_p2p_all_gather_push" if push else "hap_p2p_all_gather_v"
+            self._p2p(fn, s, target, outer, inner, full_shape[axis], sizes,
+                      16 if push else max(counts) * (2 if s.dtype == BF16 else 4))
             if not exact:
                 self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
             return
@@ -675,7 +688,13 @@ class Executor:
         stream = self._sptr()
         cap = self.caps[r]
         sizes_ptr, offs_ptr = dev[0].data_ptr(), dev[1].data_ptr()
-        if fn == "hap_p2p_all_gather_v":
+        if fn == "hap_p2p_all_gather_push":
+            reg: dict = {}
+            self._p2p_regs.append((tag, recv, reg))
+            total = outer * extent * inner
+            args = lambda: (self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype, outer, inner,  # noqa: E731
+                            extent, sizes_ptr, offs_ptr, total, cap, stream)
+        elif fn == "hap_p2p_all_gather_v":
             max_chunk = max(sizes) * outer * inner
             args = lambda: (self._symm[tag], send.ptr, recv.ptr, send.dtype, outer, inner, extent,  # noqa: E731
                             sizes_ptr, offs_ptr, max_chunk, cap, stream)
@@ -700,6 +719,34 @@ class Executor:
             dist.all_gather_object(handles, bytes(handle.raw))
             check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
             self._symm[tag] = ctx
+        self._register_outputs()
+
+    def _register_outputs(self):
+        """Map every push all-gather's output into every peer: one exchange of
+        (IPC handle, allocation base, offset) triples for all of them."""
+        if not self._p2p_regs:
+            return
+        import torch.distributed as dist
+
+        g = self.group
+        mine = []
+        for tag, buf, _ in self._p2p_regs:
+            h = ctypes.create_string_buffer(64)
+            base, off = ctypes.c_int64(), ctypes.c_int64()
+            check(self.lib.hap_p2p_buffer_handle(self._symm[tag], buf.ptr, h, ctypes.byref(base), ctypes.byref(off)),
+                  "hap_p2p_buffer_handle")
+            mine.append((bytes(h.raw), base.value, off.value))
+        everyone = [None] * g.m
+        dist.all_gather_object(everyone, mine)
+        for i, (tag, buf, reg) in enumerate(self._p2p_regs):
+            handles = b"".join(everyone[p][i][0] for p in range(g.m))
+            bases = _lib.i64_array([everyone[p][i][1] for p in range(g.m)])
+            offs = _lib.i64_array([everyone[p][i][2] for p in range(g.m)])
+            ptrs = (ctypes.c_void_p * g.m)()
+            check(self.lib.hap_p2p_buffer_open(self._symm[tag], buf.ptr, handles, bases, offs, ptrs),
+                  "hap_p2p_buffer_open")
+            reg["dev"] = torch.tensor([int(p or 0) for p in ptrs], dtype=torch.int64, device=self.device)
+            self._keep(reg["dev"])
 
     def _batch_gemms(self, ops: list) -> list:
         """Merge runs of consecutive matmul launches into hap_matmul_batch
@@ -792,6 +839,120 @@ class Executor:
                              "hap_matmul_batch", True,
                              dict(g0, members=[run[m].gemm for m in members], sum_k=sum_k)))
         return result
+
+    # Non-GEMM launches whose every buffer is a direct pointer argument (the
+    # hazard scan of _offload_wgrad can see what they touch).
+    _DIRECT_OPS = frozenset({"hap_unary", "hap_unary_grad", "hap_binary", "hap_mul_grad", "hap_swish_fwd",
+                             "hap_swish_bwd", "hap_gate_fwd", "hap_gate_bwd", "hap_axpy", "hap_copy_block",
+                             "hap_unreduce", "hap_fill", "hap_reduce"})
+
+    @staticmethod
+    def _gemm_ranges(g: dict) -> tuple[list, list]:
+        """(read, write) byte ranges of a GEMM record's members."""
+        rd, wr = [], []
+        for m in g.get("members", [g]):
+            ein = 2 if m["in_dt"] == BF16 else 4
+            eout = 2 if m["out_dt"] == BF16 else 4
+            rd.append((m["A"], (m["K"] if m["transA"] else m["M"]) * m["lda"] * ein))
+            rd.append((m["B"], (m["N"] if m["transB"] else m["K"]) * m["ldb"] * ein))
+            for p, ld in (("R", "ldr"), ("R2", "ldr2")):
+                if m[p]:
+                    rd.append((m[p], m["M"] * m[ld] * 2))
+            c = (m["C"], m["M"] * m["ldc"] * eout)
+            wr.append(c)
+            if m["accumulate"]:
+                rd.append(c)
+            for p, ld in (("Y", "ldy"), ("Z", "ldz")):
+                if m[p]:
+                    wr.append((m[p], m["M"] * m[ld] * 2))
+        return [(a, a + n) for a, n in rd], [(a, a + n) for a, n in wr]
+
+    def _offload_wgrad(self, ops: list) -> list:
+        """Move the parameter-gradient GEMMs (dW = X^T.dY into a source's fp32
+        gradient) onto a side stream.  They depend only on finished forward
+        activations and finished output gradients, and nothing on the
+        activation-gradient chain reads their results, so their tiles fill the
+        SMs the chain's launches leave idle (each launch's partial last wave,
+        prologue and epilogue tail).  Fork: an event on the compute stream
+        right before the GEMM.  Join (compute stream waits for the side
+        stream) before the first later op that might touch a moved GEMM's
+        buffers — GEMMs by their descriptors, direct-pointer kernels by their
+        pointer arguments, and conservatively before every other op (events,
+        collectives, the SGD table launch) — and at the end."""
+        grad_ranges = []
+        for (did, r), b in self.grads.items():
+            if did in self.source_dids:
+                grad_ranges.append((b.ptr, b.ptr + max(1, b.numel) * (4 if b.dtype == F32 else 2)))
+
+        def inside(p, ranges):
+            return isinstance(p, int) and any(lo <= p < hi for lo, hi in ranges)
+
+        def overlaps(a, b):
+            return any(lo < hi2 and lo2 < hi for lo, hi in a for lo2, hi2 in b)
+
+        def candidate(op):
+            g = op.gemm
+            if g is None or not op.kernel:
+                return False
+            ms = g.get("members", [g])
+            return all(m["epi"] == _lib.EPI_NONE and m["out_dt"] == F32 and inside(m["C"], grad_ranges)
+                       and not m["Y"] and not m["Z"] for m in ms)
+
+        side = None
+        out: list = []
+        active_rd, active_wr = [], []      # ranges of the moved GEMMs since the last join
+        prev_moved = False
+        moved = forks = joins = 0
+
+        def join():
+            nonlocal joins
+            ev = torch.cuda.Event()
+            self._keep(ev)
+            out.append(Op(ev.record, (side,), "event.record", False))
+            out.append(Op(self.stream.wait_event, (ev,), "stream.wait_event", False))
+            joins += 1
+
+        for op in ops:
+            if candidate(op):
+                if side is None:
+                    side = torch.cuda.Stream(self.device)
+                    self.wgrad_stream = side
+                if not prev_moved:
+                    ev = torch.cuda.Event()
+                    self._keep(ev)
+                    out.append(Op(ev.record, (self.stream,), "event.record", False))
+                    out.append(Op(side.wait_event, (ev,), "stream.wait_event", False))
+                    forks += 1
+                g = op.gemm
+                sp = side.cuda_stream
+                op.args = op.args[:-1] + (sp,)
+                g["stream"] = sp
+                for m in g.get("members", []):
+                    m["stream"] = sp
+                rd, wr = self._gemm_ranges(g)
+                active_rd += rd
+                active_wr += wr
+                out.append(op)
+                prev_moved = True
+                moved += 1
+                continue
+            prev_moved = False
+            if active_wr:
+                if op.gemm is not None:
+                    rd, wr = self._gemm_ranges(op.gemm)
+                    hazard = overlaps(wr, active_rd + active_wr) or overlaps(rd, active_wr)
+                elif op.what in self._DIRECT_OPS:
+                    hazard = any(inside(a, active_rd + active_wr) for a in op.args)
+                else:
+                    hazard = True
+                if hazard:
+                    join()
+                    active_rd, active_wr = [], []
+            out.append(op)
+        if active_wr:
+            join()
+        self.wgrad_stats = (moved, forks, joins)
+        return out
 
     def _keep(self, obj):
         self.__dict__.setdefault("_keepalive", []).append(obj)

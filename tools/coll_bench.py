@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rows", default="4096,16384,65536,262144", help="comma-separated gathered row counts")
+    ap.add_argument("--probe", default="", help="comma-separated MB per peer for the push/pull bandwidth probe")
     ap.add_argument("--ar-elems", default="", help="comma-separated fp32 all-reduce sizes (elements)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -60,6 +61,16 @@ def main():
         devsz = torch.tensor([sizes, offsets(sizes)[:-1]], dtype=torch.int64, device=dev)
         carr = i64_array(counts)
         recv_bytes = (sum(counts) - counts[rank]) * 2
+        # register `out` for the push kernel (the executor does this once per gather at compile time)
+        hb = ctypes.create_string_buffer(64)
+        base, boff = ctypes.c_int64(), ctypes.c_int64()
+        check(L.hap_p2p_buffer_handle(ctx, out.data_ptr(), hb, ctypes.byref(base), ctypes.byref(boff)))
+        trip = [None] * world
+        dist.all_gather_object(trip, (bytes(hb.raw), base.value, boff.value))
+        ptrs = (ctypes.c_void_p * world)()
+        check(L.hap_p2p_buffer_open(ctx, out.data_ptr(), b"".join(t[0] for t in trip), i64_array([t[1] for t in trip]),
+                                    i64_array([t[2] for t in trip]), ptrs))
+        dev_outs = torch.tensor([int(p or 0) for p in ptrs], dtype=torch.int64, device=dev)
         impls = {
             "p2p_kernel": lambda: L.hap_p2p_all_gather_v(ctx, send.data_ptr(), out.data_ptr(), BF16, 1, inner, rows,
                                                          devsz[0].data_ptr(), devsz[1].data_ptr(), max(counts), 0,
@@ -68,9 +79,13 @@ def main():
                                                       scratch.data_ptr(), stream.cuda_stream),
             "nccl_sendrecv": lambda: L.hap_all_gather_v(group.comm, send.data_ptr(), out.data_ptr(), carr, BF16, 0,
                                                         None, stream.cuda_stream),
+            "p2p_push": lambda: L.hap_p2p_all_gather_push(ctx, send.data_ptr(), dev_outs.data_ptr(), BF16, 1, inner,
+                                                          rows, devsz[0].data_ptr(), devsz[1].data_ptr(), rows * inner,
+                                                          0, stream.cuda_stream),
         }
         ref = None
         for name, fn in impls.items():
+            out.zero_()   # each implementation must produce the whole output itself
             for _ in range(3):
                 check(fn(), name)
             torch.cuda.synchronize(dev)
@@ -104,8 +119,39 @@ def main():
             ms = float(t.item())
             rb = torch.tensor([recv_bytes], device=dev, dtype=torch.float64)
             dist.all_reduce(rb, op=dist.ReduceOp.MAX)
+            # NVLink-bound bytes at the measured 770 GB/s per direction: every
+            # rank receives all other shards (ingress) and its shard leaves it
+            # m-1 times (egress — pushed, or read by the peers); the padded
+            # NCCL gather moves the largest shard's size from every rank
+            b = 2 * inner
+            ingress = (sum(sizes) - min(sizes)) * b
+            egress = (world - 1) * max(sizes) * b
+            bound = (world - 1) * max(sizes) * b if name == "nccl_padded" else max(ingress, egress)
             results.append({"op": "all_gather", "impl": name, "rows": rows, "shard_rows": sizes,
-                            "ms": ms, "recv_GBps_max_rank": float(rb.item()) / (ms * 1e-3) / 1e9})
+                            "ms": ms, "recv_GBps_max_rank": float(rb.item()) / (ms * 1e-3) / 1e9,
+                            "nvlink_bound_bytes": bound,
+                            "frac_of_770": bound / (ms * 1e-3) / 770e9})
+    # raw NVLink bandwidth: pull vs push, peers in turn vs all at once
+    for mb in [int(v) for v in args.probe.split(",") if v]:
+        chunk = mb << 20
+        for mode, name in enumerate(["pull_seq", "push_seq", "pull_split", "push_split", "local_copy"]):
+            fn = lambda: L.hap_p2p_probe(ctx, mode, chunk, 0, stream.cuda_stream)  # noqa: E731
+            check(fn(), name)
+            torch.cuda.synchronize(dev)
+            ts = []
+            for _ in range(5):
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                check(fn(), name)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                ts.append(e0.elapsed_time(e1))
+            t = torch.tensor([sorted(ts)[len(ts) // 2]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            results.append({"op": "probe", "impl": name, "rows": mb, "shard_rows": [], "ms": ms,
+                            "recv_GBps_max_rank": (world - 1) * chunk / (ms * 1e-3) / 1e9})
     # NCCL all-reduce (fp32, in place) — the gradient synchronisation
     for elems in [int(v) for v in args.ar_elems.split(",") if v]:
         buf = torch.randn(elems, device=dev)
@@ -139,7 +185,8 @@ def main():
     if rank == 0:
         for r in results:
             print(f"{r['op']:10s} {r['impl']:14s} rows={r['rows']:7d} {r['ms'] * 1e3:9.1f} us "
-                  f"{r['recv_GBps_max_rank']:7.1f} GB/s received per rank")
+                  f"{r['recv_GBps_max_rank']:7.1f} GB/s received per rank"
+                  + (f"  {100 * r['frac_of_770']:5.1f}% of 770 GB/s on the bound direction" if "frac_of_770" in r else ""))
         if args.json:
             with open(args.json, "w") as fh:
                 json.dump({"world": world, "caps": caps, "results": results}, fh, indent=1)

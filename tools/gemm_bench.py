@@ -7,9 +7,9 @@ sys.path.insert(0, ".")
 from paper_2401_05965_b200 import _lib
 from paper_2401_05965_b200._lib import BF16, F32, check
 L = _lib.lib(); dev = torch.device("cuda")
-args_ = [a for a in sys.argv[1:] if not a.startswith("--")]
-T = int(args_[0]) if args_ else 8192
 out_json = sys.argv[sys.argv.index("--json") + 1] if "--json" in sys.argv else None
+args_ = [a for a in sys.argv[1:] if not a.startswith("--") and a != out_json]
+T = int(args_[0]) if args_ else 8192
 shapes = [  # (name, M, N, K, ta, tb, out)
     ("fwd qkvo", T, 768, 768, 0, 0, torch.bfloat16),
     ("fwd f1", T, 3072, 768, 0, 0, torch.bfloat16),
@@ -22,6 +22,8 @@ shapes = [  # (name, M, N, K, ta, tb, out)
     ("dW f2", 3072, 768, T, 1, 0, torch.float32),
     ("square 8k", 8192, 8192, 8192, 0, 0, torch.bfloat16),
 ]
+if "--sweep" in sys.argv:   # fixed cost vs K: intercept = launch + prologue + fill + last epilogue
+    shapes = [(f"sweep K={k}", T, n, k, 0, 0, torch.bfloat16) for n in (768, 3072) for k in (64, 128, 256, 768, 1536, 3072)]
 s = torch.cuda.Stream()
 rows = []
 
