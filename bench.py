@@ -230,7 +230,31 @@ def run_reference_arm(args, rank: int) -> None:
                        "global_batch": sample, "seq_len": SEQ, "parallelism": "cpu"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit_json(line)
+
+
+# stdout carries exactly one JSON line: libraries that print to fd 1 (NCCL's
+# version banner at communicator init) are pointed at stderr, and the
+# result is written to the saved original stdout.
+_STDOUT_FD = None
+
+
+def _quiet_stdout():
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit_json(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _STDOUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_STDOUT_FD, data)
 
 
 def main() -> None:
@@ -464,7 +488,7 @@ def main() -> None:
             "clocks": clk.summary(),
             "loss": losses[0],
         }
-        print(json.dumps(line), flush=True)
+        emit_json(line)
     ex.graph = None           # release the captured collectives before the communicator
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -476,4 +500,5 @@ def main() -> None:
 
 
 if __name__ == "__main__":
+    _quiet_stdout()
     main()

@@ -278,6 +278,14 @@ hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void* const* dev
 hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype, int64_t outer,
                                     int64_t inner, int64_t extent, const int64_t* dev_sizes,
                                     const int64_t* dev_offsets, int sm_cap, void* stream);
+/* reduce_scatter (same semantics as hap_p2p_reduce_scatter_v) straight out
+ * of every rank's registered partial: `dev_sends` is a DEVICE array of the
+ * nranks partial pointers from hap_p2p_buffer_open; `recv_elems` = this
+ * rank's outer * sizes[rank] * inner.  Returns (on the stream) only after
+ * every peer has finished reading this rank's partial. */
+hap_status hap_p2p_reduce_scatter_direct(void* ctx, const void* const* dev_sends, void* recv, hap_dtype dtype,
+                                         int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
+                                         const int64_t* dev_offsets, int64_t recv_elems, int sm_cap, void* stream);
 /* Bandwidth probe (no flag protocol; callers separate calls with a host
  * barrier): moves `chunk_bytes` between this rank and every peer through the
  * arenas.  mode 0/1: pull / push one peer after another; 2/3: pull / push with

@@ -81,6 +81,8 @@ SIGNATURES = {
     "hap_p2p_probe": (c_int, [_P, c_int, c_int64, c_int, _P]),
     "hap_p2p_buffer_handle": (c_int, [_P, _P, _P, POINTER(c_int64), POINTER(c_int64)]),
     "hap_p2p_buffer_open": (c_int, [_P, _P, _P, _P, _P, _P]),
+    "hap_p2p_reduce_scatter_direct": (c_int, [_P, _P, _P, c_int, c_int64, c_int64, c_int64, _P, _P, c_int64,
+                                              c_int, _P]),
     "hap_p2p_all_gather_push": (c_int, [_P, _P, _P, c_int, c_int64, c_int64, c_int64, _P, _P, c_int64, c_int,
                                         _P]),
     "hap_p2p_all_gather_v": (c_int, [_P, _P, _P, c_int, c_int64, c_int64, c_int64, _P, _P, c_int64, c_int,

@@ -347,6 +347,99 @@ __global__ void __launch_bounds__(kThreads) p2p_probe_kernel(Peers peers, int ra
   for (; i < n4; i += stride) dst[i] = src[i];
 }
 
+// Reduce-scatter straight out of registered partials: every rank's partial
+// tensor is mapped into every peer, so rank r sums its own shard rows from
+// all partials over NVLink with no staging copy.  Per call (epoch e):
+//   1. CTA 0 tells each peer ready[r] = e+1 (my partial is complete: the
+//      kernel started after its producers); every CTA waits for all peers;
+//   2. sum: 16-byte loads from every rank's partial (own from local HBM),
+//      fp32 accumulation in rank order (r, r+1, ...), one rounding;
+//   3. grid barrier, done[r] = e+1 on every peer (finished reading theirs);
+//      every CTA waits for every peer's done, so my partial is not
+//      overwritten by later work on my stream while a peer still reads it.
+template <typename T>
+__device__ __forceinline__ void add8(float* acc, const int4& v) {
+  if constexpr (sizeof(T) == 2) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      acc[2 * i] += f.x;
+      acc[2 * i + 1] += f.y;
+    }
+  } else {
+    const float* f = reinterpret_cast<const float*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] += f[i];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
+    Peers peers, int rank, int nranks, const T* const* __restrict__ sends, T* __restrict__ out, int64_t outer,
+    int64_t inner, int64_t extent, const int64_t* __restrict__ sizes, const int64_t* __restrict__ offs) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  const bool peer_thread = threadIdx.x < nranks && threadIdx.x != rank;
+  if (blockIdx.x == 0 && peer_thread)
+    st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->ready[rank], epoch + 1);
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  const int64_t rows = sizes[rank], off = offs[rank];
+  const int64_t per = rows * inner, total = outer * per;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  constexpr int kv = 16 / sizeof(T);
+  bool vec = inner % kv == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  for (int p = 0; p < nranks; ++p) vec = vec && (reinterpret_cast<uintptr_t>(sends[p]) & 15) == 0;
+  if (vec) {
+    const int64_t per4 = per / kv, total4 = outer * per4;
+    for (int64_t e = tid; e < total4; e += stride) {
+      const int64_t o = e / per4, rem = e - o * per4;
+      const int64_t at = (o * extent + off) * inner / kv + rem;   // int4 index in a partial
+      int4 v[kMaxRanks];   // every rank's load in flight before the sum (registers: fully unrolled)
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < nranks) v[q] = reinterpret_cast<const int4*>(sends[(rank + q) % nranks])[at];
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < nranks) add8<T>(acc, v[q]);
+      int4 r;
+      if constexpr (sizeof(T) == 2) {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      } else {
+        float* f = reinterpret_cast<float*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i] = acc[i];
+      }
+      reinterpret_cast<int4*>(out)[e] = r;
+    }
+  } else {
+    for (int64_t e = tid; e < total; e += stride) {
+      const int64_t o = e / per, rem = e - o * per;
+      const int64_t at = (o * extent + off) * inner + rem;
+      float acc = 0.f;
+      for (int q = 0; q < nranks; ++q) acc += to_f32(sends[(rank + q) % nranks][at]);
+      out[e] = from_f32<T>(acc);
+    }
+  }
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[p])->done[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
+}
+
 }  // namespace
 }  // namespace hap
 
@@ -546,6 +639,27 @@ extern "C" hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void*
              static_cast<const float*>(send), reinterpret_cast<float* const*>(dev_outs), outer, inner, extent,
              dev_sizes, dev_offsets);
   return launch_status("p2p push all-gather");
+}
+
+extern "C" hap_status hap_p2p_reduce_scatter_direct(void* ctx, const void* const* dev_sends, void* recv,
+                                                    hap_dtype dtype, int64_t outer, int64_t inner, int64_t extent,
+                                                    const int64_t* dev_sizes, const int64_t* dev_offsets,
+                                                    int64_t recv_elems, int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_sends && recv && dev_sizes && dev_offsets, "hap_p2p_reduce_scatter_direct: bad arguments");
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  const int grid = p2p_grid(recv_elems * s->nranks * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    launch_k(p2p_reduce_scatter_direct_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank,
+             s->nranks, reinterpret_cast<const __nv_bfloat16* const*>(dev_sends), static_cast<__nv_bfloat16*>(recv),
+             outer, inner, extent, dev_sizes, dev_offsets);
+  else
+    launch_k(p2p_reduce_scatter_direct_kernel<float>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank, s->nranks,
+             reinterpret_cast<const float* const*>(dev_sends), static_cast<float*>(recv), outer, inner, extent,
+             dev_sizes, dev_offsets);
+  return launch_status("p2p direct reduce-scatter");
 }
 
 extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap_dtype dtype,

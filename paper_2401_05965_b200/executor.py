@@ -138,9 +138,10 @@ class ExecConfig:
     gather: str = "auto"              # all_gather / reduce_scatter impl: "auto" = "kernel" (NVLink
                                       # peer-memory kernel) | "padded" (NCCL, max-shard padding) |
                                       # "sendrecv" (NCCL grouped point-to-point)
-    p2p_push: bool = os.environ.get("HAP_P2P_PUSH", "1") == "1"   # "kernel" all-gathers into a dense
-                                      # output store straight into every rank's registered output (NVLink
-                                      # writes, no staging); else peers' shards are pulled from staging
+    p2p_push: bool = os.environ.get("HAP_P2P_PUSH", "1") == "1"   # "kernel" collectives on registered
+                                      # buffers: all-gathers store straight into every rank's output (NVLink
+                                      # writes), reduce-scatters read the peers' partials in place; no staging
+                                      # (else: staged pull kernels)
     input_grads: bool = False         # also differentiate w.r.t. placeholders
     cluster: object = None            # ClusterSpec for the cost-model choices
     ratios: tuple | None = None       # ratio row the plan was made with (cost model)
@@ -243,7 +244,8 @@ class Executor:
         self._allocate()
         self._symm: dict = {}            # stream tag -> peer-memory context
         self._p2p_bytes: dict = {}       # stream tag -> largest staging need
-        self._p2p_regs: list = []        # (stream tag, output Buf, slot) of push all-gathers
+        self._p2p_regs: list = []        # (stream tag, registered Buf, slot): push all-gather outputs,
+                                         # direct reduce-scatter partials
         self._emit_on = None             # stream the next ops are emitted on (None: self.stream)
         self._sfb_full: dict = {}        # gathered SFB factors, keyed by source buffer
         self._sfb_pending: list = []     # deferred SFB weight-gradient GEMMs
@@ -604,8 +606,11 @@ class Executor:
         if self.cfg.gather in ("auto", "kernel"):
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(dst[r].shape, s.dtype)
-            self._p2p("hap_p2p_reduce_scatter_v", s, target, outer, inner, ext, sizes,
-                      outer * ext * inner * (2 if s.dtype == BF16 else 4))
+            if self.cfg.p2p_push:   # read the peers' partials in place (registered)
+                self._p2p("hap_p2p_reduce_scatter_direct", s, target, outer, inner, ext, sizes, 16)
+            else:
+                self._p2p("hap_p2p_reduce_scatter_v", s, target, outer, inner, ext, sizes,
+                          outer * ext * inner * (2 if s.dtype == BF16 else 4))
             if not exact:
                 self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
             return
@@ -694,6 +699,12 @@ class Executor:
             total = outer * extent * inner
             args = lambda: (self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype, outer, inner,  # noqa: E731
                             extent, sizes_ptr, offs_ptr, total, cap, stream)
+        elif fn == "hap_p2p_reduce_scatter_direct":
+            reg = {}
+            self._p2p_regs.append((tag, send, reg))
+            mine = outer * sizes[r] * inner
+            args = lambda: (self._symm[tag], reg["dev"].data_ptr(), recv.ptr, send.dtype, outer, inner,  # noqa: E731
+                            extent, sizes_ptr, offs_ptr, mine, cap, stream)
         elif fn == "hap_p2p_all_gather_v":
             max_chunk = max(sizes) * outer * inner
             args = lambda: (self._symm[tag], send.ptr, recv.ptr, send.dtype, outer, inner, extent,  # noqa: E731
@@ -722,8 +733,9 @@ class Executor:
         self._register_outputs()
 
     def _register_outputs(self):
-        """Map every push all-gather's output into every peer: one exchange of
-        (IPC handle, allocation base, offset) triples for all of them."""
+        """Map every registered buffer (push all-gather outputs, direct
+        reduce-scatter partials) into every peer: one exchange of (IPC
+        handle, allocation base, offset) triples for all of them."""
         if not self._p2p_regs:
             return
         import torch.distributed as dist

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rows", default="4096,16384,65536,262144", help="comma-separated gathered row counts")
+    ap.add_argument("--rs-rows", default="16384,65536,262144", help="comma-separated reduce-scatter row counts")
     ap.add_argument("--probe", default="", help="comma-separated MB per peer for the push/pull bandwidth probe")
     ap.add_argument("--ar-elems", default="", help="comma-separated fp32 all-reduce sizes (elements)")
     args = ap.parse_args()
@@ -130,6 +131,79 @@ def main():
             results.append({"op": "all_gather", "impl": name, "rows": rows, "shard_rows": sizes,
                             "ms": ms, "recv_GBps_max_rank": float(rb.item()) / (ms * 1e-3) / 1e9,
                             "nvlink_bound_bytes": bound,
+                            "frac_of_770": bound / (ms * 1e-3) / 770e9})
+    # uneven reduce-scatter: staged pull kernel, direct kernel on registered partials, NCCL
+    for rows in [int(v) for v in args.rs_rows.split(",") if v]:
+        sizes = round_shards(rows, ratios)
+        counts = [sz * inner for sz in sizes]
+        send = torch.randn(rows * inner, device=dev).to(torch.bfloat16)
+        out = torch.empty(counts[rank], device=dev, dtype=torch.bfloat16)
+        scratch = torch.empty(world * max(counts), device=dev, dtype=torch.bfloat16)
+        devsz = torch.tensor([sizes, offsets(sizes)[:-1]], dtype=torch.int64, device=dev)
+        carr = i64_array(counts)
+        hb = ctypes.create_string_buffer(64)
+        base, boff = ctypes.c_int64(), ctypes.c_int64()
+        check(L.hap_p2p_buffer_handle(ctx, send.data_ptr(), hb, ctypes.byref(base), ctypes.byref(boff)))
+        trip = [None] * world
+        dist.all_gather_object(trip, (bytes(hb.raw), base.value, boff.value))
+        ptrs = (ctypes.c_void_p * world)()
+        check(L.hap_p2p_buffer_open(ctx, send.data_ptr(), b"".join(t[0] for t in trip),
+                                    i64_array([t[1] for t in trip]), i64_array([t[2] for t in trip]), ptrs))
+        dev_sends = torch.tensor([int(p or 0) for p in ptrs], dtype=torch.int64, device=dev)
+        impls = {
+            "p2p_rs_staged": lambda: L.hap_p2p_reduce_scatter_v(ctx, send.data_ptr(), out.data_ptr(), BF16, 1, inner,
+                                                                rows, devsz[0].data_ptr(), devsz[1].data_ptr(), 0,
+                                                                stream.cuda_stream),
+            "p2p_rs_direct": lambda: L.hap_p2p_reduce_scatter_direct(ctx, dev_sends.data_ptr(), out.data_ptr(), BF16,
+                                                                     1, inner, rows, devsz[0].data_ptr(),
+                                                                     devsz[1].data_ptr(), counts[rank], 0,
+                                                                     stream.cuda_stream),
+            "nccl_rs": lambda: L.hap_reduce_scatter_v(group.comm, send.data_ptr(), out.data_ptr(), carr, BF16,
+                                                      scratch.data_ptr(), stream.cuda_stream),
+        }
+        ref = None
+        for name, fn in impls.items():
+            out.zero_()
+            for _ in range(3):
+                check(fn(), name)
+            torch.cuda.synchronize(dev)
+            if ref is None:
+                ref = out.clone()
+            elif name.startswith("p2p"):
+                assert torch.equal(out, ref), name   # same fp32 sum order, one rounding
+            diff = float((out.float() - ref.float()).abs().max())   # NCCL: bf16 partial sums
+            dist.barrier()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+                for _ in range(10):
+                    fn()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            with torch.cuda.stream(stream):
+                graph.replay()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, args.reps // 10)
+            e0.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(reps):
+                    graph.replay()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            del graph
+            t = torch.tensor([e0.elapsed_time(e1) / (reps * 10)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            b = 2 * inner
+            # rank j reads its rows from m-1 peers (ingress (m-1) size_j); its
+            # partial's other rows leave it (egress rows - size_j)
+            ingress = (world - 1) * max(sizes) * b
+            egress = (rows - min(sizes)) * b
+            bound = max(ingress, egress)
+            results.append({"op": "reduce_scatter", "impl": name, "rows": rows, "shard_rows": sizes, "ms": ms,
+                            "max_abs_diff_vs_p2p": diff,
+                            "recv_GBps_max_rank": ingress / (ms * 1e-3) / 1e9, "nvlink_bound_bytes": bound,
                             "frac_of_770": bound / (ms * 1e-3) / 770e9})
     # raw NVLink bandwidth: pull vs push, peers in turn vs all at once
     for mb in [int(v) for v in args.probe.split(",") if v]:
