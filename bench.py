@@ -440,9 +440,23 @@ def main() -> None:
     # the timed loop at power-capped clocks (sampled below), i.e. inside a long
     # step: the sustained cuBLAS figure is the denominator (profiling recipe);
     # the fraction of the burst figure is reported beside it.
-    roofline = {"bound": "tensor", "kernel": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05, all GEMMs of one step)",
-                "achieved": round(achieved, 1), "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                "frac": round(achieved / peaks["bf16_tflops_sustained"], 4),
+    # Binding resource at the algorithmic figures: the step's GEMMs are
+    # tensor-bound when Σ flops / tensor peak exceeds Σ operand+output bytes /
+    # HBM peak (BERT, 8192-token rows), HBM-bound otherwise (the MoE stack's
+    # 256-token rows: the weights dominate, ~145 flop/B < the ~250 ridge).
+    t_tensor = gemm_flops / (peaks["bf16_tflops_sustained"] * 1e12)
+    t_hbm = gemm_bytes / (peaks["hbm_gbs"] * 1e9)
+    tensor_frac = achieved / peaks["bf16_tflops_sustained"]
+    if t_hbm > t_tensor:
+        gbs = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+        head = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / peaks["hbm_gbs"], 4), "tensor_tflops": round(achieved, 1),
+                "tensor_frac": round(tensor_frac, 4)}
+    else:
+        head = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": round(tensor_frac, 4)}
+    roofline = {**head, "kernel": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05, all GEMMs of one step)",
+                "roofline_ms_per_step": round(max(t_tensor, t_hbm) * 1e3, 4),
                 "peak_burst": peaks["bf16_tflops"], "frac_burst": round(achieved / peaks["bf16_tflops"], 4),
                 "gemm_clocks": gclk.summary(), "traffic": traffic,
                 "traffic_note": "DRAM bytes per step over all GEMM launches (ncu, profiles/r01_gemm_traffic.json)",

@@ -1356,10 +1356,18 @@ void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, i
 // C (+)= sum over s of ws[s] — the K splits' partial tiles added in split
 // order (fixed, so repeated launches give identical bits).  A thread owns 4
 // consecutive columns of a row; every split's load is issued before the sum.
+//
+// Split K under a residual epilogue (bf16 outputs): the reduction applies it
+// with the fused path's roundings — HAP_EPI_ADD: C = bf16(sum + R);
+// HAP_EPI_ADD2: C = bf16(sum), Y = bf16(bf16(sum) + R).  (ADD onto C itself
+// is the plain accumulate.)
 template <typename OutT>
 __global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ ws, int splits,
                                                            int64_t slice, int64_t ld, OutT* __restrict__ C,
-                                                           int64_t ldc, int M, int N, int accumulate, int vec) {
+                                                           int64_t ldc, int M, int N, int accumulate, int vec,
+                                                           int epi, const __nv_bfloat16* __restrict__ R,
+                                                           int64_t ldr, __nv_bfloat16* __restrict__ Y,
+                                                           int64_t ldy) {
   hap::pdl_enter();
   const int64_t nq = (static_cast<int64_t>(N) + 3) / 4;
   const int64_t total = static_cast<int64_t>(M) * nq;
@@ -1392,24 +1400,46 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restri
         }
         *reinterpret_cast<float4*>(dst) = o;
       } else {
-        float f[4] = {a[0], a[1], a[2], a[3]};
-        if (accumulate) {
-          const uint2 c = *reinterpret_cast<const uint2*>(dst);
+        auto ld4 = [](const void* p, float (&f)[4]) {
+          const uint2 c = *reinterpret_cast<const uint2*>(p);
           const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
           const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
-          f[0] += lo.x; f[1] += lo.y; f[2] += hi.x; f[3] += hi.y;
+          f[0] = lo.x; f[1] = lo.y; f[2] = hi.x; f[3] = hi.y;
+        };
+        auto st4 = [](void* p, const float (&f)[4]) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
+          uint2 o;
+          o.x = *reinterpret_cast<uint32_t*>(&lo);
+          o.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(p) = o;
+        };
+        float f[4] = {a[0], a[1], a[2], a[3]}, x[4];
+        if (accumulate) {
+          ld4(dst, x);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] += x[e];
         }
-        __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
-        uint2 o;
-        o.x = *reinterpret_cast<uint32_t*>(&lo);
-        o.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(dst) = o;
+        if (epi != EPI_OP_NONE) ld4(R + row * ldr + col, x);
+        if (epi == EPI_OP_ADD) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] += x[e];
+        }
+        st4(dst, f);
+        if (epi == EPI_OP_ADD2) {
+          float y[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) y[e] = bf16_round(f[e]) + x[e];
+          st4(Y + row * ldy + col, y);
+        }
       }
     } else {
       for (int e = 0; e < 4 && col + e < N; ++e) {
         float v = a[e];
         if (accumulate) v += to_f32(dst[e]);
+        const float r = epi != EPI_OP_NONE ? to_f32(R[row * ldr + col + e]) : 0.f;
+        if (epi == EPI_OP_ADD) v += r;
         dst[e] = from_f32<OutT>(v);
+        if (epi == EPI_OP_ADD2) Y[row * ldy + col + e] = from_f32<__nv_bfloat16>(bf16_round(v) + r);
       }
     }
   }
@@ -1652,6 +1682,15 @@ std::string tune_key(const hap_gemm_desc* d, int count, int sum_k, bool fp32, in
   return k;
 }
 
+// Split K is allowed when every output's epilogue is plain or a residual add
+// (the split reduction applies ADD / ADD2); the swish chains need the whole
+// accumulator tile in the GEMM's epilogue.
+bool split_fusable(const hap_gemm_desc* d, int nout) {
+  for (int q = 0; q < nout; ++q)
+    if (d[q].epi != HAP_EPI_NONE && d[q].epi != HAP_EPI_ADD && d[q].epi != HAP_EPI_ADD2) return false;
+  return true;
+}
+
 // Build and launch one tcgen05 batch (all problems tc-eligible, same
 // orientation, <= kMaxProblems).  sum_k: every problem adds into problem 0's
 // output (same C, M, N), accumulate taken from problem 0.
@@ -1669,9 +1708,11 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   bool fused = false;
   for (int q = 0; q < nout; ++q) fused = fused || d[q].epi != HAP_EPI_NONE;
   HAP_CHECK_ARG(!fused || !fp32, "hap_matmul: fused epilogues need a bf16 output");
-  // a fused epilogue runs once per output tile: no split K
-  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && !fused, fp32, cap,
-                                   pair_mode());
+  // a fused epilogue runs once per output tile; under split K the residual
+  // adds (ADD / ADD2) move into the split reduction, the swish chains do not
+  // split
+  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && split_fusable(d, nout), fp32,
+                                   cap, pair_mode());
   if (force) {
     shp = *force;
   } else {
@@ -1712,6 +1753,8 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   for (int q = 0; q < count; ++q) bt.sum_kb += static_cast<int>((d[q].K + tc::BK - 1) / tc::BK);
   int units = 0;
   int64_t ws_used = 0;
+  struct SplitEpi { int epi; const void* R; int64_t ldr; void* Y; int64_t ldy; int vec; };
+  SplitEpi sepi[tc::kMaxProblems] = {};
   for (int q = 0; q < count; ++q) {
     tc::TcProblem& pr = bt.p[q];
     const hap_gemm_desc& g = d[q];
@@ -1753,8 +1796,19 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
       R = out.C;
       ldr = out.ldc;
     }
+    if (epi == HAP_EPI_ADD && out.accumulate && pr.splits > 1) epi = HAP_EPI_NONE;   // += C: the accumulate
     pr.epi = epi;
-    if (epi != HAP_EPI_NONE) {
+    if (epi != HAP_EPI_NONE && pr.splits > 1) {
+      // split K: the reduction applies the residual epilogue (split_fusable)
+      HAP_CHECK_ARG(epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2, "hap_matmul: this fused epilogue cannot split K");
+      HAP_CHECK_ARG(R != nullptr && (epi != HAP_EPI_ADD2 || out.Y != nullptr),
+                    "hap_matmul: fused epilogue tensor R / Y is null");
+      auto al8 = [](const void* ptr, int64_t ld) { return (reinterpret_cast<uintptr_t>(ptr) & 7) == 0 && ld % 4 == 0; };
+      sepi[q] = {epi, R, ldr, out.Y, out.ldy, al8(R, ldr) && (epi != HAP_EPI_ADD2 || al8(out.Y, out.ldy))};
+      pr.epi = HAP_EPI_NONE;
+      pr.accumulate = 0;
+    }
+    if (pr.epi != HAP_EPI_NONE) {
       HAP_CHECK_ARG(pr.splits <= 1 && pr.vec_ok && tma_epilogue(),
                     "hap_matmul: fused epilogue needs a 16-byte pitched output and the TMA epilogue");
       HAP_CHECK_ARG(epi >= HAP_EPI_ADD && epi <= HAP_EPI_SWISH_BWD, "hap_matmul: unknown epilogue op");
@@ -1846,14 +1900,16 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     const int64_t work = static_cast<int64_t>(pr.M) * ((pr.N + 3) / 4);
     const int grid = capped_grid((work + 255) / 256, cap * 4);
     const int64_t slice = static_cast<int64_t>(pr.ws_rows) * pr.ws_ld;
+    const SplitEpi& se = sepi[q];
     if (fp32)
       launch_k(tc::split_reduce_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(pr.ws),
                pr.splits, slice, pr.ws_ld, static_cast<float*>(pr.C), pr.ldc, pr.M, pr.N, pr.accumulate,
-               pr.vec_ok);
+               pr.vec_ok, 0, nullptr, 0, nullptr, 0);
     else
       launch_k(tc::split_reduce_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
                static_cast<const float*>(pr.ws), pr.splits, slice, pr.ws_ld, static_cast<__nv_bfloat16*>(pr.C),
-               pr.ldc, pr.M, pr.N, pr.accumulate, pr.vec_ok);
+               pr.ldc, pr.M, pr.N, pr.accumulate, pr.vec_ok && (se.epi == HAP_EPI_NONE || se.vec), se.epi,
+               static_cast<const __nv_bfloat16*>(se.R), se.ldr, static_cast<__nv_bfloat16*>(se.Y), se.ldy);
     st = launch_status("split_reduce_kernel");
     if (st != HAP_OK) return st;
   }
@@ -1919,7 +1975,8 @@ extern "C" hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int
     Ks[q] = descs[q].K;
   }
   std::vector<tc::Shape> cands;
-  tc::candidate_shapes(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && !fused, cap, pair_mode(), cands);
+  tc::candidate_shapes(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && split_fusable(descs, nout), cap,
+                       pair_mode(), cands);
   if (cands.size() < 2) return HAP_OK;
   // scratch outputs: every written tensor of the batch
   const size_t osz = dtype_size(out_dtype);
@@ -1959,6 +2016,32 @@ extern "C" hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int
     HAP_CUDA_TRY(cudaEventCreate(&e1));
     float best_ms = 1e30f;
     tc::Shape best = cands[0];
+    constexpr int kReps = 5;
+    // Candidates are timed as the executor runs them: kReps launches captured
+    // in one CUDA graph (no host launch cost between them — eager timing
+    // favoured shapes with fewer launches, e.g. no split K, on small GEMMs);
+    // eager on the legacy stream, which cannot capture.
+    auto graph_ms = [&](const tc::Shape& c, float* ms) -> bool {
+      if (stream == nullptr) return false;
+      if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      bool good = true;
+      for (int r = 0; r < kReps && good; ++r) good = tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c) == HAP_OK;
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(stream, &g);
+      cudaGraphExec_t ge = nullptr;
+      good = good && ec == cudaSuccess && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+      good = good && cudaGraphLaunch(ge, stream) == cudaSuccess;   // warm
+      good = good && cudaEventRecord(e0, stream) == cudaSuccess && cudaGraphLaunch(ge, stream) == cudaSuccess &&
+             cudaEventRecord(e1, stream) == cudaSuccess && cudaEventSynchronize(e1) == cudaSuccess &&
+             cudaEventElapsedTime(ms, e0, e1) == cudaSuccess;
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      if (!good) cudaGetLastError();
+      return good;
+    };
     for (const tc::Shape& c : cands) {
       bool good = true;
       for (int w = 0; w < 2 && good; ++w) good = tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c) == HAP_OK;
@@ -1966,17 +2049,18 @@ extern "C" hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int
         cudaGetLastError();
         continue;
       }
-      constexpr int kReps = 5;
-      cudaEventRecord(e0, stream);
-      for (int r = 0; r < kReps; ++r) tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c);
-      cudaEventRecord(e1, stream);
-      if (cudaEventSynchronize(e1) != cudaSuccess) {
-        result = HAP_ERR_CUDA;
-        set_error("hap_matmul_tune: a candidate launch failed");
-        break;
-      }
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
+      if (!graph_ms(c, &ms)) {
+        cudaEventRecord(e0, stream);
+        for (int r = 0; r < kReps; ++r) tc_batch(t, count, sum_k, out_dtype, sm_cap, stream, &c);
+        cudaEventRecord(e1, stream);
+        if (cudaEventSynchronize(e1) != cudaSuccess) {
+          result = HAP_ERR_CUDA;
+          set_error("hap_matmul_tune: a candidate launch failed");
+          break;
+        }
+        cudaEventElapsedTime(&ms, e0, e1);
+      }
       if (ms < best_ms) {
         best_ms = ms;
         best = c;
