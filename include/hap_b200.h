@@ -91,6 +91,9 @@ typedef struct {
    *   HAP_EPI_SWISH     C = A.B;  Y = f(C);  Z = C * Y    (f = epi_tag)
    *   HAP_EPI_SWISH_BWD dz = A.B (not stored);
    *                     C (+)= dz*R2 + (dz*R)*f'(R, R2)   (R = x, R2 = f(x))
+   * ADD / ADD2 may split K (few output tiles, long K): the ordered split
+   * reduction then applies them with the same roundings; the swish chains
+   * never split.
    */
   int epi;
   int epi_tag;
