@@ -431,8 +431,8 @@ def main() -> None:
     gemm_bytes = sum(2 * (m["M"] * m["K"] + m["K"] * m["N"]) + m["M"] * m["N"] * (2 if m["out_dt"] else 4)
                      * (2 if m["accumulate"] else 1) for m in members)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
-    if n == 1 and args.workload == "bert" and os.path.exists(prof):
+    prof = os.path.join(ROOT, "profiles", f"r01h_gemm_traffic_{args.workload}.json")
+    if n == 1 and os.path.exists(prof):
         with open(prof) as fh:
             tr = json.load(fh)
         traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]
@@ -459,7 +459,8 @@ def main() -> None:
                 "roofline_ms_per_step": round(max(t_tensor, t_hbm) * 1e3, 4),
                 "peak_burst": peaks["bf16_tflops"], "frac_burst": round(achieved / peaks["bf16_tflops"], 4),
                 "gemm_clocks": gclk.summary(), "traffic": traffic,
-                "traffic_note": "DRAM bytes per step over all GEMM launches (ncu, profiles/r01_gemm_traffic.json)",
+                "traffic_note": f"DRAM bytes per step over all GEMM launches (ncu, caches flushed per kernel; "
+                                f"profiles/{os.path.basename(prof)})",
                 "algorithmic_bytes_per_step": gemm_bytes, "gemm_flops_per_step": gemm_flops,
                 "peak_source": peaks["source"] + ", sustained (GEMMs run inside a long power-capped step); "
                                "burst in peak_burst",

@@ -212,3 +212,37 @@ def test_fused_epilogues_match_unfused(workload):
     for ref in g0:
         err = float((g1[ref] - g0[ref]).abs().max() / g0[ref].abs().max())
         assert err < 1e-2, (ref, err)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_sgd_overlap_matches_single_update(dtype):
+    """The SGD update moved into the backward on a side stream (one launch
+    per parameter group right after the backward's last touch of the group)
+    computes what the single update at the end computes: two steps, eager and
+    graph-replayed, same masters and losses."""
+    from paper_2401_05965_b200 import api, workloads
+
+    g = workloads.moe_stack(layers=2, batch=2, seq=128)
+    inputs = workloads.synthetic_inputs(g, 5, scaled=True)
+    shapes = {n.id: n.shape for n in g.sources()}
+    out = {}
+    for overlap in ("0", "1"):
+        ex = Executor(api.single_device_program(g), 1, {}, shapes, group=LocalGroup(1),
+                      config=ExecConfig(dtype=dtype, lr=1e-4, sgd_overlap=overlap))
+        assert (ex.sgd_stats[0] > 1) == (overlap == "1"), ex.sgd_stats
+        ex.load(inputs)
+        ex.step()
+        ex.step()
+        eager = (ex.losses(), {k: b.tensor.float().cpu().clone() for k, b in ex.masters.items()})
+        ex.capture()
+        ex.load(inputs)
+        ex.step()
+        ex.step()
+        graph = (ex.losses(), {k: b.tensor.float().cpu().clone() for k, b in ex.masters.items()})
+        out[overlap] = (eager, graph)
+        ex.close()
+    tol = 1e-6 if dtype == "fp32" else 1e-4
+    for (l0, m0), (l1, m1) in zip(out["0"], out["1"]):
+        assert np.allclose(l0, l1, rtol=tol, atol=0), (l0, l1)
+        for k in m0:
+            assert torch.allclose(m0[k], m1[k], rtol=tol, atol=0), k

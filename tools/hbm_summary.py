@@ -1,5 +1,5 @@
 """Summarise an ncu step CSV with DRAM bytes (tools/gpu_hbm_step.sh): the
-last of two eager steps (after compile-time GEMM tuning), per kernel:
+second of two eager steps (profiler range around the steps), per kernel:
 launches, total time, DRAM bytes read + written, achieved GB/s and the
 fraction of the measured HBM peak.
 Usage: python tools/hbm_summary.py CSV [title] > profiles/....md"""
@@ -24,10 +24,9 @@ for r in data:
     v = float(r[vi].replace(",", ""))
     d[r[mi]] = v * scale.get(r[ui], 1)
 ids = sorted(L)
-# the last step: launches after the previous SGD launch up to the last one
-# (the executor's compile-time GEMM tuning and the first step come before)
-sgd = [i for i in ids if "sgd" in L[i]["k"]]
-step = [i for i in ids if (len(sgd) < 2 or i > sgd[-2]) and i <= sgd[-1]] if sgd else ids[len(ids) // 2:]
+# the capture holds exactly two steps (step_once.py brackets them with
+# cudaProfilerStart/Stop, ncu --profile-from-start off): the second half
+step = ids[len(ids) // 2:]
 
 
 def short(k):
@@ -49,7 +48,7 @@ for i in step:
 tot_t = sum(a[1] for a in agg.values())
 print(f"# {title}\n")
 print("ncu `gpu__time_duration.sum, dram__bytes_read.sum, dram__bytes_write.sum` per launch, caches flushed "
-      "before every kernel (ncu default), the last of two eager steps after compile-time GEMM tuning "
+      "before every kernel (ncu default), the second of two eager steps (profiler range around the steps only) "
       "(`tools/step_once.py 2`). ncu serialises "
       f"launches: compare shares and GB/s, not the absolute step time. HBM peak {peak:.0f} GB/s "
       "(MEASURED_PEAKS.json copy bandwidth).\n")

@@ -19,7 +19,12 @@ ex = Executor(api.single_device_program(g), 1, {}, {n.id: n.shape for n in g.sou
 ex.load(workloads.synthetic_inputs(g, 0, scaled=True))
 gemm_launches = sum(len(op.gemm.get("members", [op.gemm])) > 0 for op in ex.ops_fwd + ex.ops_bwd if op.gemm)
 print("gemm launches per step", gemm_launches)
+# ncu --profile-from-start off sees only the steps (not the compile-time
+# GEMM tuning, which launches thousands of candidate kernels)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
 for _ in range(steps):
     ex.step()
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok")
