@@ -1,6 +1,6 @@
 """GEMM DRAM traffic per train step from an ncu step CSV (tools/gpu_hbm_step.sh):
-the last of two eager steps, summed over the tcgen05 GEMM launches (and the
-split-K reductions that complete them).  Writes the JSON bench.py reads for
+the second of two eager steps (profiler range around the steps), summed over
+the tcgen05 GEMM launches (and the split-K reductions that complete them).  Writes the JSON bench.py reads for
 `roofline.traffic`.  Usage: python tools/gemm_traffic.py CSV WORKLOAD OUT.json"""
 import csv
 import json
