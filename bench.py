@@ -338,11 +338,13 @@ def main() -> None:
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        torch.cuda.profiler.start()   # `ncu --profile-from-start off` sees the timed steps only
         start.record(ex.stream)
         for _ in range(args.steps):
             ex.step()
         stop.record(ex.stream)
         barrier()
+        torch.cuda.profiler.stop()
     ms_local = start.elapsed_time(stop)
     ms = torch.tensor([ms_local], device=dev)
     if world > 1:
