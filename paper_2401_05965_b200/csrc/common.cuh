@@ -73,18 +73,16 @@ __device__ __forceinline__ void pdl_enter() { pdl_wait(); }
 
 int carveout_pref();
 
-// Every kernel asks for the maximum shared-memory carveout, so consecutive
-// GEMM (225 KB smem) and elementwise launches do not force the SMs to
-// re-partition L1/shared memory between kernels (HAP_CARVEOUT=-1 leaves the
-// driver default).
+// HAP_CARVEOUT=<percent>: every kernel asks for that shared-memory carveout,
+// so consecutive GEMM (225 KB smem) and elementwise launches need not
+// re-partition L1/shared memory between kernels.  Default: the driver's
+// choice (forcing 100 % measured slower).
 template <typename K>
 inline void set_carveout(K kern) {
-  static bool done = false;
-  if (!done) {
-    const int pref = carveout_pref();
-    if (pref >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pref);
-    done = true;
-  }
+  // per launch (a static flag here would be shared by every kernel of the
+  // same signature); the default -1 sets nothing
+  const int pref = carveout_pref();
+  if (pref >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pref);
 }
 
 template <typename... KArgs, typename... Args>
