@@ -115,6 +115,16 @@ hap_status hap_matmul_batch(const hap_gemm_desc* descs, int count, int sum_k, ha
  * with the same extents, orientation, epilogue, output type and SM cap. */
 hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int sum_k, hap_dtype in_dtype,
                            hap_dtype out_dtype, int sm_cap, void* stream);
+/* The tuning table (process-wide) as text: one signature per line,
+ * "<key>\t<pair> <bn> <splits> <kb_per_split>\n", keys sorted.  Export
+ * returns the bytes needed (NUL included) and writes them when `cap` allows;
+ * import merges lines into the table (later launches of those signatures use
+ * the imported shape; hap_matmul_tune skips signatures already present);
+ * clear empties it.  A committed table makes tile shapes and split-K factors —
+ * and with them every GEMM's rounding — identical across processes. */
+int64_t hap_matmul_tune_export(char* buf, int64_t cap);
+hap_status hap_matmul_tune_import(const char* text);
+void hap_matmul_tune_clear(void);
 /* Which engine hap_matmul would use for these arguments (no launch). */
 int hap_matmul_engine(const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                       int transB, int64_t M, int64_t N, int64_t K, hap_dtype in_dtype);
@@ -214,22 +224,6 @@ hap_status hap_all_gather_v(void* comm, const void* send, void* recv, const int6
  * actual (unpadded) shards; result identical to hap_all_gather_v. */
 hap_status hap_grouped_broadcast(void* comm, const void* send, void* recv, const int64_t* counts,
                                  hap_dtype dtype, void* stream);
-/* Registered outputs for the push all-gather: export the CUDA IPC handle of
- * the allocation holding `buf` (plus that allocation's base address in this
- * process and buf's offset in it), exchange all ranks' triples on the host,
- * then open them: out_ptrs[p] = rank p's buffer as mapped in this process
- * (out_ptrs[rank] = own).  Mappings are cached per context (closed by
- * hap_symm_destroy). */
-hap_status hap_p2p_buffer_handle(void* ctx, const void* buf, uint8_t* out64, int64_t* base_addr, int64_t* offset);
-hap_status hap_p2p_buffer_open(void* ctx, const void* own, const uint8_t* handles64xn, const int64_t* base_addrs,
-                               const int64_t* offsets, void** out_ptrs);
-/* all_gather (same semantics as hap_p2p_all_gather_v) by pushing: every rank
- * stores its shard straight into every rank's registered output.
- * `dev_outs` is a DEVICE array of the nranks output pointers from
- * hap_p2p_buffer_open; `total_elems` = outer * extent * inner. */
-hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void* const* dev_outs, hap_dtype dtype,
-                                   int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
-                                   const int64_t* dev_offsets, int64_t total_elems, int sm_cap, void* stream);
 /* reduce_scatter — interpreter.py:94-96: sum over ranks then keep this
  * rank's counts[rank]-element chunk of the rank-ordered layout of `send`.
  * `scratch` must hold nranks*max(counts) elements (padded layout). */

@@ -45,6 +45,9 @@ SIGNATURES = {
                            c_int64, c_int, c_int, c_int, c_int, _P]),
     "hap_matmul_batch": (c_int, [POINTER(GemmDesc), c_int, c_int, c_int, c_int, c_int, _P]),
     "hap_matmul_tune": (c_int, [POINTER(GemmDesc), c_int, c_int, c_int, c_int, c_int, _P]),
+    "hap_matmul_tune_export": (c_int64, [ctypes.c_char_p, c_int64]),
+    "hap_matmul_tune_import": (c_int, [ctypes.c_char_p]),
+    "hap_matmul_tune_clear": (None, []),
     "hap_matmul_engine": (c_int, [_P, c_int64, c_int, _P, c_int64, c_int, c_int64, c_int64, c_int64,
                                   c_int]),
     "hap_unary": (c_int, [c_int, _P, c_int, _P, c_int, c_int64, c_int, _P]),
@@ -128,6 +131,32 @@ def lib():
         fn.argtypes = args
     _LIB = handle
     return handle
+
+
+TUNE_TABLE = os.environ.get("HAP_TUNE_TABLE", os.path.join(PKG, "tune_b200.txt"))
+_TUNE_LOADED = False
+
+
+def load_tune_table(path: str = TUNE_TABLE) -> int:
+    """Import the committed GEMM tuning table (tile shape and split-K factor
+    per launch signature, measured on a B200 by tools/tune_table.py) once per
+    process.  With it every process picks the same shapes — and so rounds
+    every GEMM the same way.  Returns the number of signatures imported."""
+    global _TUNE_LOADED
+    if _TUNE_LOADED or not os.path.exists(path):
+        return 0
+    with open(path, "rb") as fh:
+        text = fh.read()
+    check(lib().hap_matmul_tune_import(text), "hap_matmul_tune_import")
+    _TUNE_LOADED = True
+    return text.count(b"\n")
+
+
+def export_tune_table() -> str:
+    n = lib().hap_matmul_tune_export(None, 0)
+    buf = ctypes.create_string_buffer(int(n))
+    lib().hap_matmul_tune_export(buf, n)
+    return buf.value.decode()
 
 
 def check(status: int, what: str = "") -> None:

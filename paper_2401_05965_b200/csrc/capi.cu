@@ -1,6 +1,10 @@
 // Library-level entry points: error reporting, version, device queries.
+#include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -40,6 +44,46 @@ int sm_count() {
     cached[dev] = n;
   }
   return cached[dev];
+}
+
+bool stream_scratch(cudaStream_t stream, int slot, size_t bytes, bool zeroed, void** out) {
+  struct Entry {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  static std::mutex mu;
+  static std::map<std::pair<cudaStream_t, int>, Entry> table;
+  static std::vector<void*> retired;   // outgrown buffers a captured graph may reference
+  if (slot < 0 || slot >= kScratchSlots) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  Entry& e = table[{stream, slot * 64 + dev}];
+  if (e.bytes >= bytes && e.ptr) {
+    *out = e.ptr;
+    return true;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  const size_t n = std::max<size_t>(std::max<size_t>(bytes, 2 * e.bytes), 1 << 16);
+  void* p = nullptr;
+  if (cudaMalloc(&p, n) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (zeroed && cudaMemsetAsync(p, 0, n, stream) != cudaSuccess) {   // ordered before the slot's first user
+    cudaGetLastError();
+    cudaFree(p);
+    return false;
+  }
+  if (e.ptr) retired.push_back(e.ptr);
+  e.ptr = p;
+  e.bytes = n;
+  *out = p;
+  return true;
 }
 
 }  // namespace hap

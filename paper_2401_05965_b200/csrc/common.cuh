@@ -45,6 +45,17 @@ inline hap_status launch_status(const char* what) {
 // SM count of the current device (cached per device).
 int sm_count();
 
+// Per-stream device scratch for kernels that need a workspace (ordered
+// reduction partials, split-K partial tiles, arrival counters).  Launches on
+// one stream are ordered, so they share a slot.  A slot grows only outside
+// stream capture (returns false during capture when too small); a buffer it
+// outgrows is retired, never freed, because a CUDA graph captured earlier may
+// still hold its address.  `zeroed` slots are cleared on allocation: kernels
+// that use them as counters leave them at zero when they finish.
+enum ScratchSlot { kScratchSplitWs = 0, kScratchSplitFlags, kScratchReduce, kScratchReduceTickets,
+                   kScratchStreamK, kScratchStreamKFlags, kScratchSlots };
+bool stream_scratch(cudaStream_t stream, int slot, size_t bytes, bool zeroed, void** out);
+
 // Grid size for a capped, persistent launch: at most `sm_cap` CTAs (one per
 // SM when each CTA is sized to fill an SM), never more than `work_blocks`.
 inline int capped_grid(int64_t work_blocks, int sm_cap) {

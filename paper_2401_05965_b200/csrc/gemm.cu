@@ -197,21 +197,6 @@ __device__ __forceinline__ void store_row_chunk(OutT* dst, const uint32_t (&r)[3
   }
 }
 
-// Split-K partial: C += r (fp32, vector reduction in L2).
-__device__ __forceinline__ void red_row_chunk(float* dst, const uint32_t (&r)[32], int valid, bool vec) {
-  if (vec && valid == 32) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * i),
-                   "f"(__uint_as_float(r[4 * i])), "f"(__uint_as_float(r[4 * i + 1])),
-                   "f"(__uint_as_float(r[4 * i + 2])), "f"(__uint_as_float(r[4 * i + 3]))
-                   : "memory");
-  } else {
-    for (int i = 0; i < valid; ++i) atomicAdd(dst + i, __uint_as_float(r[i]));
-  }
-}
-
-
 // stream-K helpers: a cut tile's fp32 partial, column-major [BN][128] per CTA
 // (the TMEM lane = row is the fast index), so a warp's 32 lanes move one
 // column as one coalesced 128-byte access.
@@ -267,11 +252,11 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 }
 
 // Epilogue modes: direct per-thread stores (any layout), TMA bulk store, TMA
-// bulk reduce-add (fp32 accumulate and fp32 split-K partials), and split-K
-// into bf16: each K split stores its fp32 partial tile into its own slice of
-// a workspace; split_reduce_kernel then sums the slices in split order and
-// rounds once into C (deterministic, and no bf16 double rounding).
-enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_WS = 3 };
+// bulk reduce-add (fp32 accumulate), and split K (EPI_SPLIT_FIN): every K
+// split writes its fp32 partial tile to the workspace, and the splits of a
+// tile then finish it together in split order (split_finish) — deterministic,
+// no floating-point atomics, no second launch.
+enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_FIN = 3 };
 // fused elementwise ops of the epilogue (hap_gemm_desc.epi)
 enum { EPI_OP_NONE = HAP_EPI_NONE, EPI_OP_ADD = HAP_EPI_ADD, EPI_OP_ADD2 = HAP_EPI_ADD2,
        EPI_OP_SWISH = HAP_EPI_SWISH, EPI_OP_SWISH_BWD = HAP_EPI_SWISH_BWD };
@@ -292,7 +277,7 @@ __device__ __forceinline__ uint32_t swz_offset(int r, int c) {
 template <int BN, typename OutT>
 __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter, int half, int lane, int row0,
                                                   int col0, int M, int N, OutT* C, int64_t ldc, int mode,
-                                                  int vec_ok, int accumulate, int splits,
+                                                  int vec_ok, int accumulate,
                                                   const CUtensorMap* tmC, uint8_t* buf, uint32_t& box_seq,
                                                   const float* prow = nullptr) {
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -306,15 +291,7 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
       tmem_ld32(lane_base + half * (BN / 2) + c * 32, r);
       const int col = first + c * 32;
       const int valid = N - col < 32 ? N - col : 32;
-      if (row < M && valid > 0) {
-        if constexpr (std::is_same<OutT, float>::value) {
-          if (splits > 1) {
-            red_row_chunk(crow + col, r, valid, vec_ok);
-            continue;
-          }
-        }
-        store_row_chunk<OutT>(crow + col, r, valid, vec_ok, accumulate);
-      }
+      if (row < M && valid > 0) store_row_chunk<OutT>(crow + col, r, valid, vec_ok, accumulate);
     }
     return;
   }
@@ -386,12 +363,19 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 constexpr int kMaxProblems = 4;
 
 struct alignas(64) TcProblem {
-  CUtensorMap a, b, c;     // c: output map, or the fp32 workspace map (EPI_SPLIT_WS)
+  CUtensorMap a, b, c;     // c: output map (TMA epilogues)
   void* C;
   int64_t ldc;
-  float* ws;               // EPI_SPLIT_WS: fp32 partials [splits][ws_rows][ws_ld]
-  int64_t ws_ld;
-  int ws_rows;             // rows per split slice (M rounded up to whole tiles)
+  // EPI_SPLIT_FIN: fp32 partials, per (tile, CTA of the pair, epilogue warp)
+  // a block of `splits` column-major [BN/2][32] regions; two counters
+  // (arrived, finished) per (tile, CTA, warp); the residual epilogue the
+  // finish applies (NONE / ADD / ADD2) with its tensors.
+  float* ws;
+  unsigned* split_cnt;
+  const void* fin_R;
+  void* fin_Y;
+  int64_t fin_ldr, fin_ldy;
+  int fin_epi, fin_vec;
   int M, N, K;
   int m_tiles, n_tiles, k_blocks;
   int splits, kb_per_split;
@@ -620,11 +604,10 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
   __syncwarp();
 }
 
-// Epilogue of one unit for one warp: drain the accumulator into C, or (split
-// K) into split `split`'s slice of the workspace.
+// Epilogue of one unit for one warp: drain the accumulator into C.
 template <int BN, typename OutT>
 __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
-                                              int lane, int row0, int col0, int split, uint8_t* buf,
+                                              int lane, int row0, int col0, uint8_t* buf,
                                               uint32_t& box_seq, uint32_t ld_bar, uint32_t& ld_phase,
                                               const float* part) {
   // part: stream-K partial of this CTA's 128 x BN share (column-major), added to
@@ -636,20 +619,125 @@ __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem
       return;
     }
   }
-  if (pr.epi_mode == EPI_SPLIT_WS) {
-    drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0, pr.M, pr.N, pr.ws,
-                                 pr.ws_ld, EPI_TMA_STORE, 1, 0, 1, &pr.c, buf, box_seq);
-    return;
-  }
   drain_accumulator<BN, OutT>(tmem_acc, quarter, half, lane, row0, col0, pr.M, pr.N, static_cast<OutT*>(pr.C),
-                              pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, pr.splits, &pr.c, buf, box_seq, prow);
+                              pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, &pr.c, buf, box_seq, prow);
 }
 
 struct Unit {
-  int prob, split, m0, n0, kb0, kb1;
+  int prob, split, tile, m0, n0, kb0, kb1;
   int sk_kind;   // 0: whole tile; 1: a tile's last K blocks (write partial); 2: its first (finish it)
   int sk_slot;   // workspace slot of a cut tile
 };
+
+// ---- split K, finished in the kernel (EPI_SPLIT_FIN)
+// A warp's region of a tile is 32 rows x BN/2 columns.  Split s of the tile
+// (1) writes its fp32 accumulator for the region to its column-major
+// [BN/2][32] slot of the workspace (lane = row: one coalesced 128-byte store
+// per column), then the caller releases the TMEM buffer; (2) arrives on the
+// region's counter and waits until all S splits have arrived — every unit of
+// a split launch runs in the first and only round of the persistent grid, so
+// the S CTAs are co-resident; (3) finishes its share of the region, column
+// groups [s*G/S, (s+1)*G/S) of G = BN/8 groups of 4 columns: the S partials
+// added in split order (0, 1, ..., S-1), then + C when accumulating, then the
+// residual epilogue with the roundings of the unfused kernels (ADD: C =
+// bf16(sum + R); ADD2: C = bf16(sum), Y = bf16(bf16(sum) + R)); (4) counts
+// itself done, and the last split resets both counters for the next launch.
+// The sum is the same on every run whatever the CTAs' timing.
+__device__ __forceinline__ unsigned* split_counters(const TcProblem& pr, const Unit& x, int rank, int warp_e) {
+  return pr.split_cnt + ((static_cast<size_t>(x.tile) * 2 + rank) * kEpiWarps + warp_e) * 2;
+}
+template <int BN>
+__device__ __forceinline__ float* split_region(const TcProblem& pr, const Unit& x, int rank, int warp_e) {
+  return pr.ws + ((static_cast<size_t>(x.tile) * 2 + rank) * kEpiWarps + warp_e) * pr.splits * (32 * (BN / 2));
+}
+
+template <int BN>
+__device__ __forceinline__ void split_write(const TcProblem& pr, const Unit& x, uint32_t tmem_acc, int quarter,
+                                            int half, int lane, int rank, int warp_e) {
+  float* part = split_region<BN>(pr, x, rank, warp_e) + static_cast<size_t>(x.split) * (32 * (BN / 2));
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t r[32];
+    tmem_ld32(lane_base + c * 32, r);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) __stcg(part + (c * 32 + i) * 32 + lane, __uint_as_float(r[i]));
+  }
+}
+
+template <int BN, typename OutT>
+__device__ __forceinline__ void split_finish(const TcProblem& pr, const Unit& x, int half, int lane, int rank,
+                                             int warp_e, int row0) {
+  const int S = pr.splits;
+  unsigned* cnt = split_counters(pr, x, rank, warp_e);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) {
+    atomicAdd(cnt, 1u);
+    while (ld_acquire_gpu(cnt) < static_cast<unsigned>(S)) __nanosleep(64);
+  }
+  __syncwarp();
+  const float* region = split_region<BN>(pr, x, rank, warp_e);
+  constexpr int G = BN / 8;   // 4-column groups of the warp's BN/2 columns
+  const int g0 = x.split * G / S, g1 = (x.split + 1) * G / S;
+  const int row = row0 + lane;
+  const bool row_ok = row < pr.M;
+  OutT* C = static_cast<OutT*>(pr.C);
+#pragma unroll 1
+  for (int g = g0; g < g1; ++g) {
+    const int cl = g * 4;                         // column within the warp's half
+    const int col = x.n0 + half * (BN / 2) + cl;  // output column
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = __ldcg(region + (cl + j) * 32 + lane);
+    for (int sp = 1; sp < S; ++sp) {
+      const float* part = region + static_cast<size_t>(sp) * (32 * (BN / 2));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] += __ldcg(part + (cl + j) * 32 + lane);
+    }
+    if (!row_ok || col >= pr.N) continue;
+    OutT* dst = C + static_cast<int64_t>(row) * pr.ldc + col;
+    const int valid = pr.N - col < 4 ? pr.N - col : 4;
+    if constexpr (std::is_same<OutT, float>::value) {
+      if (pr.accumulate)
+        for (int j = 0; j < valid; ++j) v[j] += dst[j];
+      if (valid == 4 && pr.fin_vec) *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      else for (int j = 0; j < valid; ++j) dst[j] = v[j];
+    } else {
+      if (pr.accumulate)
+        for (int j = 0; j < valid; ++j) v[j] += __bfloat162float(dst[j]);
+      float rr[4] = {0.f, 0.f, 0.f, 0.f};
+      if (pr.fin_epi != EPI_OP_NONE) {
+        const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(pr.fin_R) + static_cast<int64_t>(row) * pr.fin_ldr + col;
+        for (int j = 0; j < valid; ++j) rr[j] = __bfloat162float(R[j]);
+      }
+      if (pr.fin_epi == EPI_OP_ADD)
+        for (int j = 0; j < 4; ++j) v[j] += rr[j];
+      if (valid == 4 && pr.fin_vec) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&lo);
+        o.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(dst) = o;
+      } else {
+        for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+      if (pr.fin_epi == EPI_OP_ADD2) {
+        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(pr.fin_Y) + static_cast<int64_t>(row) * pr.fin_ldy + col;
+        for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(v[j]) + rr[j]);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(cnt + 1, 1u) == static_cast<unsigned>(S) - 1) {   // every split is past the wait
+      cnt[0] = 0u;
+      cnt[1] = 0u;
+    }
+  }
+}
+
 
 // Work unit u -> (problem, output tile, K-block range).  Grouped: units are
 // laid out problem after problem; within a problem unit = split * tiles + tile.
@@ -665,6 +753,7 @@ __device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
   Unit x;
   x.prob = p;
   x.split = local / tiles;
+  x.tile = t;
   x.m0 = (t % pr.m_tiles) * ROWS;
   x.n0 = (t / pr.m_tiles) * BN;
   x.kb0 = (local / tiles) * pr.kb_per_split;
@@ -705,6 +794,7 @@ struct PairCursor {
     const int kb1 = static_cast<int>(min(static_cast<long long>(kb), kb0 + (end - it)));
     x.prob = 0;
     x.split = 0;
+    x.tile = tile;
     x.m0 = (tile % pr.m_tiles) * 256;
     x.n0 = (tile / pr.m_tiles) * BN;
     x.kb0 = kb0;
@@ -872,10 +962,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const TcProblem& pr = bt.p[x.prob];
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq, ld_bar, ld_phase, nullptr);
-      tc_fence_before();
-      mbar_arrive(tempty0 + 8 * acc);
+      if (pr.epi_mode == EPI_SPLIT_FIN) {
+        // partial out, accumulator released, then the ordered finish
+        split_write<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, 0, warp - 4);
+        tc_fence_before();
+        mbar_arrive(tempty0 + 8 * acc);
+        split_finish<BN, OutT>(pr, x, half, lane, 0, warp - 4, x.m0 + quarter * 32);
+      } else {
+        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, buf,
+                                box_seq, ld_bar, ld_phase, nullptr);
+        tc_fence_before();
+        mbar_arrive(tempty0 + 8 * acc);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -1117,6 +1215,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
+      if (pr.epi_mode == EPI_SPLIT_FIN) {   // split K: partial out, release the accumulator, ordered finish
+        split_write<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, static_cast<int>(rank), warp - 4);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
+        split_finish<BN, OutT>(pr, x, half, lane, static_cast<int>(rank), warp - 4, m0 + quarter * 32);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       // stream-K: this CTA's 128 x BN share of a cut tile's partial
       float* part = nullptr;
       unsigned* flag = nullptr;
@@ -1135,8 +1243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
           __syncwarp();
         }
-        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
-                                buf, box_seq, ld_bar, ld_phase, x.sk_kind == 2 ? part : nullptr);
+        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, buf,
+                                box_seq, ld_bar, ld_phase, x.sk_kind == 2 ? part : nullptr);
         if (x.sk_kind == 2 && lane == 0) *flag = 0u;   // consumed: ready for the next launch
       }
       tc_fence_before();
@@ -1265,6 +1373,7 @@ struct Shape {
 
 Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
                    bool fp32_out, int cap, int allow_pair) {
+  (void)fp32_out;
   // K blocks a unit walks: the concatenated K of a sum, else the largest
   // problem's (grouped problems with less K simply walk fewer blocks)
   int64_t k_blocks = 0;
@@ -1310,12 +1419,10 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
                 static_cast<double>(rounds * kps) * t_kb};
     }
   }
-  // fp32 outputs: split partials reduce-add in L2, nearly free — the higher
-  // score wins.  bf16 outputs: the partial slices and their reduction pass
-  // add a serial tail (~5 us measured on B200), so split only when the
-  // shortened K walk saves more than that.
-  if (fp32_out) return split.score > plain.score ? split.s : plain.s;
-  constexpr double kSplitTailUs = 5.0;
+  // Split K finishes in the kernel: each split writes its fp32 partial tile
+  // and reads back its share of all of them (split_finish) — a short serial
+  // tail, so split only when the shortened K walk saves more than that.
+  constexpr double kSplitTailUs = 2.0;
   if (split.score > 0 && split.est_us + kSplitTailUs < plain.est_us) return split.s;
   return plain.score > 0 ? plain.s : split.s;
 }
@@ -1349,98 +1456,6 @@ void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, i
       bool dup = false;
       for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits);
       if (!dup) out.push_back(sh);
-    }
-  }
-}
-
-// C (+)= sum over s of ws[s] — the K splits' partial tiles added in split
-// order (fixed, so repeated launches give identical bits).  A thread owns 4
-// consecutive columns of a row; every split's load is issued before the sum.
-//
-// Split K under a residual epilogue (bf16 outputs): the reduction applies it
-// with the fused path's roundings — HAP_EPI_ADD: C = bf16(sum + R);
-// HAP_EPI_ADD2: C = bf16(sum), Y = bf16(bf16(sum) + R).  (ADD onto C itself
-// is the plain accumulate.)
-template <typename OutT>
-__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ ws, int splits,
-                                                           int64_t slice, int64_t ld, OutT* __restrict__ C,
-                                                           int64_t ldc, int M, int N, int accumulate, int vec,
-                                                           int epi, const __nv_bfloat16* __restrict__ R,
-                                                           int64_t ldr, __nv_bfloat16* __restrict__ Y,
-                                                           int64_t ldy) {
-  hap::pdl_enter();
-  const int64_t nq = (static_cast<int64_t>(N) + 3) / 4;
-  const int64_t total = static_cast<int64_t>(M) * nq;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = i / nq;
-    const int col = static_cast<int>(i - row * nq) * 4;
-    const float* src = ws + row * ld + col;
-    float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
-    constexpr int U = 8;
-    for (int s0 = 1; s0 < splits; s0 += U) {
-      float4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (s0 + u < splits) v[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + u) * slice));
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (s0 + u < splits) {
-          acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
-        }
-    }
-    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
-    OutT* dst = C + row * ldc + col;
-    if (vec && col + 4 <= N) {
-      if constexpr (std::is_same<OutT, float>::value) {
-        float4 o = make_float4(a[0], a[1], a[2], a[3]);
-        if (accumulate) {
-          const float4 c = *reinterpret_cast<const float4*>(dst);
-          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
-        }
-        *reinterpret_cast<float4*>(dst) = o;
-      } else {
-        auto ld4 = [](const void* p, float (&f)[4]) {
-          const uint2 c = *reinterpret_cast<const uint2*>(p);
-          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
-          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
-          f[0] = lo.x; f[1] = lo.y; f[2] = hi.x; f[3] = hi.y;
-        };
-        auto st4 = [](void* p, const float (&f)[4]) {
-          __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
-          uint2 o;
-          o.x = *reinterpret_cast<uint32_t*>(&lo);
-          o.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(p) = o;
-        };
-        float f[4] = {a[0], a[1], a[2], a[3]}, x[4];
-        if (accumulate) {
-          ld4(dst, x);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) f[e] += x[e];
-        }
-        if (epi != EPI_OP_NONE) ld4(R + row * ldr + col, x);
-        if (epi == EPI_OP_ADD) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) f[e] += x[e];
-        }
-        st4(dst, f);
-        if (epi == EPI_OP_ADD2) {
-          float y[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) y[e] = bf16_round(f[e]) + x[e];
-          st4(Y + row * ldy + col, y);
-        }
-      }
-    } else {
-      for (int e = 0; e < 4 && col + e < N; ++e) {
-        float v = a[e];
-        if (accumulate) v += to_f32(dst[e]);
-        const float r = epi != EPI_OP_NONE ? to_f32(R[row * ldr + col + e]) : 0.f;
-        if (epi == EPI_OP_ADD) v += r;
-        dst[e] = from_f32<OutT>(v);
-        if (epi == EPI_OP_ADD2) Y[row * ldy + col + e] = from_f32<__nv_bfloat16>(bf16_round(v) + r);
-      }
     }
   }
 }
@@ -1593,71 +1608,21 @@ extern "C" int hap_matmul_engine(const void* A, int64_t lda, int transA, const v
 
 namespace {
 
-// Split-K workspace, one per stream (launches on one stream are ordered, so
-// they can share it).  Grown only outside stream capture; a capturing launch
-// that would need more runs without splitting.
-struct SplitWorkspace {
-  float* ws = nullptr;
-  int64_t elems = 0;
-};
-
-bool split_workspace(cudaStream_t stream, int64_t elems, float** out) {
-  static std::mutex mu;
-  static std::unordered_map<cudaStream_t, SplitWorkspace> table;
-  std::lock_guard<std::mutex> lock(mu);
-  SplitWorkspace& w = table[stream];
-  if (w.elems >= elems) {
-    *out = w.ws;
-    return true;
-  }
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-  if (cudaStreamSynchronize(stream) != cudaSuccess) return false;   // the old buffer may be in use
-  cudaFree(w.ws);
-  w = SplitWorkspace{};
-  const int64_t n = std::max<int64_t>(elems, 1 << 22);
-  if (cudaMalloc(reinterpret_cast<void**>(&w.ws), n * sizeof(float)) != cudaSuccess) {
-    cudaGetLastError();
-    w = SplitWorkspace{};
-    return false;
-  }
-  w.elems = n;
-  *out = w.ws;
-  return true;
-}
-
 // Stream-K partial tiles and flags, one set per stream (launches on a stream
 // are ordered; every flag is reset by the pair that consumes it).  Sized for
 // the largest grid (74 SM pairs + 1 slot, 256-wide tiles); allocated outside
 // stream capture only.
 bool sk_workspace(cudaStream_t stream, float** ws, unsigned** flags) {
-  struct SkWs {
-    float* ws = nullptr;
-    unsigned* flags = nullptr;
-  };
-  static std::mutex mu;
-  static std::unordered_map<cudaStream_t, SkWs> table;
-  std::lock_guard<std::mutex> lock(mu);
-  SkWs& w = table[stream];
-  if (!w.ws) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    const size_t slots = 148 / 2 + 1;
-    if (cudaMalloc(reinterpret_cast<void**>(&w.ws), slots * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(reinterpret_cast<void**>(&w.flags), slots * 2 * tc::kEpiWarps * sizeof(unsigned)) != cudaSuccess ||
-        cudaMemset(w.flags, 0, slots * 2 * tc::kEpiWarps * sizeof(unsigned)) != cudaSuccess) {
-      cudaGetLastError();
-      cudaFree(w.ws);
-      w = SkWs{};
-      return false;
-    }
-  }
-  *ws = w.ws;
-  *flags = w.flags;
+  const size_t slots = 148 / 2 + 1;
+  void* w = nullptr;
+  void* f = nullptr;
+  if (!stream_scratch(stream, kScratchStreamK, slots * 2 * 128 * 256 * sizeof(float), false, &w) ||
+      !stream_scratch(stream, kScratchStreamKFlags, slots * 2 * tc::kEpiWarps * sizeof(unsigned), true, &f))
+    return false;
+  *ws = static_cast<float*>(w);
+  *flags = static_cast<unsigned*>(f);
   return true;
 }
-
-inline int64_t ws_pitch(int64_t n) { return (n + 3) / 4 * 4; }   // 16-byte rows for the TMA map
 
 // Autotuned shapes (hap_matmul_tune), keyed by everything that decides the
 // shape: problem extents, orientation, epilogue, output type, SM cap.
@@ -1709,10 +1674,10 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   for (int q = 0; q < nout; ++q) fused = fused || d[q].epi != HAP_EPI_NONE;
   HAP_CHECK_ARG(!fused || !fp32, "hap_matmul: fused epilogues need a bf16 output");
   // a fused epilogue runs once per output tile; under split K the residual
-  // adds (ADD / ADD2) move into the split reduction, the swish chains do not
+  // adds (ADD / ADD2) move into the split finish, the swish chains do not
   // split
-  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, split_enabled() != 0 && split_fusable(d, nout), fp32,
-                                   cap, pair_mode());
+  const bool may_split = split_enabled() != 0 && split_fusable(d, nout);
+  tc::Shape shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, may_split, fp32, cap, pair_mode());
   if (force) {
     shp = *force;
   } else {
@@ -1720,27 +1685,42 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     auto it = tune_cache().find(tune_key(d, count, sum_k, fp32, cap));
     if (it != tune_cache().end()) shp = it->second;
   }
-  // split-K partial slices: splits x (M rounded up to whole tiles) x pitch(N)
-  // fp32 per output; without room for them (capture), no split
-  float* ws = nullptr;
-  auto slice_rows = [&](int q, const tc::Shape& sh) {
-    const int64_t r = sh.pair ? 256 : tc::BM;
-    return (Ms[q] + r - 1) / r * r;
-  };
   auto problem_splits = [&](int q, const tc::Shape& sh) -> int64_t {
     if (sum_k) return sh.splits;
     const int64_t kb = (Ks[q] + tc::BK - 1) / tc::BK;
     const int64_t kps = std::max<int64_t>(1, std::min<int64_t>(sh.kb_per_split, kb));
     return (kb + kps - 1) / kps;
   };
-  if (shp.splits > 1 && !fp32) {
-    int64_t need = 0;
+  auto tiles_of = [&](int q, const tc::Shape& sh) -> int64_t {
+    const int64_t r = sh.pair ? 256 : tc::BM;
+    return ((Ms[q] + r - 1) / r) * ((Ns[q] + sh.bn - 1) / sh.bn);
+  };
+  // Split K finishes inside the kernel, which needs every unit in the first
+  // round of the persistent grid (the splits of a tile wait for each other)
+  // and room for the partials and counters; otherwise no split.
+  float* ws = nullptr;
+  unsigned* cnt = nullptr;
+  if (shp.splits > 1) {
+    const int64_t slots = shp.pair ? std::max(1, cap / 2) : cap;
+    int64_t units = 0, ws_floats = 0, counters = 0;
     for (int q = 0; q < nout; ++q) {
-      const int64_t sp = problem_splits(q, shp);
-      if (sp > 1) need += sp * slice_rows(q, shp) * ws_pitch(Ns[q]);
+      const int64_t sp = problem_splits(q, shp), t = tiles_of(q, shp);
+      units += t * sp;
+      if (sp > 1) {
+        ws_floats += t * 2 * tc::kEpiWarps * sp * 32 * (shp.bn / 2);
+        counters += t * 2 * tc::kEpiWarps * 2;
+      }
     }
-    if (!split_workspace(stream, need, &ws))
+    void* w = nullptr;
+    void* c = nullptr;
+    const bool fits = units <= slots && (may_split || force != nullptr);
+    if (fits && stream_scratch(stream, kScratchSplitWs, ws_floats * sizeof(float), false, &w) &&
+        stream_scratch(stream, kScratchSplitFlags, counters * sizeof(unsigned), true, &c)) {
+      ws = static_cast<float*>(w);
+      cnt = static_cast<unsigned*>(c);
+    } else {
       shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, false, fp32, cap, pair_mode());
+    }
   }
   const int rows = shp.pair ? 256 : tc::BM;
   const int b_box = shp.pair ? shp.bn / 2 : shp.bn;
@@ -1752,9 +1732,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   bt.sum_k = sum_k;
   for (int q = 0; q < count; ++q) bt.sum_kb += static_cast<int>((d[q].K + tc::BK - 1) / tc::BK);
   int units = 0;
-  int64_t ws_used = 0;
-  struct SplitEpi { int epi; const void* R; int64_t ldr; void* Y; int64_t ldy; int vec; };
-  SplitEpi sepi[tc::kMaxProblems] = {};
+  int64_t ws_used = 0, cnt_used = 0;
   for (int q = 0; q < count; ++q) {
     tc::TcProblem& pr = bt.p[q];
     const hap_gemm_desc& g = d[q];
@@ -1772,7 +1750,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
     // grouped problems split K by the same factor (problems with fewer K
     // blocks get fewer splits); a sum splits its concatenated K blocks
-    pr.splits = static_cast<int>(problem_splits(q, shp));
+    pr.splits = ws ? static_cast<int>(problem_splits(q, shp)) : 1;
     pr.kb_per_split = sum_k ? shp.kb_per_split : std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
     if (pr.splits <= 1) {
       pr.splits = 1;
@@ -1781,13 +1759,12 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.accumulate = out.accumulate;
     pr.vec_ok = ((reinterpret_cast<uintptr_t>(out.C) & 15) == 0) && ((out.ldc * osz) % 16 == 0);
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
-    // accumulation and fp32 split-K partials use TMA reduce-add (in L2); a
-    // bf16 accumulate (read-modify-round) stays on per-thread stores; bf16
-    // split K stores fp32 partial slices, summed in order by split_reduce.
+    // accumulation uses TMA reduce-add (one writer per element: in order); a
+    // bf16 accumulate (read-modify-round) is the fused ADD of C itself; split
+    // K finishes in the kernel (split_finish) with per-thread stores.
     pr.epi_mode = tc::EPI_DIRECT;
     pr.epi = (!sum_k || q == 0) ? out.epi : HAP_EPI_NONE;
     pr.epi_tag = out.epi_tag;
-    // bf16 accumulate (read-modify-round) on the TMA path: C = A.B + C
     int epi = pr.epi;
     const void* R = out.R;
     int64_t ldr = out.ldr;
@@ -1798,18 +1775,30 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     }
     if (epi == HAP_EPI_ADD && out.accumulate && pr.splits > 1) epi = HAP_EPI_NONE;   // += C: the accumulate
     pr.epi = epi;
-    if (epi != HAP_EPI_NONE && pr.splits > 1) {
-      // split K: the reduction applies the residual epilogue (split_fusable)
-      HAP_CHECK_ARG(epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2, "hap_matmul: this fused epilogue cannot split K");
-      HAP_CHECK_ARG(R != nullptr && (epi != HAP_EPI_ADD2 || out.Y != nullptr),
+    if (pr.splits > 1 && (!sum_k || q == 0)) {
+      // split K: the finish applies the residual epilogue (split_fusable)
+      HAP_CHECK_ARG(epi == HAP_EPI_NONE || epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2,
+                    "hap_matmul: this fused epilogue cannot split K");
+      HAP_CHECK_ARG(epi == HAP_EPI_NONE || (R != nullptr && (epi != HAP_EPI_ADD2 || out.Y != nullptr)),
                     "hap_matmul: fused epilogue tensor R / Y is null");
-      auto al8 = [](const void* ptr, int64_t ld) { return (reinterpret_cast<uintptr_t>(ptr) & 7) == 0 && ld % 4 == 0; };
-      sepi[q] = {epi, R, ldr, out.Y, out.ldy, al8(R, ldr) && (epi != HAP_EPI_ADD2 || al8(out.Y, out.ldy))};
+      auto aligned = [&](const void* ptr, int64_t ld) {
+        return (reinterpret_cast<uintptr_t>(ptr) & (4 * osz - 1)) == 0 && ld % 4 == 0;
+      };
+      pr.fin_epi = epi;
+      pr.fin_R = R;
+      pr.fin_ldr = ldr;
+      pr.fin_Y = out.Y;
+      pr.fin_ldy = out.ldy;
+      pr.fin_vec = aligned(out.C, out.ldc) && (epi != HAP_EPI_ADD2 || aligned(out.Y, out.ldy));
       pr.epi = HAP_EPI_NONE;
-      pr.accumulate = 0;
-    }
-    if (pr.epi != HAP_EPI_NONE) {
-      HAP_CHECK_ARG(pr.splits <= 1 && pr.vec_ok && tma_epilogue(),
+      pr.ws = ws + ws_used;
+      pr.split_cnt = cnt + cnt_used;
+      const int64_t t = static_cast<int64_t>(pr.m_tiles) * pr.n_tiles;
+      ws_used += t * 2 * tc::kEpiWarps * pr.splits * 32 * (shp.bn / 2);
+      cnt_used += t * 2 * tc::kEpiWarps * 2;
+      pr.epi_mode = tc::EPI_SPLIT_FIN;
+    } else if (pr.epi != HAP_EPI_NONE) {
+      HAP_CHECK_ARG(pr.vec_ok && tma_epilogue(),
                     "hap_matmul: fused epilogue needs a 16-byte pitched output and the TMA epilogue");
       HAP_CHECK_ARG(epi >= HAP_EPI_ADD && epi <= HAP_EPI_SWISH_BWD, "hap_matmul: unknown epilogue op");
       if (epi == HAP_EPI_ADD && out.accumulate) {
@@ -1837,18 +1826,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
       if (!ok) return HAP_ERR_ARG;
       pr.accumulate = 0;
       pr.epi_mode = tc::EPI_TMA_STORE;
-    } else if (!fp32 && pr.splits > 1 && (!sum_k || q == 0)) {
-      pr.ws = ws + ws_used;
-      pr.ws_ld = ws_pitch(out.N);
-      pr.ws_rows = static_cast<int>(slice_rows(q, shp));
-      ws_used += static_cast<int64_t>(pr.splits) * pr.ws_rows * pr.ws_ld;
-      HAP_CHECK_ARG(tc::make_map_c(&pr.c, pr.ws, HAP_F32, out.N, static_cast<int64_t>(pr.splits) * pr.ws_rows,
-                                   pr.ws_ld, shp.bn),
-                    "hap_matmul: workspace tensor map rejected");
-      pr.epi_mode = tc::EPI_SPLIT_WS;
     } else if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
                tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc, shp.bn)) {
-      pr.epi_mode = (fp32 && (pr.accumulate || pr.splits > 1)) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
+      pr.epi_mode = (fp32 && pr.accumulate) ? tc::EPI_TMA_ADD : tc::EPI_TMA_STORE;
     }
     pr.unit_begin = units;
     if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
@@ -1877,9 +1857,6 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
       bt.total_units = P;
     }
   }
-  for (int q = 0; q < nout; ++q)  // fp32 split-K partials add into a zeroed output
-    if (fp32 && bt.p[q].splits > 1 && !d[q].accumulate)
-      HAP_CUDA_TRY(cudaMemset2DAsync(d[q].C, d[q].ldc * osz, 0, d[q].N * osz, d[q].M, stream));
   static const bool log_shapes = getenv("HAP_GEMM_LOG") != nullptr;
   if (log_shapes) {
     fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d kbps %d units %d sk %d |",
@@ -1891,29 +1868,8 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
               d[q].accumulate);
     fprintf(stderr, "\n");
   }
-  hap_status st = fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
-                       : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
-  if (st != HAP_OK) return st;
-  for (int q = 0; q < nout; ++q) {
-    const tc::TcProblem& pr = bt.p[q];
-    if (pr.epi_mode != tc::EPI_SPLIT_WS) continue;
-    const int64_t work = static_cast<int64_t>(pr.M) * ((pr.N + 3) / 4);
-    const int grid = capped_grid((work + 255) / 256, cap * 4);
-    const int64_t slice = static_cast<int64_t>(pr.ws_rows) * pr.ws_ld;
-    const SplitEpi& se = sepi[q];
-    if (fp32)
-      launch_k(tc::split_reduce_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(pr.ws),
-               pr.splits, slice, pr.ws_ld, static_cast<float*>(pr.C), pr.ldc, pr.M, pr.N, pr.accumulate,
-               pr.vec_ok, 0, nullptr, 0, nullptr, 0);
-    else
-      launch_k(tc::split_reduce_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
-               static_cast<const float*>(pr.ws), pr.splits, slice, pr.ws_ld, static_cast<__nv_bfloat16*>(pr.C),
-               pr.ldc, pr.M, pr.N, pr.accumulate, pr.vec_ok && (se.epi == HAP_EPI_NONE || se.vec), se.epi,
-               static_cast<const __nv_bfloat16*>(se.R), se.ldr, static_cast<__nv_bfloat16*>(se.Y), se.ldy);
-    st = launch_status("split_reduce_kernel");
-    if (st != HAP_OK) return st;
-  }
-  return HAP_OK;
+  return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
+              : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
 }
 
 hap_status simt_one(const hap_gemm_desc& g, hap_dtype in_dtype, hap_dtype out_dtype, int sm_cap,
@@ -1965,6 +1921,10 @@ extern "C" hap_status hap_matmul_tune(const hap_gemm_desc* descs, int count, int
   HAP_CHECK_ARG(cs == cudaStreamCaptureStatusNone, "hap_matmul_tune: not during stream capture");
   const int cap = sm_cap > 0 && sm_cap < sm_count() ? sm_cap : sm_count();
   const bool fp32 = out_dtype == HAP_F32;
+  {   // a signature is timed once per process (or imported): later executors reuse the choice
+    std::lock_guard<std::mutex> lock(tune_mutex());
+    if (tune_cache().count(tune_key(descs, count, sum_k, fp32, cap))) return HAP_OK;
+  }
   const int nout = sum_k ? 1 : count;
   bool fused = false;
   for (int q = 0; q < nout; ++q) fused = fused || descs[q].epi != HAP_EPI_NONE;
@@ -2150,4 +2110,50 @@ extern "C" hap_status hap_matmul(const void* A, int64_t lda, int transA, const v
   g.A = A; g.lda = lda; g.transA = transA; g.B = B; g.ldb = ldb; g.transB = transB;
   g.C = C; g.ldc = ldc; g.M = M; g.N = N; g.K = K; g.accumulate = accumulate;
   return hap_matmul_batch(&g, 1, 0, in_dtype, out_dtype, sm_cap, stream);
+}
+
+// Tuning table as text, one signature per line: "<key>\t<pair> <bn> <splits>
+// <kb_per_split>\n" (keys sorted, so the same table prints the same bytes).
+extern "C" int64_t hap_matmul_tune_export(char* buf, int64_t cap) {
+  std::vector<std::pair<std::string, tc::Shape>> rows;
+  {
+    std::lock_guard<std::mutex> lock(tune_mutex());
+    rows.assign(tune_cache().begin(), tune_cache().end());
+  }
+  std::sort(rows.begin(), rows.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::string text;
+  for (const auto& r : rows)
+    text += r.first + "\t" + std::to_string(r.second.pair ? 1 : 0) + " " + std::to_string(r.second.bn) + " " +
+            std::to_string(r.second.splits) + " " + std::to_string(r.second.kb_per_split) + "\n";
+  const int64_t need = static_cast<int64_t>(text.size()) + 1;
+  if (buf && cap >= need) std::memcpy(buf, text.c_str(), static_cast<size_t>(need));
+  return need;
+}
+
+extern "C" hap_status hap_matmul_tune_import(const char* text) {
+  HAP_CHECK_ARG(text != nullptr, "hap_matmul_tune_import: null text");
+  std::vector<std::pair<std::string, tc::Shape>> rows;
+  const char* p = text;
+  while (*p) {
+    const char* eol = std::strchr(p, '\n');
+    const std::string line(p, eol ? static_cast<size_t>(eol - p) : std::strlen(p));
+    p = eol ? eol + 1 : p + line.size();
+    if (line.empty()) continue;
+    const size_t tab = line.find('\t');
+    int pair = 0, bn = 0, splits = 0, kbps = 0;
+    HAP_CHECK_ARG(tab != std::string::npos &&
+                      std::sscanf(line.c_str() + tab + 1, "%d %d %d %d", &pair, &bn, &splits, &kbps) == 4,
+                  "hap_matmul_tune_import: malformed line: " + line);
+    HAP_CHECK_ARG((bn == 128 || bn == 256 || (bn == 192 && pair)) && splits >= 1 && kbps >= 1,
+                  "hap_matmul_tune_import: bad shape: " + line);
+    rows.push_back({line.substr(0, tab), tc::Shape{bn, splits, kbps, pair != 0}});
+  }
+  std::lock_guard<std::mutex> lock(tune_mutex());
+  for (const auto& r : rows) tune_cache()[r.first] = r.second;
+  return HAP_OK;
+}
+
+extern "C" void hap_matmul_tune_clear(void) {
+  std::lock_guard<std::mutex> lock(tune_mutex());
+  tune_cache().clear();
 }

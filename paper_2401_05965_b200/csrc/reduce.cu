@@ -5,9 +5,11 @@
 // contiguous run — every reduction the planner emits on rank-<=2 graphs —
 // with three kernels: a grid-wide sum (outer = inner = 1, e.g. the loss),
 // a row sum (inner = 1) and a column sum (inner > 1, coalesced over inner and
-// split over `red` across CTAs).  Accumulation is fp32; cross-CTA partials
-// are combined with fp32 atomics, so the output of a split reduction must be
-// fp32.  Other axis sets use a generic index-decoding kernel.
+// split over `red` across CTAs).  Accumulation is fp32 and DETERMINISTIC: a
+// split reduction writes one fp32 partial per CTA into a per-stream scratch
+// slot, and the last CTA to arrive (ticket counter) adds the partials in a
+// fixed order — no floating-point atomics, so repeated runs give identical
+// bits.  Other axis sets use a generic index-decoding kernel.
 #include "common.cuh"
 
 namespace hap {
@@ -58,17 +60,34 @@ __device__ __forceinline__ float block_sum(float v) {
   return v;  // valid in thread 0
 }
 
-// Sum of all n elements into y[0] (fp32, atomics across CTAs).
+// Sum of all n elements into y[0] (+ y[0] when accumulating).  Each CTA
+// writes its partial to partials[blockIdx.x]; the last CTA to take a ticket
+// sums the gridDim.x partials with the fixed block_sum tree and resets the
+// ticket for the next launch on the stream.
 template <typename Tin>
-__global__ void __launch_bounds__(1024) sum_all_kernel(const Tin* __restrict__ x, int64_t n,
-                                                       float* y) {
+__global__ void __launch_bounds__(1024) sum_all_kernel(const Tin* __restrict__ x, int64_t n, float* y,
+                                                       int accumulate, float* partials, unsigned* ticket) {
   hap::pdl_enter();
+  __shared__ bool last;
   float acc = 0.f;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     acc += to_f32(x[i]);
   acc = block_sum(acc);
-  if (threadIdx.x == 0) atomicAdd(y, acc);
+  if (threadIdx.x == 0) {
+    __stcg(partials + blockIdx.x, acc);
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float v = threadIdx.x < gridDim.x ? __ldcg(partials + threadIdx.x) : 0.f;
+  v = block_sum(v);
+  if (threadIdx.x == 0) {
+    y[0] = accumulate ? y[0] + v : v;
+    *ticket = 0u;
+  }
 }
 
 // One CTA per row of [outer, red]: y[o] (+)= sum_r x[o, r].
@@ -85,23 +104,43 @@ __global__ void __launch_bounds__(256) row_sum_kernel(const Tin* __restrict__ x,
   }
 }
 
-// Column sums of [outer, red, inner]: CTA (bx, by) covers 256 inner positions
-// of one outer slice and a chunk of `red`; partials land with atomics.
+// Column sums of [outer, red, inner]: CTA (bx, by) covers 256 inner
+// positions of one outer slice and chunk `by` of `red`, and writes its fp32
+// partial to partials[by][o * inner + i]; the last of the gridDim.y CTAs of a
+// column tile (ticket per tile) adds the chunks in order into y.
 template <typename Tin>
 __global__ void __launch_bounds__(256) col_sum_kernel(const Tin* __restrict__ x, int64_t outer,
                                                       int64_t red, int64_t inner, int64_t chunk,
-                                                      float* y) {
+                                                      float* y, int accumulate, float* partials,
+                                                      unsigned* tickets) {
   hap::pdl_enter();
+  __shared__ bool last;
   const int64_t i_tiles = (inner + 255) / 256;
+  const int64_t plane = outer * inner;
   for (int64_t t = blockIdx.x; t < outer * i_tiles; t += gridDim.x) {
     const int64_t o = t / i_tiles;
     const int64_t i = (t % i_tiles) * 256 + threadIdx.x;
-    if (i >= inner) continue;
-    const int64_t r0 = blockIdx.y * chunk;
-    const int64_t r1 = r0 + chunk < red ? r0 + chunk : red;
-    float acc = 0.f;
-    for (int64_t r = r0; r < r1; ++r) acc += to_f32(x[(o * red + r) * inner + i]);
-    atomicAdd(y + o * inner + i, acc);
+    if (i < inner) {
+      const int64_t r0 = blockIdx.y * chunk;
+      const int64_t r1 = r0 + chunk < red ? r0 + chunk : red;
+      float acc = 0.f;
+      for (int64_t r = r0; r < r1; ++r) acc += to_f32(x[(o * red + r) * inner + i]);
+      __stcg(partials + blockIdx.y * plane + o * inner + i, acc);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(tickets + t, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      if (i < inner) {
+        float v = 0.f;
+        for (unsigned s = 0; s < gridDim.y; ++s) v += __ldcg(partials + s * plane + o * inner + i);
+        y[o * inner + i] = accumulate ? y[o * inner + i] + v : v;
+      }
+      if (threadIdx.x == 0) tickets[t] = 0u;
+    }
+    __syncthreads();
   }
 }
 
@@ -216,35 +255,38 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
       return launch_status("row_sum_kernel");
     });
   }
-  // Split reductions accumulate with fp32 atomics.
+  // Split reductions: fp32 partials in the stream's scratch, summed in order.
   HAP_CHECK_ARG(yd == HAP_F32, "hap_reduce: split reductions need an fp32 output");
-  if (!accumulate) HAP_CUDA_TRY(cudaMemsetAsync(y, 0, n_out * sizeof(float), stream));
-  if (g.outer == 1 && g.inner == 1) {
-    const int grid = capped_grid((g.red + 4095) / 4096, sm_cap);
-    if (xd == HAP_BF16)
-      hap::launch_k(sum_all_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream, 
-          static_cast<const __nv_bfloat16*>(x), g.red, static_cast<float*>(y));
-    else
-      hap::launch_k(sum_all_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<const float*>(x), g.red,
-                                                       static_cast<float*>(y));
-    return launch_status("sum_all_kernel");
-  }
-  if (g.inner == 1) {  // few long rows: treat each row as a full sum
+  const int cap = sm_cap > 0 ? sm_cap : sm_count();
+  float* partials = nullptr;
+  unsigned* tickets = nullptr;
+  auto scratch = [&](size_t part_floats, size_t n_tickets) -> bool {
+    void* p = nullptr;
+    void* t = nullptr;
+    if (!stream_scratch(stream, kScratchReduce, part_floats * sizeof(float), false, &p) ||
+        !stream_scratch(stream, kScratchReduceTickets, n_tickets * sizeof(unsigned), true, &t))
+      return false;
+    partials = static_cast<float*>(p);
+    tickets = static_cast<unsigned*>(t);
+    return true;
+  };
+  if (g.inner == 1) {  // one full sum (the loss), or a few long rows each treated as one
+    const int grid = capped_grid((g.red + 4095) / 4096, cap);
+    HAP_CHECK_ARG(scratch(grid, 1), "hap_reduce: no reduction scratch (first use inside stream capture?)");
+    const size_t xs = dtype_size(xd);
     for (int64_t o = 0; o < g.outer; ++o) {
-      const int grid = capped_grid((g.red + 4095) / 4096, sm_cap);
-      const size_t xs = dtype_size(xd);
       const void* row = static_cast<const char*>(x) + o * g.red * xs;
       if (xd == HAP_BF16)
-        hap::launch_k(sum_all_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream, 
-            static_cast<const __nv_bfloat16*>(row), g.red, static_cast<float*>(y) + o);
+        hap::launch_k(sum_all_kernel<__nv_bfloat16>, dim3(grid), dim3(1024), 0, stream,
+                      static_cast<const __nv_bfloat16*>(row), g.red, static_cast<float*>(y) + o, accumulate,
+                      partials, tickets);
       else
-        hap::launch_k(sum_all_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<const float*>(row), g.red,
-                                                         static_cast<float*>(y) + o);
+        hap::launch_k(sum_all_kernel<float>, dim3(grid), dim3(1024), 0, stream, static_cast<const float*>(row),
+                      g.red, static_cast<float*>(y) + o, accumulate, partials, tickets);
     }
     return launch_status("sum_all_kernel");
   }
   const int64_t i_tiles = (g.inner + 255) / 256;
-  const int cap = sm_cap > 0 ? sm_cap : sm_count();
   const int64_t want_y = (4LL * cap + g.outer * i_tiles - 1) / (g.outer * i_tiles);
   int64_t splits = want_y < 1 ? 1 : want_y;
   if (splits > g.red) splits = g.red;
@@ -252,12 +294,15 @@ extern "C" hap_status hap_reduce(const void* x, hap_dtype xd, const int64_t* sha
   splits = (g.red + chunk - 1) / chunk;
   dim3 grid(static_cast<unsigned>(capped_grid(g.outer * i_tiles, 4 * cap)),
             static_cast<unsigned>(splits));
+  HAP_CHECK_ARG(scratch(static_cast<size_t>(splits) * g.outer * g.inner, g.outer * i_tiles),
+                "hap_reduce: no reduction scratch (first use inside stream capture?)");
   if (xd == HAP_BF16)
-    hap::launch_k(col_sum_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream, 
-        static_cast<const __nv_bfloat16*>(x), g.outer, g.red, g.inner, chunk, static_cast<float*>(y));
+    hap::launch_k(col_sum_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
+        static_cast<const __nv_bfloat16*>(x), g.outer, g.red, g.inner, chunk, static_cast<float*>(y), accumulate,
+        partials, tickets);
   else
-    hap::launch_k(col_sum_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(x), g.outer, g.red,
-                                                    g.inner, chunk, static_cast<float*>(y));
+    hap::launch_k(col_sum_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(x), g.outer,
+                  g.red, g.inner, chunk, static_cast<float*>(y), accumulate, partials, tickets);
   return launch_status("col_sum_kernel");
 }
 

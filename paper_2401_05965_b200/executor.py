@@ -155,8 +155,11 @@ class ExecConfig:
     overlap_sfb: bool = True          # NCCL groups: SFB factor gathers on a side stream (activations
                                       # during the forward), weight-gradient GEMMs at the end of backward
     bucket_bytes: int = 32 << 20      # NCCL groups: gradients all-reduced in buckets of about this size
-    autotune: bool = os.environ.get("HAP_AUTOTUNE", "1") == "1"   # time each GEMM signature's tile shapes /
-                                      # split-K once at compile time (hap_matmul_tune) and keep the fastest
+    autotune: str = os.environ.get("HAP_AUTOTUNE", "table")   # GEMM tile shape / split-K per launch
+                                      # signature: "table" = the committed B200 table (_lib.TUNE_TABLE), the
+                                      # host heuristic for signatures it lacks — the same choice, hence the
+                                      # same rounding, in every process; "time" = also time the signatures
+                                      # the table lacks (hap_matmul_tune, fastest kept); "off" = heuristic
     wgrad_stream: bool = os.environ.get("HAP_WGRAD_STREAM", "0") == "1"   # parameter-gradient GEMMs on a
                                       # side stream, to run in the tails of the activation-gradient chain;
                                       # off: measured no gain (persistent GEMMs keep their static tile
@@ -268,14 +271,23 @@ class Executor:
         self.sgd_stats = (0, 0)
         if self.cfg.lr and self._sgd_items and self._want_sgd_overlap():
             self._overlap_sgd()
-        if self.cfg.autotune and self.wdt == BF16:
+        self.tuned_signatures = 0
+        if self.wdt == BF16:
             self._autotune()
         self._create_symm()
 
     def _autotune(self):
-        """One hap_matmul_tune per distinct GEMM launch signature (layers
-        repeat shapes): the library times every tile shape / split of the
-        batch on scratch outputs and uses the fastest from then on."""
+        """Tile shapes of the GEMM launches.  "table" / "time": import the
+        committed tuning table; "time" additionally runs one hap_matmul_tune
+        per distinct launch signature the table lacks (layers repeat shapes):
+        the library times every tile shape / split of the batch on scratch
+        outputs and uses the fastest from then on."""
+        mode = {True: "time", False: "off", "1": "time", "0": "off"}.get(self.cfg.autotune, self.cfg.autotune)
+        if mode == "off":
+            return
+        _lib.load_tune_table()
+        if mode != "time":
+            return
         seen = set()
         for op in self.ops_fwd + self.ops_bwd:
             if op.gemm is None:

@@ -3,7 +3,8 @@ reference interpreter's golden outputs and the CPU oracle, for every golden
 plan and every enumerated program with collectives, with all m program
 devices emulated on one GPU (LocalGroup).  Tolerances: rtol 2e-2 in bf16,
 1e-3 in fp32 (north_star), relative to max(|reference|, 1) per value and to
-the largest reference magnitude for gradient tensors."""
+the largest reference magnitude for gradient tensors; bf16 losses also
+within 5e-3 of the oracle evaluated in bf16 storage precision."""
 import numpy as np
 import pytest
 import torch
@@ -34,25 +35,31 @@ def _run(doc, g, inputs, dtype, lr=0.0, grad_sync="auto"):
     return ex
 
 
-def loss_scale(doc, inputs, want):
-    """Tolerance scale of a summed loss: max(|loss|, 1, ||summands||_2).
-
-    A loss that is the sum of N terms carrying independent relative rounding
-    errors eps has error ~ eps * ||terms||_2; when the terms cancel, |loss|
-    alone is far below that (the MLP sums 65536 terms of |.|-sum 3.7e4 to
-    42), so the 2-norm of the reduced tensor is the honest denominator."""
-    program, m, table = O.load_plan(doc)
-    env, _ = O.run_distributed(program, m, inputs, table)
-    norm = 0.0
-    for ins in program.instrs:
-        if ins.ref == program.loss and ins.kind == "reduce":
-            norm = max(norm, float(np.sqrt(sum(np.sum(np.square(v)) for v in env[ins.operands[0]]))))
-    return np.maximum(np.maximum(np.abs(want), 1.0), norm)
+# bf16 storage alone moves these losses more than the bf16 tolerance away
+# from the float64 reference: the oracle run in bf16 storage precision is
+# itself that far off (asserted below), so the executor is held to the
+# storage-precision oracle for them.  mlp.ratio12 (configs[0]) sums 65 536
+# terms of |.|-sum 3.7e4 to a loss of 42: 3.8 % in bf16 storage.
+KNOWN_BF16_STORAGE_GAP = {"mlp.ratio12"}
+LOSS_RTOL_STORAGE = 5e-3    # bf16 run vs the oracle in bf16 storage precision
 
 
-def _check_losses(ex, want, dtype, scale):
+def _check_losses(ex, doc, inputs, want, dtype, case):
+    """Losses against (1) the float64 reference goldens at the north_star
+    tolerance, relative to max(|loss|, 1) as the reference's check_equivalence
+    scales (interpreter.py:264-277), and (2) in bf16, the oracle evaluated in
+    the executor's storage precision at 5e-3."""
     got = np.array(ex.losses())
-    assert np.all(np.abs(got - want) <= RTOL[dtype] * scale), (got, want, scale)
+    scale = np.maximum(np.abs(want), 1.0)
+    if dtype == "bf16":
+        program, m, table = O.load_plan(doc)
+        _, stored = O.run_distributed(program, m, inputs, table, precision="bf16")
+        stored = np.array(stored, dtype=np.float64)
+        assert np.all(np.abs(got - stored) <= LOSS_RTOL_STORAGE * np.maximum(np.abs(stored), 1.0)), (got, stored)
+        if case in KNOWN_BF16_STORAGE_GAP:
+            assert np.any(np.abs(stored - want) > RTOL[dtype] * scale), f"{case} no longer needs the exception"
+            return
+    assert np.all(np.abs(got - want) <= RTOL[dtype] * scale), (got, want)
 
 
 def _check_grads(ex, g, inputs, dtype, doc):
@@ -92,7 +99,7 @@ def test_planned_programs_match_reference(gname, cname, dtype):
     inputs = goldens.inputs(g, vals, seed)
     ex = _run(doc, g, inputs, dtype)
     want = vals[f"seed{seed}:losses"]
-    _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
+    _check_losses(ex, doc, inputs, want, dtype, f"{gname}.{cname}")
     for did, insts in goldens.env(vals).items():
         for r, want in enumerate(insts):
             got = ex.tensor(did, r).float().cpu().numpy()
@@ -110,7 +117,7 @@ def test_programs_with_collectives_match_reference(stem, dtype):
     inputs = {k.split(":", 2)[2]: vals[k] for k in vals.files if k.startswith("seed0:input:")}
     ex = _run(doc, g, inputs, dtype)
     want = vals["seed0:losses"]
-    _check_losses(ex, want, dtype, loss_scale(doc, inputs, want))
+    _check_losses(ex, doc, inputs, want, dtype, stem)
     _check_grads(ex, g, inputs, dtype, doc)
 
 
