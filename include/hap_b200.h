@@ -243,6 +243,12 @@ hap_status hap_symm_create(void** ctx, int64_t bytes, int rank, int nranks);
 hap_status hap_symm_handle(void* ctx, uint8_t* out64);
 hap_status hap_symm_open(void* ctx, const uint8_t* handles64xn);
 hap_status hap_symm_destroy(void* ctx);
+/* All ranks in ONE process (e.g. several program devices on one GPU, each on
+ * its own stream — the driver-verifiable form of the multi-GPU path): no IPC;
+ * `peer_bases` holds every rank's hap_symm_local_base() (own included), and
+ * registered buffers are exchanged as plain device pointers. */
+hap_status hap_symm_open_local(void* ctx, const int64_t* peer_bases);
+void* hap_symm_local_base(void* ctx);
 int64_t hap_symm_capacity(void* ctx);
 /* all_gather along a blocked axis with uneven shards — interpreter.py:69-71:
  * rank j's shard is [outer, sizes[j], inner]; the output is
@@ -283,7 +289,23 @@ hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void* recv, hap
 hap_status hap_p2p_reduce_scatter_direct(void* ctx, const void* const* dev_sends, void* recv, hap_dtype dtype,
                                          int64_t outer, int64_t inner, int64_t extent, const int64_t* dev_sizes,
                                          const int64_t* dev_offsets, int64_t recv_elems, int sm_cap, void* stream);
-/* Bandwidth probe (no flag protocol; callers separate calls with a host
+/* all_reduce — interpreter.py:74-78 — over registered buffers, no NCCL:
+ * `dev_ins` / `dev_outs` are DEVICE arrays of every rank's input / output
+ * pointer (in == out allowed).  Two-shot in one kernel: rank c reduces chunk
+ * c from all inputs (fp32, rank order 0..m-1 — the LocalGroup sum bit for bit)
+ * and stores it into every output. */
+hap_status hap_p2p_all_reduce(void* ctx, const void* const* dev_ins, void* const* dev_outs, hap_dtype dtype,
+                              int64_t count, int sm_cap, void* stream);
+/* all_to_all — interpreter.py:99-101 — by pushing: chunk k of `send`
+ * (dev_send_off[k], dev_counts[k] elements) is stored into rank k's
+ * registered receive buffer (dev_recvs[k]) at dev_dst_off[k].  DEVICE int64
+ * arrays of nranks entries; `max_elems` sizes the grid. */
+hap_status hap_p2p_all_to_all(void* ctx, const void* send, void* const* dev_recvs, hap_dtype dtype,
+                              const int64_t* dev_send_off, const int64_t* dev_counts, const int64_t* dev_dst_off,
+                              int64_t max_elems, int sm_cap, void* stream);
+/* Every peer-memory kernel spins on flags, so its grid is launched
+ * cooperatively (co-residency guaranteed by the driver; HAP_P2P_COOP=0 off).
+ * Bandwidth probe (no flag protocol; callers separate calls with a host
  * barrier): moves `chunk_bytes` between this rank and every peer through the
  * arenas.  mode 0/1: pull / push one peer after another; 2/3: pull / push with
  * the grid split across all peers at once; 4: the same bytes as a local copy. */

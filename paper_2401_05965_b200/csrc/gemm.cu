@@ -1713,9 +1713,12 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     }
     void* w = nullptr;
     void* c = nullptr;
-    const bool fits = units <= slots && (may_split || force != nullptr);
-    if (fits && stream_scratch(stream, kScratchSplitWs, ws_floats * sizeof(float), false, &w) &&
-        stream_scratch(stream, kScratchSplitFlags, counters * sizeof(unsigned), true, &c)) {
+    if (units <= slots && (may_split || force != nullptr)) {
+      // no silent fallback: a different split factor would round differently
+      HAP_CHECK_ARG(stream_scratch(stream, kScratchSplitWs, ws_floats * sizeof(float), false, &w) &&
+                        stream_scratch(stream, kScratchSplitFlags, counters * sizeof(unsigned), true, &c),
+                    "hap_matmul: no split-K workspace on this stream (out of memory, or its first split launch "
+                    "is inside a CUDA graph capture: launch once eagerly first)");
       ws = static_cast<float*>(w);
       cnt = static_cast<unsigned*>(c);
     } else {

@@ -22,6 +22,7 @@
 // Every CTA spins on flags another GPU writes, so the grid is one CTA per
 // (capped) SM, all resident; separate GPUs run the ranks, never one GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -54,6 +55,7 @@ struct Symm {
   char* local = nullptr;                 // arena base (signal page + staging)
   char* peers[kMaxRanks] = {};           // peer arena bases (IPC-mapped), peers[rank] = local
   std::map<std::pair<int, uint64_t>, char*> opened;   // (peer, its allocation base) -> mapped here
+  bool local_open = false;               // peers are arenas of this process (hap_symm_open_local)
 };
 
 struct Peers {
@@ -281,10 +283,8 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_kernel(Peers peer
     const int64_t o = e / per, rem = e - o * per;
     const int64_t at = (o * extent + off) * inner + rem;
     float acc = 0.f;
-    for (int q = 0; q < nranks; ++q) {
-      const int p = (rank + q) % nranks;
+    for (int p = 0; p < nranks; ++p)   // rank order: the sum LocalGroup and every other path computes
       acc += to_f32(p == rank ? send[at] : reinterpret_cast<const T*>(peers.base[p] + kSignalBytes)[at]);
-    }
     out[e] = from_f32<T>(acc);
   }
   if (grid_barrier(sig) && threadIdx.x == 0) {
@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(kThreads) p2p_probe_kernel(Peers peers, int ra
 //   1. CTA 0 tells each peer ready[r] = e+1 (my partial is complete: the
 //      kernel started after its producers); every CTA waits for all peers;
 //   2. sum: 16-byte loads from every rank's partial (own from local HBM),
-//      fp32 accumulation in rank order (r, r+1, ...), one rounding;
+//      fp32 accumulation in rank order (0, 1, ..., m-1 — the order of the
+//      single-GPU LocalGroup sum, so both give the same bits), one rounding;
 //   3. grid barrier, done[r] = e+1 on every peer (finished reading theirs);
 //      every CTA waits for every peer's done, so my partial is not
 //      overwritten by later work on my stream while a peer still reads it.
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
       int4 v[kMaxRanks];   // every rank's load in flight before the sum (registers: fully unrolled)
 #pragma unroll
       for (int q = 0; q < kMaxRanks; ++q)
-        if (q < nranks) v[q] = reinterpret_cast<const int4*>(sends[(rank + q) % nranks])[at];
+        if (q < nranks) v[q] = reinterpret_cast<const int4*>(sends[q])[at];
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int q = 0; q < kMaxRanks; ++q)
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
       const int64_t o = e / per, rem = e - o * per;
       const int64_t at = (o * extent + off) * inner + rem;
       float acc = 0.f;
-      for (int q = 0; q < nranks; ++q) acc += to_f32(sends[(rank + q) % nranks][at]);
+      for (int q = 0; q < nranks; ++q) acc += to_f32(sends[q][at]);
       out[e] = from_f32<T>(acc);
     }
   }
@@ -438,6 +439,127 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
   }
   if (peer_thread)
     while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
+}
+
+
+// All-reduce over registered buffers (two-shot, one kernel): the tensor is
+// cut into nranks chunks of whole 8-element groups; rank c reduces chunk c
+// straight out of every rank's registered input (16-byte NVLink loads, all
+// in flight before the sum, fp32 accumulation in rank order 0..m-1, one
+// rounding — the LocalGroup sum bit for bit) and stores the result into
+// every rank's registered output.  Each element is read and then written by
+// the same thread, so in == out (in-place gradient buckets) is safe.
+// Protocol (epoch e): armed[r] = e+1 on every peer at start (my input is
+// complete and my output no longer read by earlier work on my stream), wait
+// for every peer's armed; reduce + push; grid barrier; done[r] = e+1 on every
+// peer; wait for every peer's done (my output complete, my input released).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_all_reduce_kernel(Peers peers, int rank, int nranks,
+                                                                  const T* const* __restrict__ ins,
+                                                                  T* const* __restrict__ outs, int64_t count) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  const bool peer_thread = threadIdx.x < nranks && threadIdx.x != rank;
+  if (blockIdx.x == 0 && peer_thread)
+    st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  constexpr int kv = 16 / sizeof(T);
+  const int64_t groups = count / 8;                     // whole 8-element groups, split into chunks
+  const int64_t g0 = groups * rank / nranks, g1 = groups * (rank + 1) / nranks;
+  const int64_t lo = g0 * 8, hi = rank == nranks - 1 ? count : g1 * 8;   // the tail goes to the last rank
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  bool vec = true;
+  for (int p = 0; p < nranks; ++p)
+    vec = vec && ((reinterpret_cast<uintptr_t>(ins[p]) | reinterpret_cast<uintptr_t>(outs[p])) & 15) == 0;
+  int64_t scalar_from = lo;
+  if (vec) {
+    const int64_t n4 = (g1 * 8 - lo) / kv;
+    for (int64_t e = tid; e < n4; e += stride) {
+      const int64_t at = lo / kv + e;
+      int4 v[kMaxRanks];
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < nranks) v[q] = reinterpret_cast<const int4*>(ins[q])[at];
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < nranks) add8<T>(acc, v[q]);
+      int4 r;
+      if constexpr (sizeof(T) == 2) {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+      } else {
+        float* f = reinterpret_cast<float*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i] = acc[i];
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxRanks; ++q)
+        if (q < nranks) reinterpret_cast<int4*>(outs[(rank + q) % nranks])[at] = r;   // own output last-ish
+    }
+    scalar_from = g1 * 8;
+  }
+  for (int64_t e = scalar_from + tid; e < hi; e += stride) {
+    float acc = 0.f;
+    for (int q = 0; q < nranks; ++q) acc += to_f32(ins[q][e]);
+    const T r = from_f32<T>(acc);
+    for (int q = 0; q < nranks; ++q) outs[q][e] = r;
+  }
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[p])->done[rank], epoch + 1);
+      st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[p])->ready[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
+}
+
+// All-to-all by pushing contiguous chunks: rank r stores chunk k of its send
+// buffer (elements [send_off[k], send_off[k] + cnt[k])) straight into rank
+// k's registered receive buffer at dst_off[k] (its rank-ordered receive
+// layout), own chunk included.  Same armed / ready protocol as the push
+// all-gather.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) p2p_all_to_all_kernel(Peers peers, int rank, int nranks,
+                                                                  const T* __restrict__ send,
+                                                                  T* const* __restrict__ recvs,
+                                                                  const int64_t* __restrict__ send_off,
+                                                                  const int64_t* __restrict__ cnt,
+                                                                  const int64_t* __restrict__ dst_off) {
+  hap::pdl_wait();
+  SignalPage* sig = reinterpret_cast<SignalPage*>(peers.base[rank]);
+  const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
+  const bool peer_thread = threadIdx.x < nranks && threadIdx.x != rank;
+  if (blockIdx.x == 0 && peer_thread)
+    st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+  __syncthreads();
+  for (int q = 1; q <= nranks; ++q) {
+    const int k = (rank + q) % nranks;   // peers staggered across ranks, own chunk last
+    if (cnt[k] > 0) copy_elems(recvs[k] + dst_off[k], send + send_off[k], cnt[k]);
+  }
+  if (grid_barrier(sig) && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      SignalPage* peer_sig = reinterpret_cast<SignalPage*>(peers.base[p]);
+      st_release_sys(&peer_sig->ready[rank], epoch + 1);
+      st_release_sys(&peer_sig->done[rank], epoch + 1);
+    }
+    sig->epoch = epoch + 1;
+  }
+  if (peer_thread)
+    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
 }
 
 }  // namespace
@@ -505,8 +627,9 @@ extern "C" hap_status hap_symm_destroy(void* ctx) {
   auto* s = static_cast<Symm*>(ctx);
   if (!s) return HAP_OK;
   for (auto& kv : s->opened) cudaIpcCloseMemHandle(kv.second);
-  for (int p = 0; p < s->nranks; ++p)
-    if (p != s->rank && s->peers[p]) cudaIpcCloseMemHandle(s->peers[p]);
+  if (!s->local_open)
+    for (int p = 0; p < s->nranks; ++p)
+      if (p != s->rank && s->peers[p]) cudaIpcCloseMemHandle(s->peers[p]);
   cudaFree(s->local);
   delete s;
   return HAP_OK;
@@ -586,6 +709,36 @@ inline int p2p_grid(int64_t bytes, int sm_cap) {
   return capped_grid(want, sm_cap);
 }
 
+// Every CTA of a peer-memory kernel spins on flags (peers' and the grid
+// barrier's), so the whole grid must be resident at once: launched
+// cooperatively, the driver guarantees co-residency (or fails the launch
+// loudly) even when other kernels — a persistent GEMM on another stream —
+// hold SMs.  HAP_P2P_COOP=0 launches plainly.
+int p2p_cooperative() {
+  static int on = [] {
+    const char* v = getenv("HAP_P2P_COOP");
+    return v ? atoi(v) : 1;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_p2p(void (*kern)(KArgs...), int grid, cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = p2p_cooperative();
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <typename T>
 hap_status p2p_launch(void (*kern)(Peers, int, int, const T*, T*, int64_t, int64_t, int64_t, const int64_t*,
                                    const int64_t*),
@@ -595,8 +748,8 @@ hap_status p2p_launch(void (*kern)(Peers, int, int, const T*, T*, int64_t, int64
   Peers peers{};
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   const int grid = p2p_grid(bytes, sm_cap);   // every CTA resident (they spin on peer flags)
-  launch_k(kern, dim3(grid), dim3(kThreads), 0, stream, peers, s->rank, s->nranks, static_cast<const T*>(send),
-           static_cast<T*>(out), outer, inner, extent, dev_sizes, dev_offs);
+  launch_p2p(kern, grid, stream, peers, s->rank, s->nranks, static_cast<const T*>(send), static_cast<T*>(out), outer,
+             inner, extent, dev_sizes, dev_offs);
   return launch_status("p2p kernel");
 }
 
@@ -631,11 +784,10 @@ extern "C" hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void*
   const int grid = p2p_grid(total_elems * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
   auto st = static_cast<cudaStream_t>(stream);
   if (dtype == HAP_BF16)
-    launch_k(p2p_all_gather_push_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank,
-             s->nranks, static_cast<const __nv_bfloat16*>(send), reinterpret_cast<__nv_bfloat16* const*>(dev_outs),
+    launch_p2p(p2p_all_gather_push_kernel<__nv_bfloat16>, grid, st, peers, s->rank, s->nranks, static_cast<const __nv_bfloat16*>(send), reinterpret_cast<__nv_bfloat16* const*>(dev_outs),
              outer, inner, extent, dev_sizes, dev_offsets);
   else
-    launch_k(p2p_all_gather_push_kernel<float>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank, s->nranks,
+    launch_p2p(p2p_all_gather_push_kernel<float>, grid, st, peers, s->rank, s->nranks,
              static_cast<const float*>(send), reinterpret_cast<float* const*>(dev_outs), outer, inner, extent,
              dev_sizes, dev_offsets);
   return launch_status("p2p push all-gather");
@@ -652,11 +804,10 @@ extern "C" hap_status hap_p2p_reduce_scatter_direct(void* ctx, const void* const
   const int grid = p2p_grid(recv_elems * s->nranks * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
   auto st = static_cast<cudaStream_t>(stream);
   if (dtype == HAP_BF16)
-    launch_k(p2p_reduce_scatter_direct_kernel<__nv_bfloat16>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank,
-             s->nranks, reinterpret_cast<const __nv_bfloat16* const*>(dev_sends), static_cast<__nv_bfloat16*>(recv),
+    launch_p2p(p2p_reduce_scatter_direct_kernel<__nv_bfloat16>, grid, st, peers, s->rank, s->nranks, reinterpret_cast<const __nv_bfloat16* const*>(dev_sends), static_cast<__nv_bfloat16*>(recv),
              outer, inner, extent, dev_sizes, dev_offsets);
   else
-    launch_k(p2p_reduce_scatter_direct_kernel<float>, dim3(grid), dim3(kThreads), 0, st, peers, s->rank, s->nranks,
+    launch_p2p(p2p_reduce_scatter_direct_kernel<float>, grid, st, peers, s->rank, s->nranks,
              reinterpret_cast<const float* const*>(dev_sends), static_cast<float*>(recv), outer, inner, extent,
              dev_sizes, dev_offsets);
   return launch_status("p2p direct reduce-scatter");
@@ -677,4 +828,59 @@ extern "C" hap_status hap_p2p_reduce_scatter_v(void* ctx, const void* send, void
                                      dev_sizes, dev_offsets, bytes, sm_cap, st);
   return p2p_launch<float>(p2p_reduce_scatter_kernel<float>, s, send, recv, outer, inner, extent, dev_sizes,
                            dev_offsets, bytes, sm_cap, st);
+}
+
+extern "C" hap_status hap_symm_open_local(void* ctx, const int64_t* peer_bases) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && peer_bases, "hap_symm_open_local: bad arguments");
+  for (int p = 0; p < s->nranks; ++p) {
+    HAP_CHECK_ARG(peer_bases[p] != 0, "hap_symm_open_local: null peer arena");
+    s->peers[p] = reinterpret_cast<char*>(static_cast<uintptr_t>(peer_bases[p]));
+  }
+  HAP_CHECK_ARG(s->peers[s->rank] == s->local, "hap_symm_open_local: own entry is not this context's arena");
+  s->local_open = true;
+  return HAP_OK;
+}
+
+extern "C" void* hap_symm_local_base(void* ctx) {
+  auto* s = static_cast<Symm*>(ctx);
+  return s ? s->local : nullptr;
+}
+
+extern "C" hap_status hap_p2p_all_reduce(void* ctx, const void* const* dev_ins, void* const* dev_outs, hap_dtype dtype,
+                                         int64_t count, int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_ins && dev_outs && count >= 0, "hap_p2p_all_reduce: bad arguments");
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  // bytes this rank moves: its chunk from every peer and to every peer
+  const int grid = p2p_grid(2 * count * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    launch_p2p(p2p_all_reduce_kernel<__nv_bfloat16>, grid, st, peers, s->rank, s->nranks,
+               reinterpret_cast<const __nv_bfloat16* const*>(dev_ins), reinterpret_cast<__nv_bfloat16* const*>(dev_outs),
+               count);
+  else
+    launch_p2p(p2p_all_reduce_kernel<float>, grid, st, peers, s->rank, s->nranks,
+               reinterpret_cast<const float* const*>(dev_ins), reinterpret_cast<float* const*>(dev_outs), count);
+  return launch_status("p2p all-reduce");
+}
+
+extern "C" hap_status hap_p2p_all_to_all(void* ctx, const void* send, void* const* dev_recvs, hap_dtype dtype,
+                                         const int64_t* dev_send_off, const int64_t* dev_counts,
+                                         const int64_t* dev_dst_off, int64_t max_elems, int sm_cap, void* stream) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && dev_recvs && dev_send_off && dev_counts && dev_dst_off, "hap_p2p_all_to_all: bad arguments");
+  Peers peers{};
+  for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
+  const int grid = p2p_grid(max_elems * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (dtype == HAP_BF16)
+    launch_p2p(p2p_all_to_all_kernel<__nv_bfloat16>, grid, st, peers, s->rank, s->nranks,
+               static_cast<const __nv_bfloat16*>(send), reinterpret_cast<__nv_bfloat16* const*>(dev_recvs), dev_send_off,
+               dev_counts, dev_dst_off);
+  else
+    launch_p2p(p2p_all_to_all_kernel<float>, grid, st, peers, s->rank, s->nranks, static_cast<const float*>(send),
+               reinterpret_cast<float* const*>(dev_recvs), dev_send_off, dev_counts, dev_dst_off);
+  return launch_status("p2p all-to-all");
 }

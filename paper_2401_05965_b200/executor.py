@@ -74,23 +74,38 @@ def _view(shape: tuple, axis: int) -> tuple[int, int, int]:
 class LocalGroup:
     """All m program devices emulated on the current GPU (lock step)."""
 
+    distributed = False
+
     def __init__(self, m: int):
         self.m = m
         self.rank = 0
         self.local_ranks = list(range(m))
         self.comm = None
+        self.comm_grad = None
 
     def close(self):
         pass
 
 
+def _dist_exchange(obj) -> list:
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
 class NcclGroup:
-    """One program device per process; collectives over NCCL (C ABI).
+    """One program device per process; collectives over NCCL (C ABI) or the
+    hand-written NVLink kernels, whichever the cost model picks per call site.
 
     Two communicators: ``comm`` carries the program's collectives on the
     compute stream, ``comm_grad`` the parameter-gradient all-reduces on a side
     stream that overlaps the rest of the backward pass (NCCL operations on
     one communicator must not run concurrently from two streams)."""
+
+    distributed = True
+    in_process = False
 
     def __init__(self, rank: int, m: int, comm_handle, grad_handle=None):
         self.m = m
@@ -119,12 +134,99 @@ class NcclGroup:
         rank, world = dist.get_rank(), dist.get_world_size()
         return cls(rank, world, cls._init_comm(rank, world), cls._init_comm(rank, world))
 
+    def exchange(self, obj) -> list:
+        """Every rank's ``obj``, rank-ordered (host-side, compile time only)."""
+        return _dist_exchange(obj)
+
     def close(self):
         for name in ("comm", "comm_grad"):
             handle = getattr(self, name)
             if handle is not None:
                 check(_lib.lib().hap_comm_destroy(handle), "hap_comm_destroy")
                 setattr(self, name, None)
+
+
+class PeerGroup:
+    """One program device per executor whose collectives are ONLY the
+    hand-written NVLink peer-memory kernels (p2p.cu: push all-gather, direct
+    reduce-scatter, two-shot all-reduce, push all-to-all) — no NCCL.
+
+    Two forms: one process per GPU (``from_torch_distributed``: buffers are
+    exchanged as CUDA IPC handles over any torch.distributed backend), or all
+    ranks inside ONE process (``thread_peer_groups``: each rank an Executor on
+    its own stream, built and stepped in its own thread, buffers exchanged as
+    plain device pointers — ``hap_symm_open_local``).  The in-process form
+    runs the multi-device path on a single GPU, ranks side by side under SM
+    caps, which is how the 1-GPU test box verifies it."""
+
+    distributed = True
+    comm = None
+    comm_grad = None
+
+    def __init__(self, rank: int, m: int, exchange=None):
+        self.m = m
+        self.rank = rank
+        self.local_ranks = [rank]
+        self._exchange = exchange
+        self.in_process = exchange is not None
+
+    @classmethod
+    def from_torch_distributed(cls) -> "PeerGroup":
+        import torch.distributed as dist
+
+        return cls(dist.get_rank(), dist.get_world_size())
+
+    def exchange(self, obj) -> list:
+        if self._exchange is not None:
+            return self._exchange(self.rank, obj)
+        return _dist_exchange(obj)
+
+    def close(self):
+        pass
+
+
+def thread_peer_groups(m: int, timeout: float = 120.0) -> list:
+    """m PeerGroups of one process whose exchange is an in-process rendezvous
+    (a barrier across the m threads that build the m executors)."""
+    import threading
+
+    barrier = threading.Barrier(m, timeout=timeout)
+    slots: list = [None] * m
+
+    def exchange(rank: int, obj):
+        slots[rank] = obj
+        barrier.wait()
+        out = list(slots)
+        barrier.wait()
+        return out
+
+    return [PeerGroup(r, m, exchange=exchange) for r in range(m)]
+
+
+def run_ranks(fns: list) -> list:
+    """Run fns[r]() for every rank in its own thread (ctypes calls release the
+    GIL, so the ranks enqueue concurrently and a rank's peer-memory kernel
+    never waits on a host thread that is blocked behind it); re-raises the
+    first failure."""
+    import threading
+
+    out: list = [None] * len(fns)
+    err: list = []
+
+    def body(r):
+        try:
+            out[r] = fns[r]()
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            err.append(exc)
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(len(fns))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if err:
+        raise err[0]
+    return out
 
 
 # ---------------------------------------------------------------------------- config
@@ -551,8 +653,11 @@ class Executor:
         r = g.rank
         s = src[r]
         target = dst[r] if (not accumulate and dst[r].dtype == s.dtype) else self._new(s.shape, s.dtype)
-        self._emit("hap_all_reduce", self._comm(), s.ptr, target.ptr, s.numel if s.shape else 1, s.dtype,
-                   self._sptr(), kernel=False)
+        n = s.numel if s.shape else 1
+        if self._use_p2p("all_reduce", n * (2 if s.dtype == BF16 else 4)):
+            self._p2p_all_reduce(s, target, n)
+        else:
+            self._emit("hap_all_reduce", self._comm(), s.ptr, target.ptr, n, s.dtype, self._sptr(), kernel=False)
         if target is not dst[r]:
             self._copy(target, dst[r], self.caps[r], accumulate=accumulate)
 
@@ -574,7 +679,7 @@ class Executor:
         outer, _, inner = _view(full_shape, axis)
         counts = [sz * outer * inner for sz in sizes]
         s = src[r]
-        if kind == "all_gather" and self.cfg.gather in ("auto", "kernel"):
+        if self._use_p2p(kind, sum(counts) * (2 if s.dtype == BF16 else 4)):
             # hand-written NVLink kernel: exact chunks, placed in the final layout
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(full_shape, s.dtype)
@@ -625,7 +730,7 @@ class Executor:
         r = g.rank
         s = src[r]
         counts = [sz * outer * inner for sz in sizes]
-        if self.cfg.gather in ("auto", "kernel"):
+        if self._use_p2p("reduce_scatter", sum(counts) * (2 if s.dtype == BF16 else 4)):
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(dst[r].shape, s.dtype)
             if self.cfg.p2p_push:   # read the peers' partials in place (registered)
@@ -688,17 +793,52 @@ class Executor:
         recv_shapes = [tuple(sizes1[k] if a == d1 else e for a, e in enumerate(dst[r].shape)) for k in range(self.m)]
         recv_counts = [int(math.prod(sh)) for sh in recv_shapes]
         recv = self._new((max(1, sum(recv_counts)),), s.dtype)
-        sarr, rarr = _lib.i64_array(send_counts), _lib.i64_array(recv_counts)
-        self._keep(sarr)
-        self._keep(rarr)
-        self._emit("hap_all_to_all_v", self._comm(), send.ptr, sarr, recv.ptr, rarr, s.dtype, self._sptr(),
-                   kernel=False)
+        if self._use_p2p("all_to_all", max(sum(send_counts), sum(recv_counts)) * (2 if s.dtype == BF16 else 4)):
+            # rank j's chunk for rank k lands at k's receive offset sum_{i<j} count(i -> k)
+            def count(j, k):
+                return int(math.prod(tuple(sizes2[k] if a == d2 else e for a, e in enumerate(src_shapes[j]))))
+            dst_off = [sum(count(i, k) for i in range(r)) for k in range(self.m)]
+            self._p2p_all_to_all(send, recv, soff[:-1], send_counts, dst_off)
+        else:
+            sarr, rarr = _lib.i64_array(send_counts), _lib.i64_array(recv_counts)
+            self._keep(sarr)
+            self._keep(rarr)
+            self._emit("hap_all_to_all_v", self._comm(), send.ptr, sarr, recv.ptr, rarr, s.dtype, self._sptr(),
+                       kernel=False)
         roff = offsets(recv_counts)
         for k in range(self.m):
             if recv_counts[k]:
                 chunk = Buf(recv.tensor[roff[k]:roff[k + 1]], s.dtype, recv_shapes[k])
                 self._block(chunk, _view(recv_shapes[k], d1), 0, dst[r], _view(dst[r].shape, d1), off1[k],
                             sizes1[k], self.caps[r], accumulate)
+
+    def _use_p2p(self, kind: str, nbytes: int) -> bool:
+        """Hand-written NVLink kernel (True) or NCCL (False) for one call site.
+        A PeerGroup has only the kernels; ``gather`` forces one side;
+        "auto" takes the kernels for the all-gathers and reduce-scatters
+        (exact uneven chunks in their final layout, no pack / unpack) and
+        NCCL for all-reduce and all-to-all."""
+        g = self.group
+        if g.comm is None:
+            return True
+        if self.cfg.gather == "kernel":
+            return True
+        if self.cfg.gather in ("padded", "sendrecv", "nccl"):
+            return False
+        return kind in ("all_gather", "grouped_broadcast", "reduce_scatter")
+
+    def _p2p_tag(self) -> str:
+        # one context (staging arena + flag epochs) per stream: calls on one
+        # stream are ordered, calls on two streams must not share flags
+        return "side" if self._emit_on is not None else "main"
+
+    def _register(self, tag: str, buf: Buf) -> dict:
+        """A buffer every peer maps (push outputs, in-place partials): the
+        device array of all ranks' pointers to it is filled in by
+        _register_outputs once compilation is done."""
+        reg: dict = {}
+        self._p2p_regs.append((tag, buf, reg))
+        return reg
 
     def _p2p(self, fn: str, send: Buf, recv: Buf, outer: int, inner: int, extent: int, sizes: list,
              arena_bytes: int):
@@ -707,23 +847,19 @@ class Executor:
         r = self.group.rank
         dev = torch.tensor([list(sizes), offsets(sizes)[:-1]], dtype=torch.int64, device=self.device)
         self._keep(dev)
-        # one context (staging arena + flag epochs) per stream: calls on one
-        # stream are ordered, calls on two streams must not share staging
-        tag = "side" if self._emit_on is not None else "main"
+        tag = self._p2p_tag()
         self._p2p_bytes[tag] = max(self._p2p_bytes.get(tag, 0), arena_bytes)
         fn_ptr = getattr(self.lib, fn)
         stream = self._sptr()
         cap = self.caps[r]
         sizes_ptr, offs_ptr = dev[0].data_ptr(), dev[1].data_ptr()
         if fn == "hap_p2p_all_gather_push":
-            reg: dict = {}
-            self._p2p_regs.append((tag, recv, reg))
+            reg = self._register(tag, recv)
             total = outer * extent * inner
             args = lambda: (self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype, outer, inner,  # noqa: E731
                             extent, sizes_ptr, offs_ptr, total, cap, stream)
         elif fn == "hap_p2p_reduce_scatter_direct":
-            reg = {}
-            self._p2p_regs.append((tag, send, reg))
+            reg = self._register(tag, send)
             mine = outer * sizes[r] * inner
             args = lambda: (self._symm[tag], reg["dev"].data_ptr(), recv.ptr, send.dtype, outer, inner,  # noqa: E731
                             extent, sizes_ptr, offs_ptr, mine, cap, stream)
@@ -736,33 +872,66 @@ class Executor:
                             sizes_ptr, offs_ptr, cap, stream)
         self._ops.append(Op(lambda: fn_ptr(*args()), (), fn, True))
 
+    def _p2p_all_reduce(self, src: Buf, dst: Buf, n: int, stream_ptr=None):
+        """Two-shot all-reduce kernel over registered buffers (src may be dst)."""
+        tag = self._p2p_tag() if stream_ptr is None else "side"
+        self._p2p_bytes[tag] = max(self._p2p_bytes.get(tag, 0), 16)
+        reg_in = self._register(tag, src)
+        reg_out = reg_in if dst is src else self._register(tag, dst)
+        fn = self.lib.hap_p2p_all_reduce
+        stream = stream_ptr if stream_ptr is not None else self._sptr()
+        cap = self.caps[self.group.rank]
+        dt = src.dtype
+        self._ops.append(Op(lambda: fn(self._symm[tag], reg_in["dev"].data_ptr(), reg_out["dev"].data_ptr(), dt, n,
+                                       cap, stream), (), "hap_p2p_all_reduce", True))
+
+    def _p2p_all_to_all(self, send: Buf, recv: Buf, send_off: list, counts: list, dst_off: list):
+        tag = self._p2p_tag()
+        self._p2p_bytes[tag] = max(self._p2p_bytes.get(tag, 0), 16)
+        reg = self._register(tag, recv)
+        dev = torch.tensor([list(send_off), list(counts), list(dst_off)], dtype=torch.int64, device=self.device)
+        self._keep(dev)
+        fn = self.lib.hap_p2p_all_to_all
+        stream = self._sptr()
+        cap = self.caps[self.group.rank]
+        most = max(max(counts), 1)
+        self._ops.append(Op(lambda: fn(self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype,
+                                       dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), most, cap, stream),
+                            (), "hap_p2p_all_to_all", True))
+
     def _create_symm(self):
         if not self._p2p_bytes:
             return
-        import torch.distributed as dist
-
         g = self.group
         for tag in sorted(self._p2p_bytes):   # same order on every rank
             ctx = ctypes.c_void_p()
             check(self.lib.hap_symm_create(ctypes.byref(ctx), int(self._p2p_bytes[tag]), g.rank, g.m),
                   "hap_symm_create")
-            handle = ctypes.create_string_buffer(64)
-            check(self.lib.hap_symm_handle(ctx, handle), "hap_symm_handle")
-            handles = [None] * g.m
-            dist.all_gather_object(handles, bytes(handle.raw))
-            check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
             self._symm[tag] = ctx
+            if getattr(g, "in_process", False):
+                bases = g.exchange(int(self.lib.hap_symm_local_base(ctx) or 0))
+                check(self.lib.hap_symm_open_local(ctx, _lib.i64_array(bases)), "hap_symm_open_local")
+            else:
+                handle = ctypes.create_string_buffer(64)
+                check(self.lib.hap_symm_handle(ctx, handle), "hap_symm_handle")
+                handles = g.exchange(bytes(handle.raw))
+                check(self.lib.hap_symm_open(ctx, b"".join(handles)), "hap_symm_open")
         self._register_outputs()
 
     def _register_outputs(self):
-        """Map every registered buffer (push all-gather outputs, direct
-        reduce-scatter partials) into every peer: one exchange of (IPC
-        handle, allocation base, offset) triples for all of them."""
+        """Map every registered buffer (push outputs, in-place partials,
+        all-reduce operands) into every peer: one exchange for all of them —
+        (IPC handle, allocation base, offset) triples across processes, plain
+        device pointers inside one process."""
         if not self._p2p_regs:
             return
-        import torch.distributed as dist
-
         g = self.group
+        if getattr(g, "in_process", False):
+            everyone = g.exchange([buf.ptr for _, buf, _ in self._p2p_regs])
+            for i, (_, _, reg) in enumerate(self._p2p_regs):
+                reg["dev"] = torch.tensor([everyone[p][i] for p in range(g.m)], dtype=torch.int64, device=self.device)
+                self._keep(reg["dev"])
+            return
         mine = []
         for tag, buf, _ in self._p2p_regs:
             h = ctypes.create_string_buffer(64)
@@ -770,8 +939,7 @@ class Executor:
             check(self.lib.hap_p2p_buffer_handle(self._symm[tag], buf.ptr, h, ctypes.byref(base), ctypes.byref(off)),
                   "hap_p2p_buffer_handle")
             mine.append((bytes(h.raw), base.value, off.value))
-        everyone = [None] * g.m
-        dist.all_gather_object(everyone, mine)
+        everyone = g.exchange(mine)
         for i, (tag, buf, reg) in enumerate(self._p2p_regs):
             handles = b"".join(everyone[p][i][0] for p in range(g.m))
             bases = _lib.i64_array([everyone[p][i][1] for p in range(g.m)])
@@ -1512,8 +1680,8 @@ class Executor:
         return price_grad_sync(spec, self.cfg.ratios, pins.ref, kdim, ndim, use_rows)
 
     def _sfb_overlap(self) -> bool:
-        return bool(self.sfb) and isinstance(self.group, NcclGroup) and self.cfg.overlap_sfb \
-            and self.group.comm_grad is not None
+        g = self.group
+        return bool(self.sfb) and g.distributed and self.cfg.overlap_sfb and (g.comm_grad is not None or g.comm is None)
 
     def _sfb_factor(self, did: str, bufs: dict) -> dict:
         """Row-gathered copy of an SFB factor (an activation or an output
@@ -1590,7 +1758,7 @@ class Executor:
         neighbouring gradients sync as one bucket (one large all-reduce runs
         at NCCL's bandwidth; dozens of small ones pay its latency each)."""
         g = self.group
-        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None:
+        if not g.distributed or self.m == 1 or (g.comm_grad is None and g.comm is not None):
             return
         first_use: dict = {}
         for i, ins in enumerate(self.program.instrs):
@@ -1621,7 +1789,8 @@ class Executor:
         the remaining backward kernels; the compute stream joins the side
         stream before the update."""
         g = self.group
-        if not isinstance(g, NcclGroup) or self.m == 1 or g.comm_grad is None or not hasattr(self, "_flat"):
+        if not g.distributed or self.m == 1 or (g.comm_grad is None and g.comm is not None) \
+                or not hasattr(self, "_flat"):
             return
         flat, place = self._flat
         ready = {f.output: self._grad_ready_at[f.output] for f in self._synced_params()
@@ -1653,9 +1822,16 @@ class Executor:
             self._keep(ev)
             ptr = flat.data_ptr() + lo * 4
             inserted = [Op(ev.record, (self.stream,), "event.record", False),
-                        Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False),
-                        Op(self.lib.hap_all_reduce, (g.comm_grad, ptr, ptr, hi - lo, F32,
-                                                     self.comm_stream.cuda_stream), "hap_all_reduce", False)]
+                        Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False)]
+            if g.comm_grad is not None:
+                inserted.append(Op(self.lib.hap_all_reduce, (g.comm_grad, ptr, ptr, hi - lo, F32,
+                                                             self.comm_stream.cuda_stream), "hap_all_reduce", False))
+            else:   # in place on the registered bucket, P2P kernel on the side stream
+                saved, self._ops = self._ops, []
+                bucket = Buf(flat.narrow(0, lo, hi - lo), F32, (hi - lo,))
+                self._p2p_all_reduce(bucket, bucket, hi - lo, stream_ptr=self.comm_stream.cuda_stream)
+                inserted += self._ops
+                self._ops = saved
             ops[pos:pos] = inserted
             self.overlapped.update(members)
         done = torch.cuda.Event()
@@ -1912,6 +2088,20 @@ class Executor:
         self.graph = g
         return g
 
+    _COLLECTIVE_OPS = ("hap_all_reduce", "hap_all_gather_v", "hap_grouped_broadcast", "hap_reduce_scatter_v",
+                       "hap_all_to_all_v", "hap_p2p_all_gather_push", "hap_p2p_all_gather_v",
+                       "hap_p2p_reduce_scatter_direct", "hap_p2p_reduce_scatter_v", "hap_p2p_all_reduce",
+                       "hap_p2p_all_to_all")
+
+    def collective_impls(self) -> dict:
+        """Collective launches per step by implementation (NCCL calls vs the
+        NVLink peer-memory kernels)."""
+        out: dict = {}
+        for op in self.ops_fwd + self.ops_bwd + self.ops_upd:
+            if op.what in self._COLLECTIVE_OPS:
+                out[op.what] = out.get(op.what, 0) + 1
+        return dict(sorted(out.items()))
+
     def kernel_launches(self, phase: str = "step") -> int:
         ops = {"forward": self.ops_fwd, "backward": self.ops_bwd + self.ops_upd,
                "step": self.ops_fwd + self.ops_bwd + self.ops_upd}[phase]
@@ -1921,12 +2111,8 @@ class Executor:
         """Per-device loss values of the last forward (host sync)."""
         self.stream.synchronize()
         vals = {r: float(self.loss_buf[r].tensor[0].item()) for r in self.group.local_ranks}
-        if isinstance(self.group, NcclGroup):
-            import torch.distributed as dist
-
-            out = [None] * self.m
-            dist.all_gather_object(out, vals[self.group.rank])
-            return [float(v) for v in out]
+        if self.group.distributed:
+            return [float(v) for v in self.group.exchange(vals[self.group.rank])]
         return [vals[r] for r in range(self.m)]
 
     def tensor(self, did: str, r: int) -> torch.Tensor:

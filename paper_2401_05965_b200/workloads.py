@@ -218,3 +218,36 @@ def synthetic_inputs(g: Graph, seed: int, scaled: bool = True) -> dict:
                     value = value / np.sqrt(2 * depth)
             out[node.id] = value
     return out
+
+
+
+def planned_program(g: Graph, m: int, plan_doc: dict):
+    """(program, shard table, ratio row) for ``m`` equal devices from a plan
+    document the reference planner emitted for the same graph family (same
+    node ids) at another device count.
+
+    The planner emits the SAME program for these skeletons at every device
+    count: the data-parallel program (token rows ``@shard0``, weights
+    ``@full``, ``loss@partial``) — checked by tests/test_workloads.py for the
+    2-layer BERT and BERT-MoE skeletons at m = 1, 2, 4 and for the 12-layer
+    bench plans at m = 2, 4, 8.  At m = 1 every sharding choice ties, so its
+    A* search grows ~3.6x per layer (1.2 / 6.9 / 24.7 s for 1 / 2 / 3 BERT
+    layers) and the 12-layer m = 1 plan does not finish; bench.py's N = 1
+    line therefore takes the program of the N = 2 plan, re-targeted to one
+    device (its shard table: the whole token axis)."""
+    from .program import DistributedProgram
+
+    prog = DistributedProgram.from_json(plan_doc["program"])
+    ids = {n.id for n in g.nodes}
+    missing = sorted({ins.ref for ins in prog.instrs} - ids)
+    if missing:
+        raise ValueError(f"plan does not belong to this graph: unknown tensors {missing[:5]}")
+    table = {}
+    for ins in prog.instrs:
+        for did in (ins.output,) + tuple(ins.operands):
+            ref, _, form = did.partition("@")
+            if form.startswith("shard"):
+                axis = int(form[len("shard"):])
+                extent = g.producer(ref).shape[axis]
+                table[(ref, axis)] = [extent // m + (1 if j < extent % m else 0) for j in range(m)]
+    return prog, table, tuple(1.0 / m for _ in range(m))

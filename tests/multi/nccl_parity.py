@@ -10,33 +10,17 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import goldens  # noqa: E402
 from oracle import interpreter_np as O  # noqa: E402
+from parity_common import cases, check  # noqa: E402
 from paper_2401_05965_b200.executor import ExecConfig, Executor, NcclGroup  # noqa: E402
 from paper_2401_05965_b200.program import DistributedProgram  # noqa: E402
 from paper_2401_05965_b200.sharding import table_from_plan  # noqa: E402
-
-RTOL = {"bf16": 2e-2, "fp32": 1e-3}
-
-
-def cases(world):
-    out = []
-    for gname, cname in goldens.value_cases():
-        doc = goldens.plan(gname, cname)
-        if doc["devices"] == world:
-            vals = goldens.values(gname, cname)
-            out.append((f"{gname}.{cname}", doc, gname, goldens.inputs(goldens.graph(gname), vals, goldens.seeds(vals)[0])))
-    for stem in goldens.program_cases():
-        doc, vals, gname = goldens.program_case(stem)
-        if doc["devices"] == world:
-            inputs = {k.split(":", 2)[2]: vals[k] for k in vals.files if k.startswith("seed0:input:")}
-            out.append((stem, doc, gname, inputs))
-    return out
 
 
 def main():
@@ -55,7 +39,7 @@ def main():
         # Gradient sync: all-reduce for every gather implementation, plus
         # sufficient-factor broadcasting through the P2P and send/recv gathers.
         variants = [(g_, "all_reduce") for g_ in ("kernel", "padded", "sendrecv")]
-        variants += [("kernel", "sfb"), ("sendrecv", "sfb")]
+        variants += [("kernel", "sfb"), ("sendrecv", "sfb"), ("auto", "all_reduce")]
         if os.environ.get("HAP_PARITY_VARIANTS"):
             variants = [tuple(v.split(":")) for v in os.environ["HAP_PARITY_VARIANTS"].split(",")]
         overlap = os.environ.get("HAP_PARITY_OVERLAP", "1") == "1"
@@ -69,31 +53,10 @@ def main():
                 ex.step()
                 torch.cuda.synchronize()
                 losses = ex.losses()
-                env, want = O.run_distributed(program, m, inputs, table, precision=dtype)
-                _, sg, _ = O.train_step(program, m, inputs, table, {n.id: n.shape for n in g.nodes},
-                                        precision=dtype)
-                scale = max(1.0, abs(float(want[0])))
-                for ins in program.instrs:
-                    if ins.ref == program.loss and ins.kind == "reduce":
-                        scale = max(scale, float(np.sqrt(sum(np.sum(np.square(v)) for v in env[ins.operands[0]]))))
-                if any(abs(a - float(b)) > RTOL[dtype] * scale for a, b in zip(losses, want)):
-                    failures.append(f"{name} {dtype} {gather} {sync}: losses {losses} vs {[float(v) for v in want]}")
-                for ref, value in sg.items():
-                    for r, forms in ex.gradient(ref).items():
-                        for did, grad in forms:
-                            grad = grad.float().cpu().numpy()
-                            if "@shard" in did:
-                                axis = int(did.rsplit("shard", 1)[1])
-                                sizes = table[(ref, axis)]
-                                off = int(np.sum(sizes[:r]))
-                                value_r = np.take(value, np.arange(off, off + sizes[r]), axis=axis)
-                            else:
-                                value_r = value
-                            if value_r.size == 0:
-                                continue
-                            err = float(np.max(np.abs(grad - value_r))) / max(float(np.max(np.abs(value))), 1e-3)
-                            if err > RTOL[dtype]:
-                                failures.append(f"{name} {dtype} {gather} {sync}: grad {did}@{r} rel err {err:.3g}")
+                grads = {ref: {r: [(did, t.float().cpu().numpy()) for did, t in forms]
+                               for r, forms in ex.gradient(ref).items()}
+                         for ref in {ins.ref for ins in program.instrs if ins.kind.startswith(("parameter", "placeholder"))}}
+                failures += check(f"{name} {dtype} {gather} {sync}", doc, gname, inputs, dtype, losses, grads)
                 ex.group = None  # the communicator is shared across executors
     fl = [None] * world
     dist.all_gather_object(fl, failures)

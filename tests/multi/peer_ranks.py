@@ -1,0 +1,126 @@
+"""The multi-device path on ONE GPU: every golden program for 2 and 3
+devices (the reference planner's plans and the enumerated programs with
+collectives) executed by m program ranks inside one process — each rank an
+Executor on its own stream, SM cap 148 // m, built and stepped in its own
+thread — whose collectives are only the hand-written NVLink peer-memory
+kernels (PeerGroup, in-process form): push all-gather, direct reduce-scatter,
+two-shot all-reduce, push all-to-all, the SFB factor gathers on the side
+stream and the bucketed gradient all-reduce.  Checked against the CPU oracle
+(parity_common.check), and in fp32 against the single-executor LocalGroup run
+of the same program bit for bit (the peer kernels sum in rank order, as the
+LocalGroup does).  Run by tests/test_gpu_peer_ranks.py in a subprocess with a
+timeout:
+
+    python tests/multi/peer_ranks.py [substring] [--world 2,3] [--variants all_reduce,sfb]
+"""
+import argparse
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import goldens  # noqa: E402
+from oracle import interpreter_np as O  # noqa: E402
+from parity_common import cases, check  # noqa: E402
+from paper_2401_05965_b200.executor import (ExecConfig, Executor, LocalGroup, run_ranks,  # noqa: E402
+                                            thread_peer_groups)
+from paper_2401_05965_b200.program import DistributedProgram  # noqa: E402
+from paper_2401_05965_b200.sharding import table_from_plan  # noqa: E402
+
+
+def grads_of(exs, program):
+    refs = {ins.ref for ins in program.instrs if ins.kind.startswith(("parameter", "placeholder"))}
+    out = {}
+    for ref in refs:
+        per = {}
+        for ex in exs:
+            for r, forms in ex.gradient(ref).items():
+                per[r] = [(did, t.float().cpu().numpy()) for did, t in forms]
+        out[ref] = per
+    return out
+
+
+def run_peer(doc, shapes, inputs, dtype, sync, capture):
+    prog = DistributedProgram.from_json(doc["program"])
+    m = int(doc["devices"])
+    table = table_from_plan(doc)
+    caps = [148 // m] * m
+    groups = thread_peer_groups(m)
+    exs = run_ranks([lambda r=r: Executor(prog, m, table, shapes, group=groups[r],
+                                          config=ExecConfig(dtype=dtype, sm_caps=caps, input_grads=True,
+                                                            grad_sync=sync))
+                     for r in range(m)])
+    run_ranks([lambda ex=ex: ex.load(inputs) for ex in exs])
+    if capture:
+        run_ranks([lambda ex=ex: ex.capture() for ex in exs])
+        run_ranks([lambda ex=ex: ex.load(inputs) for ex in exs])
+    run_ranks([lambda ex=ex: ex.step() for ex in exs])
+    torch.cuda.synchronize()
+    losses = run_ranks([lambda ex=ex: ex.losses() for ex in exs])[0]
+    return exs, losses
+
+
+def run_local(doc, shapes, inputs, dtype, sync):
+    m = int(doc["devices"])
+    ex = Executor(DistributedProgram.from_json(doc["program"]), m, table_from_plan(doc), shapes, group=LocalGroup(m),
+                  config=ExecConfig(dtype=dtype, sm_caps=[148 // m] * m, input_grads=True, grad_sync=sync))
+    ex.load(inputs)
+    ex.step()
+    torch.cuda.synchronize()
+    return ex, ex.losses()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("only", nargs="?")
+    ap.add_argument("--world", default="2,3")
+    ap.add_argument("--variants", default="all_reduce,sfb")
+    ap.add_argument("--dtypes", default="fp32,bf16")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    failures, count, bit_equal, bit_total = [], 0, 0, 0
+    for world in [int(w) for w in args.world.split(",")]:
+        for name, doc, gname, inputs in cases(world):
+            if args.only and args.only not in name:
+                continue
+            g = goldens.graph(gname)
+            shapes = {n.id: n.shape for n in g.sources()}
+            program, _, _ = O.load_plan(doc)
+            for dtype in args.dtypes.split(","):
+                for sync in args.variants.split(","):
+                    count += 1
+                    label = f"{name} {dtype} {sync}"
+                    capture = count % 5 == 0   # every fifth run replays a captured CUDA graph per rank
+                    try:
+                        exs, losses = run_peer(doc, shapes, inputs, dtype, sync, capture)
+                    except Exception as exc:  # noqa: BLE001 - reported as a failure
+                        failures.append(f"{label}: {type(exc).__name__}: {exc}")
+                        continue
+                    grads = grads_of(exs, program)
+                    failures += check(label + (" graph" if capture else ""), doc, gname, inputs, dtype, losses, grads)
+                    if dtype == "fp32":
+                        lex, llosses = run_local(doc, shapes, inputs, dtype, sync)
+                        lgrads = grads_of([lex], program)
+                        same = list(losses) == list(llosses) and all(
+                            all(np.array_equal(a[1], b[1]) for a, b in zip(grads[ref][r], lgrads[ref][r]))
+                            for ref in grads for r in grads[ref])
+                        bit_total += 1
+                        bit_equal += int(same)
+                        lex.close()
+                    for ex in exs:
+                        ex.close()
+    print(f"peer ranks parity: {count} runs, {len(failures)} failures; fp32 bit-identical to LocalGroup "
+          f"in {bit_equal}/{bit_total}")
+    for f in failures[:40]:
+        print("  FAIL", f)
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -109,6 +109,7 @@ def test_split_k_fp32_accumulate_is_ordered(splits, pair):
         for o in outs[1:]:
             assert torch.equal(o, outs[0])
         s = torch.cuda.Stream()
+        check(L.hap_matmul_batch(d, 1, 0, BF16, F32, 0, s.cuda_stream))   # eager first: the stream's workspace
         c.copy_(base)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()

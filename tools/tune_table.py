@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 def main() -> None:
     import torch
 
-    from paper_2401_05965_b200 import _lib, api, workloads
+    from paper_2401_05965_b200 import _lib, workloads
     from paper_2401_05965_b200.cost_model import ClusterSpec
     from paper_2401_05965_b200.executor import ExecConfig, Executor, LocalGroup
     from paper_2401_05965_b200.graph_ir import graph_from_dict
@@ -51,11 +51,12 @@ def main() -> None:
                 workloads.bert(layers=12, batch=batch, seq=128)
             caps = workloads.sm_caps(n)
             shapes = {nd.id: nd.shape for nd in g.sources()}
+            k = max(n, 2)
+            with open(os.path.join(plans, f"{stem[wl]}_b{per_gpu[wl] * k}.b200x{k}.json")) as fh:
+                doc = json.load(fh)
             if n == 1:
-                prog, table, ratios = workloads.planned_program(g, 1)
+                prog, table, ratios = workloads.planned_program(g, 1, doc)
             else:
-                with open(os.path.join(plans, f"{stem[wl]}_b{batch}.b200x{n}.json")) as fh:
-                    doc = json.load(fh)
                 prog, table, ratios = (DistributedProgram.from_json(doc["program"]), table_from_plan(doc),
                                        tuple(doc["ratios"][0]))
             cluster = ClusterSpec.from_dict(workloads.cluster_doc(caps))
@@ -80,7 +81,6 @@ def main() -> None:
     with open(args.out, "w") as fh:
         fh.write(text)
     print(f"wrote {args.out}: {text.count(chr(10))} signatures ({total} timed)")
-    _ = api
 
 
 if __name__ == "__main__":
