@@ -229,6 +229,25 @@ def run_ranks(fns: list) -> list:
     return out
 
 
+class _HostStream:
+    """Stand-in for a CUDA stream when the executor only COMPILES on the host
+    (device "cpu": the dry-run form used by the CPU tests to check the
+    per-rank collective planning without a GPU).  Never runs a kernel."""
+
+    cuda_stream = 0
+
+    def synchronize(self):
+        pass
+
+    def wait_event(self, _event):
+        pass
+
+
+class _HostEvent:
+    def record(self, _stream=None):
+        pass
+
+
 # ---------------------------------------------------------------------------- config
 
 @dataclass
@@ -281,6 +300,7 @@ class Op:
     what: str
     kernel: bool = True               # launches one of our kernels (vs NCCL / memcpy)
     gemm: dict | None = None          # matmul record (for launch batching)
+    meta: dict | None = None          # peer-memory collectives: what the launch moves (buffers, sizes)
 
 
 # ---------------------------------------------------------------------------- executor
@@ -328,7 +348,10 @@ class Executor:
         self.cfg = config or ExecConfig()
         self.wdt = BF16 if self.cfg.dtype == "bf16" else F32
         self.device = device or torch.device("cuda", torch.cuda.current_device())
-        self.stream = torch.cuda.Stream(self.device)
+        # device "cpu": compile only (the op list, buffers on the host) — the
+        # CPU tests' dry run of the per-rank planning; nothing can be launched
+        self.dry = self.device.type == "cpu"
+        self.stream = self._stream()
         self.caps = list(self.cfg.sm_caps) if self.cfg.sm_caps else [0] * m
         self.ops_fwd: list[Op] = []
         self.ops_bwd: list[Op] = []
@@ -374,9 +397,15 @@ class Executor:
         if self.cfg.lr and self._sgd_items and self._want_sgd_overlap():
             self._overlap_sgd()
         self.tuned_signatures = 0
-        if self.wdt == BF16:
+        if self.wdt == BF16 and not self.dry:
             self._autotune()
         self._create_symm()
+
+    def _stream(self):
+        return _HostStream() if self.dry else torch.cuda.Stream(self.device)
+
+    def _event(self):
+        return _HostEvent() if self.dry else torch.cuda.Event()
 
     def _autotune(self):
         """Tile shapes of the GEMM launches.  "table" / "time": import the
@@ -542,7 +571,7 @@ class Executor:
 
     def _side(self):
         if self.comm_stream is None:
-            self.comm_stream = torch.cuda.Stream(self.device)
+            self.comm_stream = self._stream()
         return self.comm_stream
 
     def _copy(self, src: Buf, dst: Buf, cap: int, accumulate: int = 0, alpha: float = 1.0):
@@ -870,7 +899,9 @@ class Executor:
         else:
             args = lambda: (self._symm[tag], send.ptr, recv.ptr, send.dtype, outer, inner, extent,  # noqa: E731
                             sizes_ptr, offs_ptr, cap, stream)
-        self._ops.append(Op(lambda: fn_ptr(*args()), (), fn, True))
+        self._ops.append(Op(lambda: fn_ptr(*args()), (), fn, True,
+                            meta=dict(send=send, recv=recv, outer=outer, inner=inner, extent=extent,
+                                      sizes=list(sizes))))
 
     def _p2p_all_reduce(self, src: Buf, dst: Buf, n: int, stream_ptr=None):
         """Two-shot all-reduce kernel over registered buffers (src may be dst)."""
@@ -883,7 +914,8 @@ class Executor:
         cap = self.caps[self.group.rank]
         dt = src.dtype
         self._ops.append(Op(lambda: fn(self._symm[tag], reg_in["dev"].data_ptr(), reg_out["dev"].data_ptr(), dt, n,
-                                       cap, stream), (), "hap_p2p_all_reduce", True))
+                                       cap, stream), (), "hap_p2p_all_reduce", True,
+                            meta=dict(send=src, recv=dst, n=n)))
 
     def _p2p_all_to_all(self, send: Buf, recv: Buf, send_off: list, counts: list, dst_off: list):
         tag = self._p2p_tag()
@@ -897,10 +929,12 @@ class Executor:
         most = max(max(counts), 1)
         self._ops.append(Op(lambda: fn(self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype,
                                        dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), most, cap, stream),
-                            (), "hap_p2p_all_to_all", True))
+                            (), "hap_p2p_all_to_all", True,
+                            meta=dict(send=send, recv=recv, send_off=list(send_off), counts=list(counts),
+                                      dst_off=list(dst_off))))
 
     def _create_symm(self):
-        if not self._p2p_bytes:
+        if not self._p2p_bytes or self.dry:
             return
         g = self.group
         for tag in sorted(self._p2p_bytes):   # same order on every rank
@@ -1108,7 +1142,7 @@ class Executor:
 
         def join():
             nonlocal joins
-            ev = torch.cuda.Event()
+            ev = self._event()
             self._keep(ev)
             out.append(Op(ev.record, (side,), "event.record", False))
             out.append(Op(self.stream.wait_event, (ev,), "stream.wait_event", False))
@@ -1117,10 +1151,10 @@ class Executor:
         for op in ops:
             if candidate(op):
                 if side is None:
-                    side = torch.cuda.Stream(self.device)
+                    side = self._stream()
                     self.wgrad_stream = side
                 if not prev_moved:
-                    ev = torch.cuda.Event()
+                    ev = self._event()
                     self._keep(ev)
                     out.append(Op(ev.record, (self.stream,), "event.record", False))
                     out.append(Op(side.wait_event, (ev,), "stream.wait_event", False))
@@ -1699,7 +1733,7 @@ class Executor:
         full = {r: self._new((rows,) + tuple(self.shapes[did][0][1:]), bufs[r].dtype) for r in L}
         if self._sfb_overlap():
             side = self._side()
-            ready = torch.cuda.Event()
+            ready = self._event()
             self._keep(ready)
             self._ops.append(Op(ready.record, (self.stream,), "event.record", False))
             self._ops.append(Op(side.wait_event, (ready,), "stream.wait_event", False))
@@ -1733,7 +1767,7 @@ class Executor:
         stream's gathers; consecutive, so launch batching can group them."""
         if not self._sfb_pending:
             return
-        done = torch.cuda.Event()
+        done = self._event()
         self._keep(done)
         self._ops.append(Op(done.record, (self._side(),), "event.record", False))
         self._ops.append(Op(self.stream.wait_event, (done,), "stream.wait_event", False))
@@ -1818,7 +1852,7 @@ class Executor:
             plan.append((max(ready[d] for d in members), lo, hi, members))
         self.grad_buckets = [(hi - lo) * 4 for _, lo, hi, _ in plan]
         for pos, lo, hi, members in sorted(plan, key=lambda t: -t[0]):
-            ev = torch.cuda.Event()
+            ev = self._event()
             self._keep(ev)
             ptr = flat.data_ptr() + lo * 4
             inserted = [Op(ev.record, (self.stream,), "event.record", False),
@@ -1834,7 +1868,7 @@ class Executor:
                 self._ops = saved
             ops[pos:pos] = inserted
             self.overlapped.update(members)
-        done = torch.cuda.Event()
+        done = self._event()
         self._keep(done)
         ops.append(Op(done.record, (self.comm_stream,), "event.record", False))
         ops.append(Op(self.stream.wait_event, (done,), "stream.wait_event", False))
@@ -1974,7 +2008,7 @@ class Executor:
             ready.append(last)
         order = sorted(range(len(items)), key=lambda j: ready[j])
         total = sum(it[0].numel for it in items)
-        side = torch.cuda.Stream(self.device)
+        side = self._stream()
         self.sgd_stream = side
         groups, cur, size = [], [], 0
         for j in order:
@@ -1990,7 +2024,7 @@ class Executor:
         for grp in groups:
             at = max(ready[j] for j in grp)
             self._ops = []
-            ev = torch.cuda.Event()
+            ev = self._event()
             self._keep(ev)
             self._ops.append(Op(ev.record, (self.stream,), "event.record", False))
             self._ops.append(Op(side.wait_event, (ev,), "stream.wait_event", False))
@@ -2001,7 +2035,7 @@ class Executor:
         for i, op in enumerate(self.ops_bwd):
             out.append(op)
             out.extend(inserts.get(i, []))
-        done = torch.cuda.Event()
+        done = self._event()
         self._keep(done)
         out.append(Op(done.record, (side,), "event.record", False))
         out.append(Op(self.stream.wait_event, (done,), "stream.wait_event", False))
