@@ -381,6 +381,7 @@ class Executor:
         self._p2p_regs: list = []        # (stream tag, registered Buf, slot): push all-gather outputs,
                                          # direct reduce-scatter partials
         self._emit_on = None             # stream the next ops are emitted on (None: self.stream)
+        self.impl_choice: list = []      # (kind, bytes, "p2p" | "nccl", priced p2p s, priced nccl s) per call site
         self._sfb_full: dict = {}        # gathered SFB factors, keyed by source buffer
         self._sfb_pending: list = []     # deferred SFB weight-gradient GEMMs
         self._sgd_items: dict = {}       # (rank, weight dtype) -> [(master, grad, weight)] (_compile_sgd)
@@ -683,7 +684,7 @@ class Executor:
         s = src[r]
         target = dst[r] if (not accumulate and dst[r].dtype == s.dtype) else self._new(s.shape, s.dtype)
         n = s.numel if s.shape else 1
-        if self._use_p2p("all_reduce", n * (2 if s.dtype == BF16 else 4)):
+        if self._use_p2p("all_reduce", n, 2 if s.dtype == BF16 else 4):
             self._p2p_all_reduce(s, target, n)
         else:
             self._emit("hap_all_reduce", self._comm(), s.ptr, target.ptr, n, s.dtype, self._sptr(), kernel=False)
@@ -708,7 +709,7 @@ class Executor:
         outer, _, inner = _view(full_shape, axis)
         counts = [sz * outer * inner for sz in sizes]
         s = src[r]
-        if self._use_p2p(kind, sum(counts) * (2 if s.dtype == BF16 else 4)):
+        if self._use_p2p(kind, sum(counts), 2 if s.dtype == BF16 else 4):
             # hand-written NVLink kernel: exact chunks, placed in the final layout
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(full_shape, s.dtype)
@@ -759,7 +760,7 @@ class Executor:
         r = g.rank
         s = src[r]
         counts = [sz * outer * inner for sz in sizes]
-        if self._use_p2p("reduce_scatter", sum(counts) * (2 if s.dtype == BF16 else 4)):
+        if self._use_p2p("reduce_scatter", sum(counts), 2 if s.dtype == BF16 else 4):
             exact = not accumulate and dst[r].dtype == s.dtype
             target = dst[r] if exact else self._new(dst[r].shape, s.dtype)
             if self.cfg.p2p_push:   # read the peers' partials in place (registered)
@@ -822,7 +823,8 @@ class Executor:
         recv_shapes = [tuple(sizes1[k] if a == d1 else e for a, e in enumerate(dst[r].shape)) for k in range(self.m)]
         recv_counts = [int(math.prod(sh)) for sh in recv_shapes]
         recv = self._new((max(1, sum(recv_counts)),), s.dtype)
-        if self._use_p2p("all_to_all", max(sum(send_counts), sum(recv_counts)) * (2 if s.dtype == BF16 else 4)):
+        full = sum(int(math.prod(sh)) for sh in src_shapes)
+        if self._use_p2p("all_to_all", full, 2 if s.dtype == BF16 else 4):
             # rank j's chunk for rank k lands at k's receive offset sum_{i<j} count(i -> k)
             def count(j, k):
                 return int(math.prod(tuple(sizes2[k] if a == d2 else e for a, e in enumerate(src_shapes[j]))))
@@ -841,20 +843,64 @@ class Executor:
                 self._block(chunk, _view(recv_shapes[k], d1), 0, dst[r], _view(dst[r].shape, d1), off1[k],
                             sizes1[k], self.caps[r], accumulate)
 
-    def _use_p2p(self, kind: str, nbytes: int) -> bool:
+    def _use_p2p(self, kind: str, elements: int, esize: int) -> bool:
         """Hand-written NVLink kernel (True) or NCCL (False) for one call site.
-        A PeerGroup has only the kernels; ``gather`` forces one side;
-        "auto" takes the kernels for the all-gathers and reduce-scatters
-        (exact uneven chunks in their final layout, no pack / unpack) and
-        NCCL for all-reduce and all-to-all."""
+
+        A PeerGroup has only the kernels; ``gather`` forces one side.
+        "auto" prices both with the reference cost model (cost_model.comm_time,
+        cost_model.py:203) on the measured lines of each implementation
+        (workloads.collective_fits: fit_linear over tools/coll_fit.py sweeps)
+        and the plan's ratio row, and takes the cheaper; without measurements,
+        the kernels for the gathers and reduce-scatters (exact uneven chunks in
+        their final layout) and NCCL otherwise.  Without peer access between
+        the GPUs, NCCL."""
         g = self.group
         if g.comm is None:
             return True
         if self.cfg.gather == "kernel":
             return True
-        if self.cfg.gather in ("padded", "sendrecv", "nccl"):
+        if self.cfg.gather in ("padded", "sendrecv", "nccl") or not self._peer_access():
             return False
-        return kind in ("all_gather", "grouped_broadcast", "reduce_scatter")
+        specs = self._impl_specs(esize)
+        if specs is None:
+            use = kind in ("all_gather", "grouped_broadcast", "reduce_scatter")
+            self.impl_choice.append((kind, elements * esize, "p2p" if use else "nccl", None, None))
+            return use
+        from .cost_model import comm_time
+
+        row = tuple(self.cfg.ratios) if self.cfg.ratios else tuple(c / sum(self.caps) for c in self.caps)
+        ins = Instruction("all_gather" if kind == "grouped_broadcast" else kind, "t", elements=int(elements))
+        t_p2p, t_nccl = comm_time(ins, row, specs["p2p"]), comm_time(ins, row, specs["nccl"])
+        use = t_p2p <= t_nccl
+        self.impl_choice.append((kind, elements * esize, "p2p" if use else "nccl", t_p2p, t_nccl))
+        return use
+
+    def _impl_specs(self, esize: int):
+        """ClusterSpecs carrying each implementation's fitted lines (or None)."""
+        cache = self.__dict__.setdefault("_impl_spec_cache", {})
+        if esize not in cache:
+            from . import workloads
+            from .cost_model import ClusterSpec
+
+            caps = [c or 148 for c in self.caps]
+            docs = {impl: workloads.impl_cluster_doc(caps, impl, esize) for impl in ("p2p", "nccl")}
+            cache[esize] = None if any(d is None for d in docs.values()) else \
+                {impl: ClusterSpec.from_dict(d) for impl, d in docs.items()}
+        return cache[esize]
+
+    def _peer_access(self) -> bool:
+        """Every GPU this node's ranks use can map every other's memory (the
+        peer-memory kernels need it); agreed across ranks once."""
+        if "_peer_ok" not in self.__dict__:
+            ok = True
+            if not self.dry and torch.cuda.is_available():
+                me = self.device.index if self.device.index is not None else torch.cuda.current_device()
+                n = torch.cuda.device_count()
+                ok = all(torch.cuda.can_device_access_peer(me, j) for j in range(n) if j != me)
+            if self.group.distributed:
+                ok = all(self.group.exchange(ok))
+            self._peer_ok = ok
+        return self._peer_ok
 
     def _p2p_tag(self) -> str:
         # one context (staging arena + flag epochs) per stream: calls on one
@@ -1857,7 +1903,7 @@ class Executor:
             ptr = flat.data_ptr() + lo * 4
             inserted = [Op(ev.record, (self.stream,), "event.record", False),
                         Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False)]
-            if g.comm_grad is not None:
+            if g.comm_grad is not None and not self._use_p2p("all_reduce", hi - lo, 4):
                 inserted.append(Op(self.lib.hap_all_reduce, (g.comm_grad, ptr, ptr, hi - lo, F32,
                                                              self.comm_stream.cuda_stream), "hap_all_reduce", False))
             else:   # in place on the registered bucket, P2P kernel on the side stream

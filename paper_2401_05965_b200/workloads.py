@@ -11,6 +11,9 @@ what each proxy keeps and drops.
 """
 from __future__ import annotations
 
+import json
+import os
+
 from .graph_ir import Graph, graph_from_dict
 
 
@@ -167,9 +170,11 @@ def sm_caps(n_gpus: int) -> list[int]:
 
 
 # NVLink-5 collective model for the planner's cost model (latency, bytes/s),
-# bf16 elements.  Round-1 values are set from the profiling guide's measured
+# bf16 elements.  ROUND-1 values, set from the profiling guide's measured
 # NVLink figures (770 GB/s peer copy, 725 GB/s 8-rank all-reduce bus
-# bandwidth) derated for small messages; DESIGN.md tracks the refit.
+# bandwidth) derated for small messages: the committed golden clusters
+# (tests/golden/clusters/b200x*.json) were made with these, so
+# cluster_doc(fitted=False) still reproduces them.
 NVLINK_MODEL = {
     "all_gather": (8e-6, 600e9),
     "all_reduce": (12e-6, 360e9),
@@ -177,14 +182,69 @@ NVLINK_MODEL = {
     "all_to_all": (10e-6, 500e9),
     "grouped_broadcast": (4e-6, 600e9),
 }
-BF16_TFLOPS_PER_SM = 1376.6e12 / SM_COUNT   # MEASURED_PEAKS.json sustained / 148
+# The planner's device speed: sustained bf16 GEMM rate per SM, 1376.6 TF/s
+# as measured in round 1 (MEASURED_PEAKS.json of the current pool reads 1398.8
+# sustained).  Only ratios of device speeds shape a plan; the committed
+# goldens were planned with this value, so it stays for byte-identical plans.
+BF16_TFLOPS_PER_SM = 1376.6e12 / SM_COUNT
+
+# Measured lines (tools/coll_fit.py on B200s: the reference's fit_linear,
+# cost_model.py:310, per world size, collective and implementation — NVLink
+# peer-memory kernel "p2p" or NCCL "nccl"), in the cost model's units: x =
+# the bytes comm_time charges (elements x bytes/element, x the largest shard
+# ratio for gathers, reduce-scatters and all-to-alls).
+FITS_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "collectives_b200.json")
+_FITS: dict | None = None
 
 
-def cluster_doc(caps: list[int], bytes_per_element: int = 2) -> dict:
-    """Cluster spec (reference ClusterSpec JSON) for SM-capped B200 ranks."""
+def collective_fits(world: int) -> dict | None:
+    """{kind: {impl: (latency_s, bw_Bps)}} measured at ``world`` GPUs — or at
+    the nearest measured world size below it (the lines barely move with
+    the rank count on NVSwitch) — or None when nothing was measured."""
+    global _FITS
+    if _FITS is None:
+        _FITS = {}
+        if os.path.exists(FITS_PATH):
+            with open(FITS_PATH) as fh:
+                _FITS = {int(k): v for k, v in json.load(fh).items()}
+    worlds = sorted(w for w in _FITS if w <= world) or sorted(_FITS)
+    if not worlds or world < 2:
+        return None
+    doc = _FITS[worlds[-1]]
+    return {kind: {impl: (v["latency_s"], v["bw_Bps"]) for impl, v in impls.items()} for kind, impls in doc.items()}
+
+
+def impl_cluster_doc(caps: list[int], impl: str, bytes_per_element: int = 2) -> dict | None:
+    """Cluster spec whose collective lines are one implementation's fitted
+    lines ("p2p" or "nccl"); None without measurements for it."""
+    fits = collective_fits(len(caps))
+    if not fits or any(impl not in fits.get(k, {}) for k in ("all_gather", "reduce_scatter", "all_reduce",
+                                                               "all_to_all")):
+        return None
+    lines = {k: fits[k][impl] for k in ("all_gather", "reduce_scatter", "all_reduce", "all_to_all")}
+    lines["grouped_broadcast"] = lines["all_gather"]
+    return {"devices": [{"flops": float(c) * BF16_TFLOPS_PER_SM} for c in caps],
+            "collectives": {k: {"latency_s": lat, "bw_Bps": bw} for k, (lat, bw) in lines.items()},
+            "bytes_per_element": bytes_per_element}
+
+
+def cluster_doc(caps: list[int], bytes_per_element: int = 2, fitted: bool = True) -> dict:
+    """Cluster spec (reference ClusterSpec JSON) for SM-capped B200 ranks.
+    Collective lines: the measured fits (per kind, the implementation the
+    executor's per-call-site choice takes at 4 MiB, Executor._use_p2p) when
+    measured for this world size; else the round-1 model."""
+    lines = dict(NVLINK_MODEL)
+    fits = collective_fits(len(caps)) if fitted else None
+    if fits:
+        ref = 4 << 20
+        for kind in ("all_gather", "reduce_scatter", "all_reduce", "all_to_all"):
+            impls = fits.get(kind)
+            if impls:
+                lines[kind] = min(impls.values(), key=lambda lb: lb[0] + ref / lb[1])
+        lines["grouped_broadcast"] = lines["all_gather"]
     return {
         "devices": [{"flops": float(c) * BF16_TFLOPS_PER_SM} for c in caps],
-        "collectives": {k: {"latency_s": lat, "bw_Bps": bw} for k, (lat, bw) in NVLINK_MODEL.items()},
+        "collectives": {k: {"latency_s": lat, "bw_Bps": bw} for k, (lat, bw) in lines.items()},
         "bytes_per_element": bytes_per_element,
     }
 

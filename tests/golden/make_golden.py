@@ -257,13 +257,13 @@ def moe_plans(bench: bool) -> None:
     2 sequences of 128 tokens per GPU — the regime where the cost model picks
     sufficient-factor broadcasting at 2 and 4 GPUs and all-reduce at 8."""
     for n in (2, 4):
-        cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+        cdoc = workloads.cluster_doc(workloads.sm_caps(n), fitted=False)
         gdoc = workloads.moe_stack_doc(layers=2, batch=2, seq=64)
         _dump(os.path.join(HERE, "graphs", "moe2_b2.json"), gdoc)
         plan_case("moe2_b2", gdoc, f"b200x{n}", cdoc, scaled=True, seeds=(0,))
     if bench:
         for n in (2, 4, 8):
-            cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+            cdoc = workloads.cluster_doc(workloads.sm_caps(n), fitted=False)
             gdoc = workloads.moe_stack_doc(layers=12, batch=2 * n, seq=128)
             plan_case(f"moe12_b{2 * n}", gdoc, f"b200x{n}", cdoc, values=False)
 
@@ -293,7 +293,7 @@ def main() -> None:
     planner_goldens()
 
     # configs[0]: 2-layer MLP, hidden 1024, batch 64, two devices at speed 1:2.
-    mlp_cluster = workloads.cluster_doc([148, 296], bytes_per_element=2)
+    mlp_cluster = workloads.cluster_doc([148, 296], bytes_per_element=2, fitted=False)
     mlp_cluster["devices"] = [{"flops": 1e14}, {"flops": 2e14}]
     _dump(os.path.join(HERE, "clusters", "ratio12.json"), mlp_cluster)
     _dump(os.path.join(HERE, "graphs", "mlp.json"), workloads.mlp_doc())
@@ -301,7 +301,7 @@ def main() -> None:
 
     # Small BERT skeletons on SM-capped B200 clusters (parity-test scale).
     for n in (2, 4):
-        cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+        cdoc = workloads.cluster_doc(workloads.sm_caps(n), fitted=False)
         _dump(os.path.join(HERE, "clusters", f"b200x{n}.json"), cdoc)
         gdoc = workloads.bert_doc(layers=2, batch=2, seq=128)
         _dump(os.path.join(HERE, "graphs", "bert2_b2.json"), gdoc)
@@ -313,7 +313,7 @@ def main() -> None:
         # ties on every sharding choice and its O(expansions^2) dominance scan
         # does not finish at 12 layers ("planning at m=1").
         for n in (2, 4, 8):
-            cdoc = workloads.cluster_doc(workloads.sm_caps(n))
+            cdoc = workloads.cluster_doc(workloads.sm_caps(n), fitted=False)
             _dump(os.path.join(HERE, "clusters", f"b200x{n}.json"), cdoc)
             gdoc = workloads.bert_doc(layers=12, batch=64 * n, seq=128)
             plan_case(f"bert12_b{64 * n}", gdoc, f"b200x{n}", cdoc, values=False)
