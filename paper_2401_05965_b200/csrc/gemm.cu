@@ -654,6 +654,9 @@ __device__ __forceinline__ float* split_region(const TcProblem& pr, const Unit& 
 template <int BN>
 __device__ __forceinline__ void split_write(const TcProblem& pr, const Unit& x, uint32_t tmem_acc, int quarter,
                                             int half, int lane, int rank, int warp_e) {
+  // partial of split s: [BN/8 column groups][32 rows][4 columns] — lane = row
+  // stores its 4 consecutive columns as one float4, 512 contiguous bytes per
+  // warp store, and the finish reads a column group the same way
   float* part = split_region<BN>(pr, x, rank, warp_e) + static_cast<size_t>(x.split) * (32 * (BN / 2));
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
 #pragma unroll 1
@@ -661,7 +664,49 @@ __device__ __forceinline__ void split_write(const TcProblem& pr, const Unit& x, 
     uint32_t r[32];
     tmem_ld32(lane_base + c * 32, r);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) __stcg(part + (c * 32 + i) * 32 + lane, __uint_as_float(r[i]));
+    for (int j = 0; j < 8; ++j)
+      __stcg(reinterpret_cast<float4*>(part) + (c * 8 + j) * 32 + lane,
+             make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                         __uint_as_float(r[4 * j + 3])));
+  }
+}
+
+// Store one finished 4-column group of a lane's row (accumulate, residual
+// epilogue, rounding as the unfused kernels).
+template <typename OutT>
+__device__ __noinline__ void split_store(const TcProblem& pr, int row, int col, float4 a) {
+  if (row >= pr.M || col >= pr.N) return;
+  float v[4] = {a.x, a.y, a.z, a.w};
+  OutT* dst = static_cast<OutT*>(pr.C) + static_cast<int64_t>(row) * pr.ldc + col;
+  const int valid = pr.N - col < 4 ? pr.N - col : 4;
+  if constexpr (std::is_same<OutT, float>::value) {
+    if (pr.accumulate)
+      for (int j = 0; j < valid; ++j) v[j] += dst[j];
+    if (valid == 4 && pr.fin_vec) *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+    else for (int j = 0; j < valid; ++j) dst[j] = v[j];
+  } else {
+    if (pr.accumulate)
+      for (int j = 0; j < valid; ++j) v[j] += __bfloat162float(dst[j]);
+    float rr[4] = {0.f, 0.f, 0.f, 0.f};
+    if (pr.fin_epi != EPI_OP_NONE) {
+      const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(pr.fin_R) + static_cast<int64_t>(row) * pr.fin_ldr + col;
+      for (int j = 0; j < valid; ++j) rr[j] = __bfloat162float(R[j]);
+    }
+    if (pr.fin_epi == EPI_OP_ADD)
+      for (int j = 0; j < 4; ++j) v[j] += rr[j];
+    if (valid == 4 && pr.fin_vec) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&lo);
+      o.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst) = o;
+    } else {
+      for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+    }
+    if (pr.fin_epi == EPI_OP_ADD2) {
+      __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(pr.fin_Y) + static_cast<int64_t>(row) * pr.fin_ldy + col;
+      for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(v[j]) + rr[j]);
+    }
   }
 }
 
@@ -677,54 +722,38 @@ __device__ __forceinline__ void split_finish(const TcProblem& pr, const Unit& x,
     while (ld_acquire_gpu(cnt) < static_cast<unsigned>(S)) __nanosleep(64);
   }
   __syncwarp();
-  const float* region = split_region<BN>(pr, x, rank, warp_e);
-  constexpr int G = BN / 8;   // 4-column groups of the warp's BN/2 columns
+  const float4* region = reinterpret_cast<const float4*>(split_region<BN>(pr, x, rank, warp_e));
+  constexpr int G = BN / 8;                 // 4-column groups of the warp's BN/2 columns
+  constexpr int kSlice = 32 * (BN / 8);     // float4s per split partial
   const int g0 = x.split * G / S, g1 = (x.split + 1) * G / S;
   const int row = row0 + lane;
-  const bool row_ok = row < pr.M;
-  OutT* C = static_cast<OutT*>(pr.C);
+  const int col_base = x.n0 + half * (BN / 2);
+  // (group, split) pairs in group-major order, 16 float4 loads in flight per
+  // batch; each group is summed in split order 0..S-1 whatever the batching
+  const int total = (g1 - g0) * S;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
-  for (int g = g0; g < g1; ++g) {
-    const int cl = g * 4;                         // column within the warp's half
-    const int col = x.n0 + half * (BN / 2) + cl;  // output column
-    float v[4];
+  for (int base = 0; base < total; base += 16) {
+    float4 v[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = __ldcg(region + (cl + j) * 32 + lane);
-    for (int sp = 1; sp < S; ++sp) {
-      const float* part = region + static_cast<size_t>(sp) * (32 * (BN / 2));
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[j] += __ldcg(part + (cl + j) * 32 + lane);
+    for (int i = 0; i < 16; ++i) {
+      const int k = base + i;
+      if (k < total) {
+        const int gi = k / S, sp = k - gi * S;
+        v[i] = __ldcg(region + sp * kSlice + (g0 + gi) * 32 + lane);
+      }
     }
-    if (!row_ok || col >= pr.N) continue;
-    OutT* dst = C + static_cast<int64_t>(row) * pr.ldc + col;
-    const int valid = pr.N - col < 4 ? pr.N - col : 4;
-    if constexpr (std::is_same<OutT, float>::value) {
-      if (pr.accumulate)
-        for (int j = 0; j < valid; ++j) v[j] += dst[j];
-      if (valid == 4 && pr.fin_vec) *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-      else for (int j = 0; j < valid; ++j) dst[j] = v[j];
-    } else {
-      if (pr.accumulate)
-        for (int j = 0; j < valid; ++j) v[j] += __bfloat162float(dst[j]);
-      float rr[4] = {0.f, 0.f, 0.f, 0.f};
-      if (pr.fin_epi != EPI_OP_NONE) {
-        const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(pr.fin_R) + static_cast<int64_t>(row) * pr.fin_ldr + col;
-        for (int j = 0; j < valid; ++j) rr[j] = __bfloat162float(R[j]);
-      }
-      if (pr.fin_epi == EPI_OP_ADD)
-        for (int j = 0; j < 4; ++j) v[j] += rr[j];
-      if (valid == 4 && pr.fin_vec) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
-        uint2 o;
-        o.x = *reinterpret_cast<uint32_t*>(&lo);
-        o.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(dst) = o;
-      } else {
-        for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
-      }
-      if (pr.fin_epi == EPI_OP_ADD2) {
-        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(pr.fin_Y) + static_cast<int64_t>(row) * pr.fin_ldy + col;
-        for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(v[j]) + rr[j]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = base + i;
+      if (k < total) {
+        const int gi = k / S, sp = k - gi * S;
+        if (sp == 0) {
+          acc = v[i];
+        } else {
+          acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
+        }
+        if (sp == S - 1) split_store<OutT>(pr, row, col_base + (g0 + gi) * 4, acc);
       }
     }
   }

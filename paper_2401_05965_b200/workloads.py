@@ -140,6 +140,153 @@ def moe_stack_doc(layers: int = 12, experts: int = 2, batch: int = 8, seq: int =
     return {"nodes": nodes, "loss": "loss"}
 
 
+def vit_moe_doc(layers: int = 12, experts: int = 2, images: int = 16, tokens: int = 197, hidden: int = 768,
+                ffn: int = 3072) -> dict:
+    """configs[3] (ViT-MoE): a ViT-B/16 GEMM skeleton (197 tokens per image,
+    hidden 768) whose every block is an attention skeleton (Q/K/V, the gate
+    sigmoid(q*k)*v, output projection + residual — as bert_doc) followed by
+    a mixture of `experts` SiLU FFN experts (768 -> 3072 -> 768) whose outputs
+    are summed and added to the residual stream.  Every expert sees every
+    token (a dense mixture: the reference IR has no routing op)."""
+    rows = images * tokens
+    nodes = [_n("x0", "Placeholder", [rows, hidden])]
+    prev = "x0"
+    for layer in range(layers):
+        p = f"l{layer}_"
+        for w in ("q", "k", "v"):
+            nodes.append(_n(p + "W" + w, "Parameter", [hidden, hidden]))
+            nodes.append(_n(p + w, "MatMul", [rows, hidden], [prev, p + "W" + w]))
+        nodes.append(_n(p + "qk", "ElemwiseBinary", [rows, hidden], [p + "q", p + "k"], tag="mul"))
+        nodes.append(_n(p + "att", "ElemwiseUnary", [rows, hidden], [p + "qk"], tag="sigmoid"))
+        nodes.append(_n(p + "ctx", "ElemwiseBinary", [rows, hidden], [p + "att", p + "v"], tag="mul"))
+        nodes.append(_n(p + "Wo", "Parameter", [hidden, hidden]))
+        nodes.append(_n(p + "o", "MatMul", [rows, hidden], [p + "ctx", p + "Wo"]))
+        nodes.append(_n(p + "x1", "ElemwiseBinary", [rows, hidden], [prev, p + "o"], tag="add"))
+        ys = []
+        for e in range(experts):
+            q = f"{p}e{e}_"
+            nodes.append(_n(q + "W1", "Parameter", [hidden, ffn]))
+            nodes.append(_n(q + "f1", "MatMul", [rows, ffn], [p + "x1", q + "W1"]))
+            nodes.append(_n(q + "s1", "ElemwiseUnary", [rows, ffn], [q + "f1"], tag="sigmoid"))
+            nodes.append(_n(q + "g", "ElemwiseBinary", [rows, ffn], [q + "f1", q + "s1"], tag="mul"))
+            nodes.append(_n(q + "W2", "Parameter", [ffn, hidden]))
+            nodes.append(_n(q + "y", "MatMul", [rows, hidden], [q + "g", q + "W2"]))
+            ys.append(q + "y")
+        acc = ys[0]
+        for i, y in enumerate(ys[1:], 1):
+            nodes.append(_n(f"{p}ysum{i}", "ElemwiseBinary", [rows, hidden], [acc, y], tag="add"))
+            acc = f"{p}ysum{i}"
+        nodes.append(_n(p + "x2", "ElemwiseBinary", [rows, hidden], [p + "x1", acc], tag="add"))
+        prev = p + "x2"
+    nodes.append(_n("loss", "Reduce", [], [prev], dims="all"))
+    return {"nodes": nodes, "loss": "loss"}
+
+
+def vit_moe(layers: int = 12, experts: int = 2, images: int = 16, tokens: int = 197, hidden: int = 768,
+            ffn: int = 3072) -> Graph:
+    return graph_from_dict(vit_moe_doc(layers, experts, images, tokens, hidden, ffn))
+
+
+def expert_sharded_program(g: Graph):
+    """The expert-sharded program of a ViT-MoE skeleton (configs[3]).
+
+    Attention blocks run data parallel (token rows ``@shard0``, weights
+    replicated); each MoE FFN block runs expert-sliced over all devices:
+    the block input is all-gathered along the token axis (``x1@full``), every
+    expert's W1 is column-sharded and W2 row-sharded (``@shard1`` /
+    ``@shard0``: each device holds a ratio-weighted slice of every expert),
+    the expert outputs are partial sums, added across experts and
+    reduce-scattered back to token rows.  Uneven all-gather and
+    reduce-scatter run in every layer's forward, and their adjoints
+    (reduce-scatter, all-gather) in the backward.
+
+    The same instruction pattern is in the REFERENCE planner's program space:
+    tools/vit_moe_plan.py enumerates every complete program of one expert
+    FFN block with the reference-restated synthesizer
+    (synthesizer.enumerate_all_complete, reference synthesizer.py:538) and
+    finds this one; the planner itself never emits it for these graphs
+    because its forward-only cost model prices data parallelism as
+    communication-free (DESIGN.md, configs[3])."""
+    from .program import DistributedProgram, Instruction
+
+    kinds = {"MatMul": "matmul", "ElemwiseUnary": "elemwise_unary", "ElemwiseBinary": "elemwise_binary",
+             "Reduce": "reduce", "Identity": "identity"}
+    form: dict = {}
+    instrs: list = []
+    emitted: set = set()
+
+    def source(ref: str, out: str, kind: str, axis=None):
+        if out not in emitted:
+            emitted.add(out)
+            instrs.append(Instruction(kind, ref, output=out, axis=axis))
+
+    for n in g.nodes:
+        if n.op in ("Placeholder", "Parameter"):
+            continue
+        base = n.id.split("_", 1)[-1]
+        expert = "_e" in n.id and base.split("_", 1)[-1] in ("f1", "s1", "g", "y")
+        ops = []
+        for i in n.inputs:
+            src = g.producer(i)
+            if src.op == "Parameter":
+                if expert and i.endswith("_W1"):
+                    source(i, f"{i}@shard1", "parameter_shard", 1)
+                    ops.append(f"{i}@shard1")
+                elif expert and i.endswith("_W2"):
+                    source(i, f"{i}@shard0", "parameter_shard", 0)
+                    ops.append(f"{i}@shard0")
+                else:
+                    source(i, f"{i}@full", "parameter")
+                    ops.append(f"{i}@full")
+            elif src.op == "Placeholder":
+                source(i, f"{i}@shard0", "placeholder_shard", 0)
+                ops.append(f"{i}@shard0")
+            else:
+                ops.append(form[i])
+        out_form = "shard0"
+        if expert:
+            kind = n.id.rsplit("_", 1)[-1]
+            if kind == "f1":
+                x = n.inputs[0]
+                if f"{x}@full" not in emitted:
+                    emitted.add(f"{x}@full")
+                    instrs.append(Instruction("all_gather", x, operands=(f"{x}@shard0",), output=f"{x}@full", axis=0))
+                ops[0] = f"{x}@full"
+            out_form = "partial" if kind == "y" else "shard1"
+        elif "ysum" in n.id:
+            out_form = "partial"
+        elif n.op == "Reduce":
+            out_form = "partial"
+        elif n.id.endswith("_x2"):
+            # the summed expert outputs go back to token rows
+            y = n.inputs[1]
+            instrs.append(Instruction("reduce_scatter", y, operands=(f"{y}@partial",), output=f"{y}@shard0", axis=0))
+            ops[1] = f"{y}@shard0"
+        out = f"{n.id}@{out_form}"
+        form[n.id] = out
+        instrs.append(Instruction(kinds[n.op], n.id, operands=tuple(ops), output=out, dims=n.dims, tag=n.tag))
+    return DistributedProgram(instrs=tuple(instrs), loss=g.loss)
+
+
+def expert_sharded_plan(g: Graph, spec) -> dict:
+    """Reference-schema plan document (cli.py:73) of the expert-sharded
+    program: ratios by the planner's own alternating loop with the synthesis
+    step fixed to this program (optimizer_loop.alternate: the LP of
+    load_balancer.optimize_ratios), shard table by its rounding rule,
+    estimate by its cost model."""
+    from .cli import plan_document
+    from .optimizer_loop import alternate
+    from .synthesizer import SynthesisResult
+
+    prog = expert_sharded_program(g)
+
+    def synth(*_args):
+        return SynthesisResult(program=prog, cost_s=0.0, complete=True, optimal=True, exhausted=False,
+                               expansions=0, generated=0, purged=0)
+
+    return plan_document(g, spec, alternate(g, spec, synth_fn=synth))
+
+
 def moe_stack(layers: int = 12, experts: int = 2, batch: int = 8, seq: int = 128) -> Graph:
     return graph_from_dict(moe_stack_doc(layers, experts, batch, seq))
 
