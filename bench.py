@@ -46,11 +46,22 @@ WORKLOADS = {
     "moe": {"per_gpu_batch": 2, "stem": "moe12",
             "desc": "BERT-MoE FFN stack (configs[4]): 12 layers x 2 SiLU experts (768->3072->768), seq 128, "
                     "SFB-vs-all-reduce chosen per weight by the cost model, train step fwd+bwd+sync+SGD"},
+    "vitmoe": {"per_gpu_batch": 16, "stem": "vitmoe12", "seq": 197,
+               "desc": "ViT-MoE skeleton (configs[3]): 12 ViT-B/16 blocks (197 tokens, hidden 768), each an "
+                       "attention skeleton + 2 SiLU experts (768->3072->768) expert-sliced over the GPUs: uneven "
+                       "all-gather / reduce-scatter per layer (program from the reference's program space, LP "
+                       "ratios), train step fwd+bwd+sync+SGD"},
 }
+
+
+def _seq(workload: str) -> int:
+    return WORKLOADS[workload].get("seq", SEQ)
 
 
 def _graph(workload: str, batch: int):
     from paper_2401_05965_b200 import workloads
+    if workload == "vitmoe":
+        return workloads.vit_moe(layers=LAYERS, experts=2, images=batch, tokens=_seq(workload))
     if workload == "moe":
         return workloads.moe_stack(layers=LAYERS, batch=batch, seq=SEQ)
     return workloads.bert(layers=LAYERS, batch=batch, seq=SEQ)
@@ -219,7 +230,7 @@ def cpu_baseline(steps: int, sample_batch: int, workload: str = "bert", budget_s
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     return {"value": sample_batch / dt, "unit": "samples/s", "cores": threads, "kind": "port",
             "sample": f"{steps} train steps (fwd+bwd+SGD, float64) of the planner's 12-layer {workload} program "
-                      f"at batch {sample_batch} x seq {SEQ} on one simulated device",
+                      f"at batch {sample_batch} x seq {_seq(workload)} on one simulated device",
             "seconds_per_step": dt}
 
 
@@ -232,7 +243,7 @@ def run_reference_arm(args, rank: int) -> None:
             "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload]["desc"],
-                       "global_batch": sample, "seq_len": SEQ, "parallelism": "cpu"},
+                       "global_batch": sample, "seq_len": _seq(args.workload), "parallelism": "cpu"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit_json(line)
@@ -545,7 +556,7 @@ def main() -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl["desc"],
-                       "global_batch": batch, "seq_len": SEQ, "parallelism": f"hap-spmd{n}",
+                       "global_batch": batch, "seq_len": _seq(args.workload), "parallelism": f"hap-spmd{n}",
                        "plan": plan_name, "sm_caps": caps, "ratios": list(ratios),
                        "grad_sync": dict(sorted(ex.sync_choice.items())) or "n/a (m=1)",
                        "grad_sync_mode": args.grad_sync, "collectives": args.collectives,

@@ -265,7 +265,34 @@ def expert_sharded_program(g: Graph):
         out = f"{n.id}@{out_form}"
         form[n.id] = out
         instrs.append(Instruction(kinds[n.op], n.id, operands=tuple(ops), output=out, dims=n.dims, tag=n.tag))
-    return DistributedProgram(instrs=tuple(instrs), loss=g.loss)
+    return DistributedProgram(instrs=tuple(_theory_instrs(g, instrs)), loss=g.loss)
+
+
+def _theory_instrs(g: Graph, instrs: list) -> list:
+    """Each instruction as the planner's theory states it (its Hoare triple's
+    instruction: ``sharded``, ``flops`` and ``elements`` as the cost model
+    reads them), checking on the way that the sequence is a valid program of
+    that theory: every triple's precondition holds when it runs, and the
+    loss property is realised at the end (theory.py; reference theory.py)."""
+    from .theory import build_theory, merge_post
+
+    theory = build_theory(g, 2, fuse=False)   # one instruction per triple (sources unfused)
+    index = {}
+    for t in theory.triples:
+        if len(t.instrs) == 1:
+            index.setdefault(t.instrs[0].canonical(), []).append(t)
+    props = frozenset(theory.initial_props)
+    out = []
+    for ins in instrs:
+        triples = [t for t in index.get(ins.canonical(), []) if t.pre <= props]
+        if not triples:
+            raise ValueError(f"{ins.canonical()} is not applicable under the planner's theory")
+        t = triples[0]
+        out.append(t.instrs[0])
+        props = merge_post(props, t.post)
+    if not any(p.ref == g.loss for p in props):
+        raise ValueError("program does not realise the loss")
+    return out
 
 
 def expert_sharded_plan(g: Graph, spec) -> dict:

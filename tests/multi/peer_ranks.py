@@ -82,7 +82,13 @@ def main():
     ap.add_argument("--world", default="2,3")
     ap.add_argument("--variants", default="all_reduce,sfb")
     ap.add_argument("--dtypes", default="fp32,bf16")
+    ap.add_argument("--capture-every", type=int, default=5, help="every k-th run replays a captured graph (0: never)")
+    ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
+    if args.verbose:
+        import faulthandler
+
+        faulthandler.dump_traceback_later(60, repeat=True)
     torch.cuda.set_device(0)
     failures, count, bit_equal, bit_total = [], 0, 0, 0
     for world in [int(w) for w in args.world.split(",")]:
@@ -96,7 +102,9 @@ def main():
                 for sync in args.variants.split(","):
                     count += 1
                     label = f"{name} {dtype} {sync}"
-                    capture = count % 5 == 0   # every fifth run replays a captured CUDA graph per rank
+                    capture = args.capture_every > 0 and count % args.capture_every == 0
+                    if args.verbose:
+                        print(f"run {count}: {label}{' (graph)' if capture else ''}", flush=True)
                     try:
                         exs, losses = run_peer(doc, shapes, inputs, dtype, sync, capture)
                     except Exception as exc:  # noqa: BLE001 - reported as a failure
