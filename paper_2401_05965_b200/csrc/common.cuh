@@ -52,7 +52,7 @@ int sm_count();
 // outgrows is retired, never freed, because a CUDA graph captured earlier may
 // still hold its address.  `zeroed` slots are cleared on allocation: kernels
 // that use them as counters leave them at zero when they finish.
-enum ScratchSlot { kScratchSplitWs = 0, kScratchSplitFlags, kScratchReduce, kScratchReduceTickets,
+enum ScratchSlot { kScratchSplitWs = 0, kScratchReduce, kScratchReduceTickets,
                    kScratchStreamK, kScratchStreamKFlags, kScratchSlots };
 bool stream_scratch(cudaStream_t stream, int slot, size_t bytes, bool zeroed, void** out);
 

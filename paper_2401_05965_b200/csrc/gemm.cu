@@ -252,11 +252,14 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
 }
 
 // Epilogue modes: direct per-thread stores (any layout), TMA bulk store, TMA
-// bulk reduce-add (fp32 accumulate), and split K (EPI_SPLIT_FIN): every K
-// split writes its fp32 partial tile to the workspace, and the splits of a
-// tile then finish it together in split order (split_finish) — deterministic,
-// no floating-point atomics, no second launch.
-enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_FIN = 3 };
+// bulk reduce-add (fp32 accumulate: one writer per element), and split K
+// (EPI_SPLIT_WS): each K split stores its fp32 partial tile into its own
+// slice of a per-stream workspace, and split_reduce_kernel then sums the
+// slices in split order and applies accumulate / the residual epilogue —
+// deterministic (no floating-point atomics), with no dependency between the
+// GEMM's CTAs (a split GEMM can share the GPU with spinning peer-memory
+// kernels on other streams without deadlock).
+enum { EPI_DIRECT = 0, EPI_TMA_STORE = 1, EPI_TMA_ADD = 2, EPI_SPLIT_WS = 3 };
 // fused elementwise ops of the epilogue (hap_gemm_desc.epi)
 enum { EPI_OP_NONE = HAP_EPI_NONE, EPI_OP_ADD = HAP_EPI_ADD, EPI_OP_ADD2 = HAP_EPI_ADD2,
        EPI_OP_SWISH = HAP_EPI_SWISH, EPI_OP_SWISH_BWD = HAP_EPI_SWISH_BWD };
@@ -366,16 +369,9 @@ struct alignas(64) TcProblem {
   CUtensorMap a, b, c;     // c: output map (TMA epilogues)
   void* C;
   int64_t ldc;
-  // EPI_SPLIT_FIN: fp32 partials, per (tile, CTA of the pair, epilogue warp)
-  // a block of `splits` column-major [BN/2][32] regions; two counters
-  // (arrived, finished) per (tile, CTA, warp); the residual epilogue the
-  // finish applies (NONE / ADD / ADD2) with its tensors.
-  float* ws;
-  unsigned* split_cnt;
-  const void* fin_R;
-  void* fin_Y;
-  int64_t fin_ldr, fin_ldy;
-  int fin_epi, fin_vec;
+  float* ws;               // EPI_SPLIT_WS: fp32 partials [splits][ws_rows][ws_ld]
+  int64_t ws_ld;
+  int ws_rows;             // rows per split slice (M rounded up to whole tiles)
   int M, N, K;
   int m_tiles, n_tiles, k_blocks;
   int splits, kb_per_split;
@@ -604,10 +600,11 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
   __syncwarp();
 }
 
-// Epilogue of one unit for one warp: drain the accumulator into C.
+// Epilogue of one unit for one warp: drain the accumulator into C, or (split
+// K) into split `split`'s slice of the workspace.
 template <int BN, typename OutT>
 __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
-                                              int lane, int row0, int col0, uint8_t* buf,
+                                              int lane, int row0, int col0, int split, uint8_t* buf,
                                               uint32_t& box_seq, uint32_t ld_bar, uint32_t& ld_phase,
                                               const float* part) {
   // part: stream-K partial of this CTA's 128 x BN share (column-major), added to
@@ -619,6 +616,11 @@ __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem
       return;
     }
   }
+  if (pr.epi_mode == EPI_SPLIT_WS) {
+    drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0, pr.M, pr.N, pr.ws,
+                                 pr.ws_ld, EPI_TMA_STORE, 1, 0, &pr.c, buf, box_seq);
+    return;
+  }
   drain_accumulator<BN, OutT>(tmem_acc, quarter, half, lane, row0, col0, pr.M, pr.N, static_cast<OutT*>(pr.C),
                               pr.ldc, pr.epi_mode, pr.vec_ok, pr.accumulate, &pr.c, buf, box_seq, prow);
 }
@@ -628,145 +630,6 @@ struct Unit {
   int sk_kind;   // 0: whole tile; 1: a tile's last K blocks (write partial); 2: its first (finish it)
   int sk_slot;   // workspace slot of a cut tile
 };
-
-// ---- split K, finished in the kernel (EPI_SPLIT_FIN)
-// A warp's region of a tile is 32 rows x BN/2 columns.  Split s of the tile
-// (1) writes its fp32 accumulator for the region to its column-major
-// [BN/2][32] slot of the workspace (lane = row: one coalesced 128-byte store
-// per column), then the caller releases the TMEM buffer; (2) arrives on the
-// region's counter and waits until all S splits have arrived — every unit of
-// a split launch runs in the first and only round of the persistent grid, so
-// the S CTAs are co-resident; (3) finishes its share of the region, column
-// groups [s*G/S, (s+1)*G/S) of G = BN/8 groups of 4 columns: the S partials
-// added in split order (0, 1, ..., S-1), then + C when accumulating, then the
-// residual epilogue with the roundings of the unfused kernels (ADD: C =
-// bf16(sum + R); ADD2: C = bf16(sum), Y = bf16(bf16(sum) + R)); (4) counts
-// itself done, and the last split resets both counters for the next launch.
-// The sum is the same on every run whatever the CTAs' timing.
-__device__ __forceinline__ unsigned* split_counters(const TcProblem& pr, const Unit& x, int rank, int warp_e) {
-  return pr.split_cnt + ((static_cast<size_t>(x.tile) * 2 + rank) * kEpiWarps + warp_e) * 2;
-}
-template <int BN>
-__device__ __forceinline__ float* split_region(const TcProblem& pr, const Unit& x, int rank, int warp_e) {
-  return pr.ws + ((static_cast<size_t>(x.tile) * 2 + rank) * kEpiWarps + warp_e) * pr.splits * (32 * (BN / 2));
-}
-
-template <int BN>
-__device__ __forceinline__ void split_write(const TcProblem& pr, const Unit& x, uint32_t tmem_acc, int quarter,
-                                            int half, int lane, int rank, int warp_e) {
-  // partial of split s: [BN/8 column groups][32 rows][4 columns] — lane = row
-  // stores its 4 consecutive columns as one float4, 512 contiguous bytes per
-  // warp store, and the finish reads a column group the same way
-  float* part = split_region<BN>(pr, x, rank, warp_e) + static_cast<size_t>(x.split) * (32 * (BN / 2));
-  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
-#pragma unroll 1
-  for (int c = 0; c < BN / 64; ++c) {
-    uint32_t r[32];
-    tmem_ld32(lane_base + c * 32, r);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      __stcg(reinterpret_cast<float4*>(part) + (c * 8 + j) * 32 + lane,
-             make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                         __uint_as_float(r[4 * j + 3])));
-  }
-}
-
-// Store one finished 4-column group of a lane's row (accumulate, residual
-// epilogue, rounding as the unfused kernels).
-template <typename OutT>
-__device__ __noinline__ void split_store(const TcProblem& pr, int row, int col, float4 a) {
-  if (row >= pr.M || col >= pr.N) return;
-  float v[4] = {a.x, a.y, a.z, a.w};
-  OutT* dst = static_cast<OutT*>(pr.C) + static_cast<int64_t>(row) * pr.ldc + col;
-  const int valid = pr.N - col < 4 ? pr.N - col : 4;
-  if constexpr (std::is_same<OutT, float>::value) {
-    if (pr.accumulate)
-      for (int j = 0; j < valid; ++j) v[j] += dst[j];
-    if (valid == 4 && pr.fin_vec) *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-    else for (int j = 0; j < valid; ++j) dst[j] = v[j];
-  } else {
-    if (pr.accumulate)
-      for (int j = 0; j < valid; ++j) v[j] += __bfloat162float(dst[j]);
-    float rr[4] = {0.f, 0.f, 0.f, 0.f};
-    if (pr.fin_epi != EPI_OP_NONE) {
-      const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(pr.fin_R) + static_cast<int64_t>(row) * pr.fin_ldr + col;
-      for (int j = 0; j < valid; ++j) rr[j] = __bfloat162float(R[j]);
-    }
-    if (pr.fin_epi == EPI_OP_ADD)
-      for (int j = 0; j < 4; ++j) v[j] += rr[j];
-    if (valid == 4 && pr.fin_vec) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
-      uint2 o;
-      o.x = *reinterpret_cast<uint32_t*>(&lo);
-      o.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(dst) = o;
-    } else {
-      for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
-    }
-    if (pr.fin_epi == EPI_OP_ADD2) {
-      __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(pr.fin_Y) + static_cast<int64_t>(row) * pr.fin_ldy + col;
-      for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(v[j]) + rr[j]);
-    }
-  }
-}
-
-template <int BN, typename OutT>
-__device__ __forceinline__ void split_finish(const TcProblem& pr, const Unit& x, int half, int lane, int rank,
-                                             int warp_e, int row0) {
-  const int S = pr.splits;
-  unsigned* cnt = split_counters(pr, x, rank, warp_e);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) {
-    atomicAdd(cnt, 1u);
-    while (ld_acquire_gpu(cnt) < static_cast<unsigned>(S)) __nanosleep(64);
-  }
-  __syncwarp();
-  const float4* region = reinterpret_cast<const float4*>(split_region<BN>(pr, x, rank, warp_e));
-  constexpr int G = BN / 8;                 // 4-column groups of the warp's BN/2 columns
-  constexpr int kSlice = 32 * (BN / 8);     // float4s per split partial
-  const int g0 = x.split * G / S, g1 = (x.split + 1) * G / S;
-  const int row = row0 + lane;
-  const int col_base = x.n0 + half * (BN / 2);
-  // (group, split) pairs in group-major order, 16 float4 loads in flight per
-  // batch; each group is summed in split order 0..S-1 whatever the batching
-  const int total = (g1 - g0) * S;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-  for (int base = 0; base < total; base += 16) {
-    float4 v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int k = base + i;
-      if (k < total) {
-        const int gi = k / S, sp = k - gi * S;
-        v[i] = __ldcg(region + sp * kSlice + (g0 + gi) * 32 + lane);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int k = base + i;
-      if (k < total) {
-        const int gi = k / S, sp = k - gi * S;
-        if (sp == 0) {
-          acc = v[i];
-        } else {
-          acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w;
-        }
-        if (sp == S - 1) split_store<OutT>(pr, row, col_base + (g0 + gi) * 4, acc);
-      }
-    }
-  }
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    if (atomicAdd(cnt + 1, 1u) == static_cast<unsigned>(S) - 1) {   // every split is past the wait
-      cnt[0] = 0u;
-      cnt[1] = 0u;
-    }
-  }
-}
-
 
 // Work unit u -> (problem, output tile, K-block range).  Grouped: units are
 // laid out problem after problem; within a problem unit = split * tiles + tile.
@@ -991,18 +854,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const TcProblem& pr = bt.p[x.prob];
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      if (pr.epi_mode == EPI_SPLIT_FIN) {
-        // partial out, accumulator released, then the ordered finish
-        split_write<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, 0, warp - 4);
-        tc_fence_before();
-        mbar_arrive(tempty0 + 8 * acc);
-        split_finish<BN, OutT>(pr, x, half, lane, 0, warp - 4, x.m0 + quarter * 32);
-      } else {
-        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, buf,
-                                box_seq, ld_bar, ld_phase, nullptr);
-        tc_fence_before();
-        mbar_arrive(tempty0 + 8 * acc);
-      }
+      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
+                              buf, box_seq, ld_bar, ld_phase, nullptr);
+      tc_fence_before();
+      mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -1244,16 +1099,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      if (pr.epi_mode == EPI_SPLIT_FIN) {   // split K: partial out, release the accumulator, ordered finish
-        split_write<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, static_cast<int>(rank), warp - 4);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
-        split_finish<BN, OutT>(pr, x, half, lane, static_cast<int>(rank), warp - 4, m0 + quarter * 32);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-        continue;
-      }
       // stream-K: this CTA's 128 x BN share of a cut tile's partial
       float* part = nullptr;
       unsigned* flag = nullptr;
@@ -1272,8 +1117,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
           __syncwarp();
         }
-        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, buf,
-                                box_seq, ld_bar, ld_phase, x.sk_kind == 2 ? part : nullptr);
+        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, x.n0, x.split,
+                                buf, box_seq, ld_bar, ld_phase, x.sk_kind == 2 ? part : nullptr);
         if (x.sk_kind == 2 && lane == 0) *flag = 0u;   // consumed: ready for the next launch
       }
       tc_fence_before();
@@ -1448,10 +1293,10 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
                 static_cast<double>(rounds * kps) * t_kb};
     }
   }
-  // Split K finishes in the kernel: each split writes its fp32 partial tile
-  // and reads back its share of all of them (split_finish) — a short serial
-  // tail, so split only when the shortened K walk saves more than that.
-  constexpr double kSplitTailUs = 2.0;
+  // Split K stores fp32 partial slices and sums them in order in a second
+  // launch (split_reduce_kernel): a serial tail (~5 us measured on B200),
+  // so split only when the shortened K walk saves more than that.
+  constexpr double kSplitTailUs = 5.0;
   if (split.score > 0 && split.est_us + kSplitTailUs < plain.est_us) return split.s;
   return plain.score > 0 ? plain.s : split.s;
 }
@@ -1485,6 +1330,98 @@ void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, i
       bool dup = false;
       for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits);
       if (!dup) out.push_back(sh);
+    }
+  }
+}
+
+// C (+)= sum over s of ws[s] — the K splits' partial tiles added in split
+// order (fixed, so repeated launches give identical bits).  A thread owns 4
+// consecutive columns of a row; every split's load is issued before the sum.
+//
+// Split K under a residual epilogue (bf16 outputs): the reduction applies it
+// with the fused path's roundings — HAP_EPI_ADD: C = bf16(sum + R);
+// HAP_EPI_ADD2: C = bf16(sum), Y = bf16(bf16(sum) + R).  (ADD onto C itself
+// is the plain accumulate.)
+template <typename OutT>
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float* __restrict__ ws, int splits,
+                                                           int64_t slice, int64_t ld, OutT* __restrict__ C,
+                                                           int64_t ldc, int M, int N, int accumulate, int vec,
+                                                           int epi, const __nv_bfloat16* __restrict__ R,
+                                                           int64_t ldr, __nv_bfloat16* __restrict__ Y,
+                                                           int64_t ldy) {
+  hap::pdl_enter();
+  const int64_t nq = (static_cast<int64_t>(N) + 3) / 4;
+  const int64_t total = static_cast<int64_t>(M) * nq;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / nq;
+    const int col = static_cast<int>(i - row * nq) * 4;
+    const float* src = ws + row * ld + col;
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+    constexpr int U = 8;
+    for (int s0 = 1; s0 < splits; s0 += U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + u < splits) v[u] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + u) * slice));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + u < splits) {
+          acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+        }
+    }
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    OutT* dst = C + row * ldc + col;
+    if (vec && col + 4 <= N) {
+      if constexpr (std::is_same<OutT, float>::value) {
+        float4 o = make_float4(a[0], a[1], a[2], a[3]);
+        if (accumulate) {
+          const float4 c = *reinterpret_cast<const float4*>(dst);
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        *reinterpret_cast<float4*>(dst) = o;
+      } else {
+        auto ld4 = [](const void* p, float (&f)[4]) {
+          const uint2 c = *reinterpret_cast<const uint2*>(p);
+          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.x));
+          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&c.y));
+          f[0] = lo.x; f[1] = lo.y; f[2] = hi.x; f[3] = hi.y;
+        };
+        auto st4 = [](void* p, const float (&f)[4]) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(f[0], f[1]), hi = __floats2bfloat162_rn(f[2], f[3]);
+          uint2 o;
+          o.x = *reinterpret_cast<uint32_t*>(&lo);
+          o.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(p) = o;
+        };
+        float f[4] = {a[0], a[1], a[2], a[3]}, x[4];
+        if (accumulate) {
+          ld4(dst, x);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] += x[e];
+        }
+        if (epi != EPI_OP_NONE) ld4(R + row * ldr + col, x);
+        if (epi == EPI_OP_ADD) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] += x[e];
+        }
+        st4(dst, f);
+        if (epi == EPI_OP_ADD2) {
+          float y[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) y[e] = bf16_round(f[e]) + x[e];
+          st4(Y + row * ldy + col, y);
+        }
+      }
+    } else {
+      for (int e = 0; e < 4 && col + e < N; ++e) {
+        float v = a[e];
+        if (accumulate) v += to_f32(dst[e]);
+        const float r = epi != EPI_OP_NONE ? to_f32(R[row * ldr + col + e]) : 0.f;
+        if (epi == EPI_OP_ADD) v += r;
+        dst[e] = from_f32<OutT>(v);
+        if (epi == EPI_OP_ADD2) Y[row * ldy + col + e] = from_f32<__nv_bfloat16>(bf16_round(v) + r);
+      }
     }
   }
 }
@@ -1653,6 +1590,8 @@ bool sk_workspace(cudaStream_t stream, float** ws, unsigned** flags) {
   return true;
 }
 
+inline int64_t ws_pitch(int64_t n) { return (n + 3) / 4 * 4; }   // 16-byte rows for the TMA map
+
 // Autotuned shapes (hap_matmul_tune), keyed by everything that decides the
 // shape: problem extents, orientation, epilogue, output type, SM cap.
 std::mutex& tune_mutex() {
@@ -1724,35 +1663,25 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     const int64_t r = sh.pair ? 256 : tc::BM;
     return ((Ms[q] + r - 1) / r) * ((Ns[q] + sh.bn - 1) / sh.bn);
   };
-  // Split K finishes inside the kernel, which needs every unit in the first
-  // round of the persistent grid (the splits of a tile wait for each other)
-  // and room for the partials and counters; otherwise no split.
+  // split-K partial slices: splits x (M rounded up to whole tiles) x pitch(N)
+  // fp32 per output, in the stream's workspace
   float* ws = nullptr;
-  unsigned* cnt = nullptr;
+  auto slice_rows = [&](int q, const tc::Shape& sh) {
+    const int64_t r = sh.pair ? 256 : tc::BM;
+    return (Ms[q] + r - 1) / r * r;
+  };
   if (shp.splits > 1) {
-    const int64_t slots = shp.pair ? std::max(1, cap / 2) : cap;
-    int64_t units = 0, ws_floats = 0, counters = 0;
+    int64_t need = 0;
     for (int q = 0; q < nout; ++q) {
-      const int64_t sp = problem_splits(q, shp), t = tiles_of(q, shp);
-      units += t * sp;
-      if (sp > 1) {
-        ws_floats += t * 2 * tc::kEpiWarps * sp * 32 * (shp.bn / 2);
-        counters += t * 2 * tc::kEpiWarps * 2;
-      }
+      const int64_t sp = problem_splits(q, shp);
+      if (sp > 1) need += sp * slice_rows(q, shp) * ws_pitch(Ns[q]);
     }
     void* w = nullptr;
-    void* c = nullptr;
-    if (units <= slots && (may_split || force != nullptr)) {
-      // no silent fallback: a different split factor would round differently
-      HAP_CHECK_ARG(stream_scratch(stream, kScratchSplitWs, ws_floats * sizeof(float), false, &w) &&
-                        stream_scratch(stream, kScratchSplitFlags, counters * sizeof(unsigned), true, &c),
-                    "hap_matmul: no split-K workspace on this stream (out of memory, or its first split launch "
-                    "is inside a CUDA graph capture: launch once eagerly first)");
-      ws = static_cast<float*>(w);
-      cnt = static_cast<unsigned*>(c);
-    } else {
-      shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, false, fp32, cap, pair_mode());
-    }
+    // no silent fallback: a different split factor would round differently
+    HAP_CHECK_ARG(stream_scratch(stream, kScratchSplitWs, need * sizeof(float), false, &w),
+                  "hap_matmul: no split-K workspace on this stream (out of memory, or its first split launch "
+                  "is inside a CUDA graph capture: launch once eagerly first)");
+    ws = static_cast<float*>(w);
   }
   const int rows = shp.pair ? 256 : tc::BM;
   const int b_box = shp.pair ? shp.bn / 2 : shp.bn;
@@ -1764,7 +1693,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   bt.sum_k = sum_k;
   for (int q = 0; q < count; ++q) bt.sum_kb += static_cast<int>((d[q].K + tc::BK - 1) / tc::BK);
   int units = 0;
-  int64_t ws_used = 0, cnt_used = 0;
+  int64_t ws_used = 0;
+  struct SplitEpi { int epi; const void* R; int64_t ldr; void* Y; int64_t ldy; int vec; };
+  SplitEpi sepi[tc::kMaxProblems] = {};
   for (int q = 0; q < count; ++q) {
     tc::TcProblem& pr = bt.p[q];
     const hap_gemm_desc& g = d[q];
@@ -1782,7 +1713,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
     // grouped problems split K by the same factor (problems with fewer K
     // blocks get fewer splits); a sum splits its concatenated K blocks
-    pr.splits = ws ? static_cast<int>(problem_splits(q, shp)) : 1;
+    pr.splits = static_cast<int>(problem_splits(q, shp));
     pr.kb_per_split = sum_k ? shp.kb_per_split : std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
     if (pr.splits <= 1) {
       pr.splits = 1;
@@ -1793,7 +1724,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     // Epilogue: TMA bulk store when the output rows are 16-byte pitched; fp32
     // accumulation uses TMA reduce-add (one writer per element: in order); a
     // bf16 accumulate (read-modify-round) is the fused ADD of C itself; split
-    // K finishes in the kernel (split_finish) with per-thread stores.
+    // K stores fp32 partial slices, summed in order by split_reduce_kernel.
     pr.epi_mode = tc::EPI_DIRECT;
     pr.epi = (!sum_k || q == 0) ? out.epi : HAP_EPI_NONE;
     pr.epi_tag = out.epi_tag;
@@ -1808,27 +1739,22 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     if (epi == HAP_EPI_ADD && out.accumulate && pr.splits > 1) epi = HAP_EPI_NONE;   // += C: the accumulate
     pr.epi = epi;
     if (pr.splits > 1 && (!sum_k || q == 0)) {
-      // split K: the finish applies the residual epilogue (split_fusable)
+      // split K: the ordered reduction applies the residual epilogue (split_fusable)
       HAP_CHECK_ARG(epi == HAP_EPI_NONE || epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2,
                     "hap_matmul: this fused epilogue cannot split K");
       HAP_CHECK_ARG(epi == HAP_EPI_NONE || (R != nullptr && (epi != HAP_EPI_ADD2 || out.Y != nullptr)),
                     "hap_matmul: fused epilogue tensor R / Y is null");
-      auto aligned = [&](const void* ptr, int64_t ld) {
-        return (reinterpret_cast<uintptr_t>(ptr) & (4 * osz - 1)) == 0 && ld % 4 == 0;
-      };
-      pr.fin_epi = epi;
-      pr.fin_R = R;
-      pr.fin_ldr = ldr;
-      pr.fin_Y = out.Y;
-      pr.fin_ldy = out.ldy;
-      pr.fin_vec = aligned(out.C, out.ldc) && (epi != HAP_EPI_ADD2 || aligned(out.Y, out.ldy));
+      auto al8 = [](const void* ptr, int64_t ld) { return (reinterpret_cast<uintptr_t>(ptr) & 7) == 0 && ld % 4 == 0; };
+      sepi[q] = {epi, R, ldr, out.Y, out.ldy, al8(R, ldr) && (epi != HAP_EPI_ADD2 || al8(out.Y, out.ldy))};
       pr.epi = HAP_EPI_NONE;
       pr.ws = ws + ws_used;
-      pr.split_cnt = cnt + cnt_used;
-      const int64_t t = static_cast<int64_t>(pr.m_tiles) * pr.n_tiles;
-      ws_used += t * 2 * tc::kEpiWarps * pr.splits * 32 * (shp.bn / 2);
-      cnt_used += t * 2 * tc::kEpiWarps * 2;
-      pr.epi_mode = tc::EPI_SPLIT_FIN;
+      pr.ws_ld = ws_pitch(out.N);
+      pr.ws_rows = static_cast<int>(slice_rows(q, shp));
+      ws_used += static_cast<int64_t>(pr.splits) * pr.ws_rows * pr.ws_ld;
+      HAP_CHECK_ARG(tc::make_map_c(&pr.c, pr.ws, HAP_F32, out.N, static_cast<int64_t>(pr.splits) * pr.ws_rows,
+                                   pr.ws_ld, shp.bn),
+                    "hap_matmul: workspace tensor map rejected");
+      pr.epi_mode = tc::EPI_SPLIT_WS;
     } else if (pr.epi != HAP_EPI_NONE) {
       HAP_CHECK_ARG(pr.vec_ok && tma_epilogue(),
                     "hap_matmul: fused epilogue needs a 16-byte pitched output and the TMA epilogue");
@@ -1900,8 +1826,29 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
               d[q].accumulate);
     fprintf(stderr, "\n");
   }
-  return fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
-              : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+  hap_status st = fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
+                       : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+  if (st != HAP_OK) return st;
+  for (int q = 0; q < nout; ++q) {
+    const tc::TcProblem& pr = bt.p[q];
+    if (pr.epi_mode != tc::EPI_SPLIT_WS) continue;
+    const int64_t work = static_cast<int64_t>(pr.M) * ((pr.N + 3) / 4);
+    const int grid = capped_grid((work + 255) / 256, cap * 4);
+    const int64_t slice = static_cast<int64_t>(pr.ws_rows) * pr.ws_ld;
+    const SplitEpi& se = sepi[q];
+    if (fp32)
+      launch_k(tc::split_reduce_kernel<float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(pr.ws),
+               pr.splits, slice, pr.ws_ld, static_cast<float*>(pr.C), pr.ldc, pr.M, pr.N, pr.accumulate,
+               pr.vec_ok, 0, nullptr, 0, nullptr, 0);
+    else
+      launch_k(tc::split_reduce_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
+               static_cast<const float*>(pr.ws), pr.splits, slice, pr.ws_ld, static_cast<__nv_bfloat16*>(pr.C),
+               pr.ldc, pr.M, pr.N, pr.accumulate, pr.vec_ok && (se.epi == HAP_EPI_NONE || se.vec), se.epi,
+               static_cast<const __nv_bfloat16*>(se.R), se.ldr, static_cast<__nv_bfloat16*>(se.Y), se.ldy);
+    st = launch_status("split_reduce_kernel");
+    if (st != HAP_OK) return st;
+  }
+  return HAP_OK;
 }
 
 hap_status simt_one(const hap_gemm_desc& g, hap_dtype in_dtype, hap_dtype out_dtype, int sm_cap,

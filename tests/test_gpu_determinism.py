@@ -3,8 +3,8 @@
 Sources of nondeterminism the executor removes (VERDICT r1 "what's weak" 2):
 timing-based tile / split-K choice (now the committed tuning table or the
 host heuristic, _lib.load_tune_table), split-K partials combined with
-floating-point atomics (now the ordered in-kernel finish, gemm.cu
-split_finish) and cross-CTA reduction atomics (now ticketed ordered sums,
+floating-point atomics (now fp32 partial slices summed in split order,
+gemm.cu split_reduce_kernel) and cross-CTA reduction atomics (now ticketed ordered sums,
 reduce.cu).  Shapes are forced through hap_matmul_tune_import, the same door
 the committed table uses."""
 import os
@@ -87,9 +87,9 @@ def test_tile_shape_does_not_change_the_bits(out, ta, tb):
 @pytest.mark.parametrize("splits", [2, 3, 4, 8])
 @pytest.mark.parametrize("pair", [1, 0])
 def test_split_k_fp32_accumulate_is_ordered(splits, pair):
-    """Weight-gradient shape (fp32 out, accumulate): the K splits finish the
-    tile in split order inside the kernel — 20 eager launches and a CUDA
-    graph replay give identical bits, and the result matches fp32 torch."""
+    """Weight-gradient shape (fp32 out, accumulate): the K splits' partial
+    tiles are summed in split order — 20 eager launches and a CUDA graph
+    replay give identical bits, and the result matches fp32 torch."""
     torch.manual_seed(splits)
     M, N, K = 768, 768, 4096
     a = torch.randn(K, M, device=DEV).to(torch.bfloat16)   # A^T . B  (dW = X^T dY)
@@ -127,7 +127,8 @@ def test_split_k_fp32_accumulate_is_ordered(splits, pair):
 @pytest.mark.parametrize("epi", ["none", "add2"])
 def test_split_k_bf16_residual_is_ordered(epi):
     """Few-token bf16 GEMM with the residual-add epilogue under split K: the
-    finish applies C = bf16(sum), Y = bf16(bf16(sum) + R) identically every run."""
+    ordered reduction applies C = bf16(sum), Y = bf16(bf16(sum) + R)
+    identically every run."""
     torch.manual_seed(5)
     M, N, K = 256, 768, 3072
     a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
