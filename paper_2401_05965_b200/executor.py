@@ -2153,10 +2153,16 @@ class Executor:
             self._run(self.ops_bwd)
             self._run(self.ops_upd)
 
-    def capture(self):
+    def capture(self, warmup: bool = True):
         """Record forward+backward+update into one CUDA graph (all ops were
-        compiled against self.stream, the capture stream)."""
-        self.step()  # warm-up outside capture (kernel attributes, NCCL setup)
+        compiled against self.stream, the capture stream).  ``warmup``: one
+        eager step first (kernel attributes, NCCL setup, per-stream
+        workspaces).  Ranks that live in one process (thread_peer_groups) warm
+        up together (their peer kernels wait for each other) and then capture
+        one after another with warmup=False: torch's graph capture frees cached
+        memory on entry, which would invalidate another thread's capture."""
+        if warmup:
+            self.step()
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         # thread-local capture: NCCL's proxy thread keeps issuing CUDA calls

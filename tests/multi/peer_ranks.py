@@ -58,7 +58,9 @@ def run_peer(doc, shapes, inputs, dtype, sync, capture):
                      for r in range(m)])
     run_ranks([lambda ex=ex: ex.load(inputs) for ex in exs])
     if capture:
-        run_ranks([lambda ex=ex: ex.capture() for ex in exs])
+        run_ranks([lambda ex=ex: ex.step() for ex in exs])   # warm up together, capture one by one
+        for ex in exs:
+            ex.capture(warmup=False)
         run_ranks([lambda ex=ex: ex.load(inputs) for ex in exs])
     run_ranks([lambda ex=ex: ex.step() for ex in exs])
     torch.cuda.synchronize()

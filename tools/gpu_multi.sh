@@ -1,0 +1,29 @@
+#!/bin/bash
+# One multi-GPU session under `gpurun --gpus N`: collective latency/bandwidth
+# sweeps for the cost model, NVLink counters of the peer-memory kernels (ncu,
+# one pass), bench lines (BERT, BERT-MoE with each gradient sync, ViT-MoE with
+# each collective implementation) and the NCCL-group parity run.  Outputs in
+# gpurun_out/m$N/.
+N=${1:-2}
+STEPS=${STEPS:-20}
+OUT=gpurun_out/m$N
+mkdir -p $OUT
+port=29500
+trun() { port=$((port + 1)); python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $port "$@"; }
+nvidia-smi topo -m > $OUT/topo.txt 2>&1
+timeout 900 trun tools/coll_fit.py --json $OUT/coll_fit.json > $OUT/coll_fit.log 2>&1; echo "coll_fit rc=$?" >> $OUT/status.txt
+timeout 300 trun tools/nvlink_ncu.py --json $OUT/nvl_events.json > $OUT/nvl_events.log 2>&1; echo "nvl_events rc=$?" >> $OUT/status.txt
+port=$((port + 1))
+timeout 900 ncu --target-processes all -k regex:p2p_ --clock-control none --csv \
+  --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum \
+  --log-file $OUT/nvl_ncu.csv python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+  --master-port $port tools/nvlink_ncu.py --calls 2 > $OUT/nvl_ncu.log 2>&1; echo "nvl_ncu rc=$?" >> $OUT/status.txt
+for args in "--workload bert" "--workload moe" "--workload moe --grad-sync sfb" "--workload moe --grad-sync all_reduce" \
+            "--workload vitmoe" "--workload vitmoe --collectives p2p" "--workload vitmoe --collectives nccl"; do
+  tag=$(echo $args | tr -d '-' | tr ' ' '_')
+  timeout 900 trun bench.py --gpus $N --steps $STEPS --warmup 5 $args > $OUT/bench_$tag.json 2> $OUT/bench_$tag.err
+  echo "bench $args rc=$?" >> $OUT/status.txt
+done
+if [ "${PARITY:-1}" = "1" ]; then
+  timeout 1800 trun tests/multi/nccl_parity.py > $OUT/parity.log 2>&1; echo "parity rc=$?" >> $OUT/status.txt
+fi

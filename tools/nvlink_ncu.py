@@ -1,0 +1,132 @@
+"""NVLink traffic of the peer-memory collectives, for an ncu capture of the
+NVLRX / NVLTX byte counters (one pass: no kernel replay, so the kernels'
+cross-GPU flag waits are safe under the profiler):
+
+    ncu --target-processes all -k regex:p2p_ --clock-control none --csv \\
+        --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,\\
+nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum \\
+        --log-file gpurun_out/nvl.csv \\
+        torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/nvlink_ncu.py
+
+Each rank runs, eagerly with a barrier between calls, the push all-gather,
+the direct reduce-scatter, the two-shot all-reduce and the push all-to-all of
+a [rows, 768] bf16 tensor sharded by the bench's SM-cap ratios (the executor's
+buffers, registered the same way), and prints the algorithmic bytes each rank
+must receive / send per call so the counters can be set against them
+(tools/summarize_nvlink.py).  Without ncu it prints CUDA-event times.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    from coll_fit import _register
+    from paper_2401_05965_b200 import workloads
+    from paper_2401_05965_b200._lib import BF16, check, lib
+    from paper_2401_05965_b200.sharding import offsets, round_shards
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", default="16384,65536")
+    ap.add_argument("--calls", type=int, default=3)
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    L = lib()
+    caps = workloads.sm_caps(world)
+    cap = caps[rank]
+    ratios = [c / sum(caps) for c in caps]
+    inner = 768
+    ctx = ctypes.c_void_p()
+    check(L.hap_symm_create(ctypes.byref(ctx), 1 << 20, rank, world))
+    h = ctypes.create_string_buffer(64)
+    check(L.hap_symm_handle(ctx, h))
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(h.raw))
+    check(L.hap_symm_open(ctx, b"".join(handles)))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    report = []
+    for rows in [int(v) for v in args.rows.split(",")]:
+        sizes = round_shards(rows, ratios)
+        offs = offsets(sizes)
+        counts = [sz * inner for sz in sizes]
+        devsz = torch.tensor([sizes, offs[:-1]], dtype=torch.int64, device=dev)
+        send = torch.randn(max(1, counts[rank]), device=dev).to(torch.bfloat16)
+        out = torch.empty(rows * inner, device=dev, dtype=torch.bfloat16)
+        outs = _register(L, ctx, out, world)
+        part = torch.randn(rows * inner, device=dev).to(torch.bfloat16)
+        parts = _register(L, ctx, part, world)
+        rs_out = torch.empty(max(1, counts[rank]), device=dev, dtype=torch.bfloat16)
+        ar = torch.randn(rows * inner, device=dev).to(torch.bfloat16)
+        ars = _register(L, ctx, ar, world)
+        csz = round_shards(inner, ratios)
+        send_counts = [sizes[rank] * c for c in csz]
+        recv_counts = [sizes[j] * csz[rank] for j in range(world)]
+        a2a_send = torch.randn(max(1, sum(send_counts)), device=dev).to(torch.bfloat16)
+        a2a_recv = torch.empty(max(1, sum(recv_counts)), device=dev, dtype=torch.bfloat16)
+        recvs = _register(L, ctx, a2a_recv, world)
+        dst_off = [sum(sizes[i] * csz[k] for i in range(rank)) for k in range(world)]
+        meta = torch.tensor([offsets(send_counts)[:-1], send_counts, dst_off], dtype=torch.int64, device=dev)
+        b = 2
+        ops = {
+            # name: (call, bytes received per rank, bytes sent per rank)
+            "all_gather_push": (lambda: L.hap_p2p_all_gather_push(ctx, send.data_ptr(), outs.data_ptr(), BF16, 1,
+                                                                  inner, rows, devsz[0].data_ptr(),
+                                                                  devsz[1].data_ptr(), rows * inner, cap, stream),
+                                (rows - sizes[rank]) * inner * b, (world - 1) * sizes[rank] * inner * b),
+            "reduce_scatter_direct": (lambda: L.hap_p2p_reduce_scatter_direct(ctx, parts.data_ptr(), rs_out.data_ptr(),
+                                                                              BF16, 1, inner, rows, devsz[0].data_ptr(),
+                                                                              devsz[1].data_ptr(), counts[rank], cap,
+                                                                              stream),
+                                      (world - 1) * sizes[rank] * inner * b, (rows - sizes[rank]) * inner * b),
+            "all_reduce": (lambda: L.hap_p2p_all_reduce(ctx, ars.data_ptr(), ars.data_ptr(), BF16, rows * inner, cap,
+                                                        stream),
+                           2 * (world - 1) * rows * inner * b // world, 2 * (world - 1) * rows * inner * b // world),
+            "all_to_all_push": (lambda: L.hap_p2p_all_to_all(ctx, a2a_send.data_ptr(), recvs.data_ptr(), BF16,
+                                                             meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
+                                                             max(send_counts), cap, stream),
+                                (sum(recv_counts) - recv_counts[rank]) * b, (sum(send_counts) - send_counts[rank]) * b),
+        }
+        for name, (fn, rx, tx) in ops.items():
+            times = []
+            for _ in range(args.calls):
+                dist.barrier()
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                check(fn(), name)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1))
+            report.append({"rank": rank, "op": name, "rows": rows, "rx_bytes": rx, "tx_bytes": tx,
+                           "event_ms_min": min(times)})
+    everyone = [None] * world
+    dist.all_gather_object(everyone, report)
+    if rank == 0:
+        flat = [r for sub in everyone for r in sub]
+        for r in flat:
+            print(json.dumps(r))
+        if args.json:
+            with open(args.json, "w") as fh:
+                json.dump({"world": world, "caps": caps, "calls": args.calls, "rows": args.rows, "ranks": flat}, fh,
+                          indent=1)
+    dist.barrier()
+    check(L.hap_symm_destroy(ctx))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
