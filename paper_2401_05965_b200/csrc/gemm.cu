@@ -403,6 +403,17 @@ struct alignas(64) TcBatch {
   long long sk_iters;      // I
   float* sk_ws;            // [P + 1][2 CTAs][128][BN] fp32 partial tiles
   unsigned* sk_flags;      // [P + 1][2 CTAs][8 epilogue warps]: partial written
+  // cluster split K (single-CTA kernel): csplit > 1 CTAs of one thread-block
+  // cluster share an output tile, CTA rank s walking the s-th slice of its K
+  // blocks; their fp32 partials meet in distributed shared memory and every
+  // CTA finishes 128 / csplit rows of the tile, adding the partials in rank
+  // order (cluster_split_finish)
+  int csplit;
+  // the residual epilogue the finish applies per problem (NONE / ADD / ADD2)
+  int fin_epi[kMaxProblems];
+  const void* fin_R[kMaxProblems];
+  void* fin_Y[kMaxProblems];
+  int64_t fin_ldr[kMaxProblems], fin_ldy[kMaxProblems];
 };
 
 __device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
@@ -631,10 +642,139 @@ struct Unit {
   int sk_slot;   // workspace slot of a cut tile
 };
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t cta) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(cta));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// ---- cluster split K (single-CTA kernel, TcBatch.csplit = S > 1)
+// Each CTA of the tile's cluster drains its 128 x BN fp32 accumulator into
+// its own (now idle) pipeline shared memory, row-major with the 16-byte
+// chunks of row r XOR-swizzled by (r & 7) (a warp's 32 rows hit all banks).
+// After a cluster barrier CTA s reduces rows [s * 128 / S, (s + 1) * 128 / S):
+// every float4 chunk is read from all S CTAs' shared memory through DSMEM
+// (mapa) and summed in rank order 0..S-1 — the same bits whatever the
+// timing — then + C when accumulating, the residual epilogue with the
+// unfused roundings (ADD: C = bf16(sum + R); ADD2: C = bf16(sum),
+// Y = bf16(bf16(sum) + R)), and stored.  A second cluster barrier keeps every
+// CTA's shared memory alive until all have read it.  The hardware schedules
+// a cluster's CTAs together, so these waits need no co-residency beyond the
+// cluster (unlike a grid-wide split finish).
+__device__ __forceinline__ uint32_t csplit_offset(int row, int chunk, int bn) {
+  return static_cast<uint32_t>(row * bn * 4 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int BN>
+__device__ __forceinline__ void csplit_drain(uint32_t tmem_acc, int quarter, int half, int lane, uint8_t* part,
+                                             bool empty) {
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
+  const uint32_t base = smem_u32(part);
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t r[32];
+    if (empty) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = 0u;   // an empty K slice contributes zeros
+    } else {
+      tmem_ld32(lane_base + c * 32, r);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int chunk = (half * (BN / 2) + c * 32) / 4 + j;
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + csplit_offset(row, chunk, BN)),
+                   "r"(r[4 * j]), "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3]));
+    }
+  }
+}
+
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
+}
+
+template <int BN, typename OutT>
+__device__ __forceinline__ void csplit_finish(const TcBatch& bt, const TcProblem& pr, int prob, int m0, int n0,
+                                              uint8_t* part, int rank, int S, int tid) {
+  constexpr int kChunks = BN / 4;   // float4 chunks per row
+  const int rows = 128 / S;
+  const int r0 = rank * rows;
+  const uint32_t base = smem_u32(part);
+  uint32_t peer[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    if (q < S) peer[q] = map_to_cta(base, static_cast<uint32_t>(q));
+  const int epi = bt.fin_epi[prob];
+  for (int k = tid; k < rows * kChunks; k += kEpiWarps * 32) {
+    const int row = r0 + k / kChunks, chunk = k % kChunks;
+    const uint32_t off = csplit_offset(row, chunk, BN);
+    float4 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q < S) v[q] = ld_dsmem_f4(peer[q] + off);
+    float4 a = v[0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q)
+      if (q < S) {
+        a.x += v[q].x; a.y += v[q].y; a.z += v[q].z; a.w += v[q].w;
+      }
+    const int grow = m0 + row, col = n0 + chunk * 4;
+    if (grow >= pr.M || col >= pr.N) continue;
+    float f[4] = {a.x, a.y, a.z, a.w};
+    const int valid = pr.N - col < 4 ? pr.N - col : 4;
+    OutT* dst = static_cast<OutT*>(pr.C) + static_cast<int64_t>(grow) * pr.ldc + col;
+    const bool vec = valid == 4 && pr.vec_ok;
+    if constexpr (std::is_same<OutT, float>::value) {
+      if (pr.accumulate) {
+        if (vec) {
+          const float4 o = *reinterpret_cast<const float4*>(dst);
+          f[0] += o.x; f[1] += o.y; f[2] += o.z; f[3] += o.w;
+        } else {
+          for (int j = 0; j < valid; ++j) f[j] += dst[j];
+        }
+      }
+      if (vec) *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+      else for (int j = 0; j < valid; ++j) dst[j] = f[j];
+    } else {
+      if (pr.accumulate)
+        for (int j = 0; j < valid; ++j) f[j] += __bfloat162float(dst[j]);
+      float x[4] = {0.f, 0.f, 0.f, 0.f};
+      if (epi != EPI_OP_NONE) {
+        const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(bt.fin_R[prob]) +
+                                 static_cast<int64_t>(grow) * bt.fin_ldr[prob] + col;
+        for (int j = 0; j < valid; ++j) x[j] = __bfloat162float(R[j]);
+      }
+      if (epi == EPI_OP_ADD)
+        for (int j = 0; j < 4; ++j) f[j] += x[j];
+      for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(f[j]);
+      if (epi == EPI_OP_ADD2) {
+        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(bt.fin_Y[prob]) + static_cast<int64_t>(grow) * bt.fin_ldy[prob]
+                           + col;
+        for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(f[j]) + x[j]);
+      }
+    }
+  }
+}
+
 // Work unit u -> (problem, output tile, K-block range).  Grouped: units are
 // laid out problem after problem; within a problem unit = split * tiles + tile.
 template <int ROWS, int BN>
 __device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
+  const int S = bt.csplit > 1 ? bt.csplit : 1;
+  const int cs = u % S;   // cluster split: CTA rank within the tile's cluster
+  u /= S;
   int p = 0;
   if (!bt.sum_k)
     while (p + 1 < bt.count && u >= bt.p[p + 1].unit_begin) ++p;
@@ -650,6 +790,13 @@ __device__ __forceinline__ Unit decode_unit(const TcBatch& bt, int u) {
   x.n0 = (t / pr.m_tiles) * BN;
   x.kb0 = (local / tiles) * pr.kb_per_split;
   x.kb1 = min(bt.sum_k ? bt.sum_kb : pr.k_blocks, x.kb0 + pr.kb_per_split);
+  if (S > 1) {
+    const int kb = bt.sum_k ? bt.sum_kb : pr.k_blocks;
+    const int per = (kb + S - 1) / S;
+    x.split = cs;
+    x.kb0 = min(kb, cs * per);
+    x.kb1 = min(kb, x.kb0 + per);
+  }
   return x;
 }
 
@@ -854,8 +1001,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       const TcProblem& pr = bt.p[x.prob];
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
-                              buf, box_seq, ld_bar, ld_phase, nullptr);
+      if (bt.csplit > 1) {
+        // cluster split K: the partial goes to this CTA's shared memory (the
+        // pipeline stages are idle: this was the CTA's only unit); the
+        // cluster reduces it after the loop
+        fence_async_smem();
+        csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+      } else {
+        epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
+                                buf, box_seq, ld_bar, ld_phase, nullptr);
+      }
       tc_fence_before();
       mbar_arrive(tempty0 + 8 * acc);
       acc ^= 1;
@@ -863,6 +1018,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
     hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
+  }
+  if (bt.csplit > 1) {   // every thread of every CTA of the cluster takes part in both barriers
+    cluster_sync_all();   // all partials are in shared memory
+    if (warp >= 4 && static_cast<int>(blockIdx.x) < num_units) {
+      const Unit x = decode_unit<BM, BN>(bt, blockIdx.x);
+      csplit_finish<BN, OutT>(bt, bt.p[x.prob], x.prob, x.m0, x.n0, smem, static_cast<int>(cluster_rank()), bt.csplit,
+                              threadIdx.x - 128);
+    }
+    cluster_sync_all();   // every peer has read this CTA's partial
   }
   tc_fence_before();
   __syncthreads();
@@ -896,19 +1060,6 @@ struct Cfg2 {
 };
 
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t cta) {
-  uint32_t out;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(cta));
-  return out;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
@@ -1191,7 +1342,7 @@ bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_
 
 template <typename K>
 hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cudaStream_t stream,
-                        const char* what) {
+                        const char* what, int cluster = 0) {
   static_assert(sizeof(TcBatch) < 4096, "TcBatch must fit the kernel parameter space");
   // per-instantiation once: large dynamic shared memory
   static std::mutex mu;
@@ -1202,6 +1353,25 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
       HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
       configured.push_back(reinterpret_cast<const void*>(kern));
     }
+  }
+  if (cluster > 1) {
+    set_carveout(kern);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, kern, bt);
+    return launch_status(what);
   }
   launch_k(kern, dim3(grid), dim3(kThreads), smem_bytes, stream, bt);
   return launch_status(what);
@@ -1215,6 +1385,9 @@ hap_status launch_shape(bool pair, const TcBatch& bt, int cap, cudaStream_t stre
                         "gemm_tc2_kernel");
   }
   if constexpr (BN != 192) {
+    if (bt.csplit > 1)   // one CTA per unit, the splits of a tile one cluster
+      return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, bt.total_units, stream,
+                          "gemm_tc_kernel (cluster split K)", bt.csplit);
     return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, std::min(bt.total_units, cap),
                         stream, "gemm_tc_kernel");
   }
@@ -1243,7 +1416,12 @@ hap_status launch_dispatch(bool pair, int bn, bool amn, bool bmn, const TcBatch&
 struct Shape {
   int bn, splits, kb_per_split;
   bool pair;
+  bool cl = false;   // split K over a thread-block cluster (single-CTA tiles, DSMEM reduction)
 };
+
+// Cluster split factors: a cluster of S single-CTA tiles (portable size
+// <= 8) whose rows divide 128 evenly.
+inline bool cluster_split_ok(int64_t splits) { return splits == 2 || splits == 4 || splits == 8; }
 
 Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
                    bool fp32_out, int cap, int allow_pair) {
@@ -1293,12 +1471,40 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
                 static_cast<double>(rounds * kps) * t_kb};
     }
   }
-  // Split K stores fp32 partial slices and sums them in order in a second
-  // launch (split_reduce_kernel): a serial tail (~5 us measured on B200),
-  // so split only when the shortened K walk saves more than that.
-  constexpr double kSplitTailUs = 5.0;
-  if (split.score > 0 && split.est_us + kSplitTailUs < plain.est_us) return split.s;
-  return plain.score > 0 ? plain.s : split.s;
+  // Cluster split K (single-CTA tiles): the S splits of a tile reduce through
+  // distributed shared memory inside the launch — a ~1 us tail.
+  Pick cl = plain;
+  cl.score = -1.0;
+  if (allow_split && k_blocks >= 8) {
+    for (const Cand& c : cands) {
+      if (c.pair) continue;
+      int64_t tiles = 0;
+      for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + 127) / 128) * ((Ns[q] + c.bn - 1) / c.bn);
+      const double t_kb = 0.26 * c.bn / 256.0 / c.weight;
+      for (int64_t S = 2; S <= 8; S *= 2) {
+        if (tiles * S > cap || k_blocks / S < 2) break;
+        const int64_t kps = (k_blocks + S - 1) / S;
+        if ((S - 1) * kps >= k_blocks) continue;   // every split walks at least one K block
+        const double est = static_cast<double>(kps) * t_kb;
+        if (cl.score < 0 || est < cl.est_us) {
+          cl = {{c.bn, static_cast<int>(S), static_cast<int>(kps), false}, 1.0, est};
+          cl.s.cl = true;
+        }
+      }
+    }
+  }
+  // Split K through the workspace stores fp32 partial slices and sums them in
+  // order in a second launch (split_reduce_kernel): a serial tail (~5 us
+  // measured on B200), so split only when the shortened K walk saves more.
+  constexpr double kSplitTailUs = 5.0, kClusterTailUs = 1.0;
+  double best_us = plain.score > 0 ? plain.est_us : 1e30;
+  Shape best = plain.score > 0 ? plain.s : split.s;
+  if (split.score > 0 && split.est_us + kSplitTailUs < best_us) {
+    best_us = split.est_us + kSplitTailUs;
+    best = split.s;
+  }
+  if (cl.score > 0 && cl.est_us + kClusterTailUs < best_us) best = cl.s;
+  return best;
 }
 
 // Every tile shape / split choose_shape considers (the autotuner times them).
@@ -1328,8 +1534,18 @@ void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, i
       if (splits < 2) continue;
       Shape sh{c.bn, static_cast<int>(splits), static_cast<int>(kps), c.pair};
       bool dup = false;
-      for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits);
+      for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits && !o.cl);
       if (!dup) out.push_back(sh);
+    }
+    if (!c.pair) {   // cluster split K of the single-CTA tiles
+      for (int64_t S = 2; S <= 8; S *= 2) {
+        if (tiles * S > cap || k_blocks / S < 2) break;
+        const int64_t kps = (k_blocks + S - 1) / S;
+        if ((S - 1) * kps >= k_blocks) continue;
+        Shape sh{c.bn, static_cast<int>(S), static_cast<int>(kps), false};
+        sh.cl = true;
+        out.push_back(sh);
+      }
     }
   }
 }
@@ -1670,7 +1886,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     const int64_t r = sh.pair ? 256 : tc::BM;
     return (Ms[q] + r - 1) / r * r;
   };
-  if (shp.splits > 1) {
+  const bool csplit = shp.cl && shp.splits > 1 && !shp.pair && tc::cluster_split_ok(shp.splits);
+  if (shp.cl && !csplit) shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, false, fp32, cap, pair_mode());
+  if (shp.splits > 1 && !csplit) {
     int64_t need = 0;
     for (int q = 0; q < nout; ++q) {
       const int64_t sp = problem_splits(q, shp);
@@ -1713,7 +1931,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     pr.k_blocks = static_cast<int>((g.K + tc::BK - 1) / tc::BK);
     // grouped problems split K by the same factor (problems with fewer K
     // blocks get fewer splits); a sum splits its concatenated K blocks
-    pr.splits = static_cast<int>(problem_splits(q, shp));
+    pr.splits = csplit ? 1 : static_cast<int>(problem_splits(q, shp));
     pr.kb_per_split = sum_k ? shp.kb_per_split : std::max(1, std::min(shp.kb_per_split, pr.k_blocks));
     if (pr.splits <= 1) {
       pr.splits = 1;
@@ -1738,7 +1956,21 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     }
     if (epi == HAP_EPI_ADD && out.accumulate && pr.splits > 1) epi = HAP_EPI_NONE;   // += C: the accumulate
     pr.epi = epi;
-    if (pr.splits > 1 && (!sum_k || q == 0)) {
+    if (csplit && (!sum_k || q == 0)) {
+      // cluster split K: the DSMEM finish applies accumulate and the residual
+      // epilogue (split_fusable)
+      HAP_CHECK_ARG(epi == HAP_EPI_NONE || epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2,
+                    "hap_matmul: this fused epilogue cannot split K");
+      HAP_CHECK_ARG(epi == HAP_EPI_NONE || (R != nullptr && (epi != HAP_EPI_ADD2 || out.Y != nullptr)),
+                    "hap_matmul: fused epilogue tensor R / Y is null");
+      bt.fin_epi[q] = epi;
+      bt.fin_R[q] = R;
+      bt.fin_ldr[q] = ldr;
+      bt.fin_Y[q] = out.Y;
+      bt.fin_ldy[q] = out.ldy;
+      pr.epi = HAP_EPI_NONE;
+      pr.epi_mode = tc::EPI_DIRECT;
+    } else if (pr.splits > 1 && (!sum_k || q == 0)) {
       // split K: the ordered reduction applies the residual epilogue (split_fusable)
       HAP_CHECK_ARG(epi == HAP_EPI_NONE || epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2,
                     "hap_matmul: this fused epilogue cannot split K");
@@ -1792,6 +2024,10 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     if (!sum_k || q == 0) units += pr.m_tiles * pr.n_tiles * pr.splits;
   }
   bt.total_units = units;
+  if (csplit) {
+    bt.csplit = shp.splits;
+    bt.total_units = units * shp.splits;
+  }
   // stream-K: one problem on SM pairs whose data-parallel rounds would leave
   // pairs idle (tile counts are products of 2s and 3s, the pair count 74 is
   // 2 x 37: the last round is rarely full).  Every pair gets the same number
@@ -1817,9 +2053,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   }
   static const bool log_shapes = getenv("HAP_GEMM_LOG") != nullptr;
   if (log_shapes) {
-    fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d kbps %d units %d sk %d |",
+    fprintf(stderr, "[hap gemm] count %d sum_k %d out %s cap %d -> %s BN %d splits %d%s kbps %d units %d sk %d |",
             count, sum_k, fp32 ? "f32" : "bf16", cap, shp.pair ? "pair" : "cta", shp.bn, shp.splits,
-            shp.kb_per_split, units, bt.sk);
+            csplit ? " (cluster)" : "", shp.kb_per_split, units, bt.sk);
     for (int q = 0; q < count; ++q)
       fprintf(stderr, " %lldx%lldx%lld t%d%d epi%d acc%d", static_cast<long long>(d[q].M),
               static_cast<long long>(d[q].N), static_cast<long long>(d[q].K), d[q].transA, d[q].transB, d[q].epi,
@@ -1828,6 +2064,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
   }
   hap_status st = fp32 ? tc::launch_dispatch<float>(shp.pair, shp.bn, amn, bmn, bt, cap, stream)
                        : tc::launch_dispatch<__nv_bfloat16>(shp.pair, shp.bn, amn, bmn, bt, cap, stream);
+  if (st != HAP_OK || csplit) return st;
   if (st != HAP_OK) return st;
   for (int q = 0; q < nout; ++q) {
     const tc::TcProblem& pr = bt.p[q];
@@ -2103,7 +2340,8 @@ extern "C" int64_t hap_matmul_tune_export(char* buf, int64_t cap) {
   std::string text;
   for (const auto& r : rows)
     text += r.first + "\t" + std::to_string(r.second.pair ? 1 : 0) + " " + std::to_string(r.second.bn) + " " +
-            std::to_string(r.second.splits) + " " + std::to_string(r.second.kb_per_split) + "\n";
+            std::to_string(r.second.splits) + " " + std::to_string(r.second.kb_per_split) + " " +
+            std::to_string(r.second.cl ? 1 : 0) + "\n";
   const int64_t need = static_cast<int64_t>(text.size()) + 1;
   if (buf && cap >= need) std::memcpy(buf, text.c_str(), static_cast<size_t>(need));
   return need;
@@ -2119,13 +2357,17 @@ extern "C" hap_status hap_matmul_tune_import(const char* text) {
     p = eol ? eol + 1 : p + line.size();
     if (line.empty()) continue;
     const size_t tab = line.find('\t');
-    int pair = 0, bn = 0, splits = 0, kbps = 0;
-    HAP_CHECK_ARG(tab != std::string::npos &&
-                      std::sscanf(line.c_str() + tab + 1, "%d %d %d %d", &pair, &bn, &splits, &kbps) == 4,
-                  "hap_matmul_tune_import: malformed line: " + line);
-    HAP_CHECK_ARG((bn == 128 || bn == 256 || (bn == 192 && pair)) && splits >= 1 && kbps >= 1,
+    int pair = 0, bn = 0, splits = 0, kbps = 0, cl = 0;
+    const int got = tab == std::string::npos ? 0
+                                             : std::sscanf(line.c_str() + tab + 1, "%d %d %d %d %d", &pair, &bn,
+                                                           &splits, &kbps, &cl);
+    HAP_CHECK_ARG(got == 4 || got == 5, "hap_matmul_tune_import: malformed line: " + line);
+    HAP_CHECK_ARG((bn == 128 || bn == 256 || (bn == 192 && pair)) && splits >= 1 && kbps >= 1 &&
+                      (!cl || (!pair && tc::cluster_split_ok(splits))),
                   "hap_matmul_tune_import: bad shape: " + line);
-    rows.push_back({line.substr(0, tab), tc::Shape{bn, splits, kbps, pair != 0}});
+    tc::Shape shape{bn, splits, kbps, pair != 0};
+    shape.cl = cl != 0;
+    rows.push_back({line.substr(0, tab), shape});
   }
   std::lock_guard<std::mutex> lock(tune_mutex());
   for (const auto& r : rows) tune_cache()[r.first] = r.second;

@@ -907,6 +907,15 @@ class Executor:
         # stream are ordered, calls on two streams must not share flags
         return "side" if self._emit_on is not None else "main"
 
+    SIDE_P2P_CTAS = 32
+
+    def _p2p_cap(self, tag: str) -> int:
+        """Grid cap of a peer kernel: the rank's SM cap; on the side stream at
+        most SIDE_P2P_CTAS, so a spinning side-stream kernel leaves the
+        compute stream's persistent GEMM most of the GPU."""
+        cap = self.caps[self.group.rank] or 148
+        return min(cap, self.SIDE_P2P_CTAS) if tag == "side" else cap
+
     def _register(self, tag: str, buf: Buf) -> dict:
         """A buffer every peer maps (push outputs, in-place partials): the
         device array of all ranks' pointers to it is filled in by
@@ -926,7 +935,7 @@ class Executor:
         self._p2p_bytes[tag] = max(self._p2p_bytes.get(tag, 0), arena_bytes)
         fn_ptr = getattr(self.lib, fn)
         stream = self._sptr()
-        cap = self.caps[r]
+        cap = self._p2p_cap(tag)
         sizes_ptr, offs_ptr = dev[0].data_ptr(), dev[1].data_ptr()
         if fn == "hap_p2p_all_gather_push":
             reg = self._register(tag, recv)
@@ -957,7 +966,7 @@ class Executor:
         reg_out = reg_in if dst is src else self._register(tag, dst)
         fn = self.lib.hap_p2p_all_reduce
         stream = stream_ptr if stream_ptr is not None else self._sptr()
-        cap = self.caps[self.group.rank]
+        cap = self._p2p_cap(tag)
         dt = src.dtype
         self._ops.append(Op(lambda: fn(self._symm[tag], reg_in["dev"].data_ptr(), reg_out["dev"].data_ptr(), dt, n,
                                        cap, stream), (), "hap_p2p_all_reduce", True,
@@ -971,7 +980,7 @@ class Executor:
         self._keep(dev)
         fn = self.lib.hap_p2p_all_to_all
         stream = self._sptr()
-        cap = self.caps[self.group.rank]
+        cap = self._p2p_cap(tag)
         most = max(max(counts), 1)
         self._ops.append(Op(lambda: fn(self._symm[tag], send.ptr, reg["dev"].data_ptr(), send.dtype,
                                        dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), most, cap, stream),
@@ -1761,7 +1770,18 @@ class Executor:
 
     def _sfb_overlap(self) -> bool:
         g = self.group
-        return bool(self.sfb) and g.distributed and self.cfg.overlap_sfb and (g.comm_grad is not None or g.comm is None)
+        return bool(self.sfb) and self._side_streams() and self.cfg.overlap_sfb
+
+    def _side_streams(self) -> bool:
+        """Collectives may run on a side stream beside the compute stream
+        (SFB factor gathers, bucketed gradient all-reduces): one process per
+        GPU only.  Ranks sharing one GPU in one process (thread_peer_groups)
+        keep every collective on their compute stream: each rank then has one
+        kernel at a time within its SM cap, the caps sum to the GPU, and a
+        rank's persistent GEMM can never be starved of SMs by another rank's
+        peer kernel spinning for a partner that is queued behind that GEMM."""
+        g = self.group
+        return g.distributed and not getattr(g, "in_process", False) and (g.comm_grad is not None or g.comm is None)
 
     def _sfb_factor(self, did: str, bufs: dict) -> dict:
         """Row-gathered copy of an SFB factor (an activation or an output
@@ -1838,7 +1858,7 @@ class Executor:
         neighbouring gradients sync as one bucket (one large all-reduce runs
         at NCCL's bandwidth; dozens of small ones pay its latency each)."""
         g = self.group
-        if not g.distributed or self.m == 1 or (g.comm_grad is None and g.comm is not None):
+        if self.m == 1 or not self._side_streams():
             return
         first_use: dict = {}
         for i, ins in enumerate(self.program.instrs):
@@ -1869,8 +1889,7 @@ class Executor:
         the remaining backward kernels; the compute stream joins the side
         stream before the update."""
         g = self.group
-        if not g.distributed or self.m == 1 or (g.comm_grad is None and g.comm is not None) \
-                or not hasattr(self, "_flat"):
+        if self.m == 1 or not self._side_streams() or not hasattr(self, "_flat"):
             return
         flat, place = self._flat
         ready = {f.output: self._grad_ready_at[f.output] for f in self._synced_params()

@@ -1,4 +1,5 @@
-"""Split-K A/B on the few-tile GEMM shapes (MoE 256-token stack, BERT weight
+"""Split-K A/B on the few-tile GEMM shapes (suffix c: cluster split K, DSMEM
+reduction; no suffix: workspace slices + ordered reduction kernel) (MoE 256-token stack, BERT weight
 gradients): every tile shape x split candidate forced through the tuning
 table, CUDA-graph timed (20 launches per graph).  With --lib PATH a second
 build (e.g. the round-1 library, abtest/libgemm_r01.so) is timed the same
@@ -91,9 +92,10 @@ def main():
                 if sp > 1 and (tiles * sp > slots or kb // sp < 2):
                     continue
                 kbps = -(-kb // sp)
-                L.hap_matmul_tune_import(f"{key}\t{pair} {bn} {sp} {kbps}\n".encode())
-                us = graph_us(lambda: L.hap_matmul_batch(d, 1, 0, BF16, odt, 0, s.cuda_stream), s)
-                res.append((us, f"{'pair' if pair else 'cta'}{bn}/s{sp}"))
+                for cl in ((0, 1) if (not pair and sp in (2, 4, 8)) else (0,)):
+                    L.hap_matmul_tune_import(f"{key}\t{pair} {bn} {sp} {kbps} {cl}\n".encode())
+                    us = graph_us(lambda: L.hap_matmul_batch(d, 1, 0, BF16, odt, 0, s.cuda_stream), s)
+                    res.append((us, f"{'pair' if pair else 'cta'}{bn}/s{sp}{'c' if cl else ''}"))
         L.hap_matmul_tune_clear()
         res.sort()
         heur = graph_us(lambda: L.hap_matmul_batch(d, 1, 0, BF16, odt, 0, s.cuda_stream), s)
