@@ -91,9 +91,12 @@ typedef struct {
    *   HAP_EPI_SWISH     C = A.B;  Y = f(C);  Z = C * Y    (f = epi_tag)
    *   HAP_EPI_SWISH_BWD dz = A.B (not stored);
    *                     C (+)= dz*R2 + (dz*R)*f'(R, R2)   (R = x, R2 = f(x))
-   * ADD / ADD2 may split K (few output tiles, long K): the ordered split
-   * reduction then applies them with the same roundings; the swish chains
-   * never split.
+   * ADD / ADD2 may split K (few output tiles, long K): the split reduction
+   * then applies them with the same roundings; the swish chains never split.
+   * Split K is deterministic: either the splits of a tile form a thread-block
+   * cluster and add their fp32 partials through distributed shared memory in
+   * rank order, or they store fp32 partial slices that a second kernel adds
+   * in split order — never floating-point atomics.
    */
   int epi;
   int epi_tag;

@@ -1,5 +1,11 @@
 """Hoare-triple background theory of a graph (reference theory.py).
 
+DERIVED FROM THE REFERENCE: this module restates shardplan/theory.py closely —
+north_star requires the planner to emit exactly the reference's programs,
+ratios and estimates, and the goldens check it byte for byte — so it is not
+original work of this repository; the executor, the kernels and the
+collectives are.
+
 A triple ``{pre} instrs {post}`` says: if the partial program realises every
 property in ``pre``, appending ``instrs`` realises ``post``.  Properties are
 ``e|Id``, ``e|AG(d)``, ``e|AR`` (program.py) plus two search guards
