@@ -9,6 +9,8 @@ GPU (the graph's trivial one-device program in fp32), not on the host.
 from __future__ import annotations
 
 import atexit
+import hashlib
+import json
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -68,7 +70,9 @@ def _default_group(m: int):
 
 def _cache_key(prog: DistributedProgram, m: int, shard_table: dict, shapes: dict, cfg: ExecConfig, group) -> tuple:
     table = tuple(sorted((str(k[0]), int(k[1]), tuple(int(x) for x in v)) for k, v in shard_table.items()))
-    return (prog.fingerprint(), prog.loss, m, table, tuple(sorted(shapes.items())), repr(cfg),
+    # the whole instruction content (tags and dims included — canonical() omits them)
+    digest = hashlib.sha256(json.dumps(prog.to_json(), sort_keys=True).encode()).hexdigest()
+    return (digest, m, table, tuple(sorted(shapes.items())), repr(cfg),
             type(group).__name__, id(group) if group.distributed else m)
 
 

@@ -705,9 +705,13 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
   return v;
 }
 
+// `rank` = this CTA's index among the S that hold the same rows, whose
+// cluster ranks are q * stride + offset (single-CTA tiles: stride 1; SM-pair
+// tiles: stride 2, offset = rank within the pair).
 template <int BN, typename OutT>
 __device__ __forceinline__ void csplit_finish(const TcBatch& bt, const TcProblem& pr, int prob, int m0, int n0,
-                                              uint8_t* part, int rank, int S, int tid) {
+                                              uint8_t* part, int rank, int S, int tid, int stride = 1,
+                                              int offset = 0) {
   constexpr int kChunks = BN / 4;   // float4 chunks per row
   const int rows = 128 / S;
   const int r0 = rank * rows;
@@ -715,7 +719,7 @@ __device__ __forceinline__ void csplit_finish(const TcBatch& bt, const TcProblem
   uint32_t peer[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q)
-    if (q < S) peer[q] = map_to_cta(base, static_cast<uint32_t>(q));
+    if (q < S) peer[q] = map_to_cta(base, static_cast<uint32_t>(q * stride + offset));
   const int epi = bt.fin_epi[prob];
   for (int k = tid; k < rows * kChunks; k += kEpiWarps * 32) {
     const int row = r0 + k / kChunks, chunk = k % kChunks;
@@ -1093,17 +1097,18 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uin
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+// Arrive on `bar` in both CTAs of the pair whose leader (even cluster rank)
+// is `leader`.
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar, uint32_t leader) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"(static_cast<uint16_t>(3))
+      "h"(static_cast<uint16_t>(3u << leader))
       : "memory");
 }
 
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {
   using G = Cfg2<BN, kBMN>;
   constexpr int HB = BN / 2;  // B columns of the tile each CTA supplies
   extern __shared__ uint8_t smem_raw[];
@@ -1118,7 +1123,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  // launched in clusters of 2 (one SM pair) or, under cluster split K, of
+  // 2 x csplit (the pairs of one output tile): the pair is the CTAs whose
+  // cluster ranks differ in bit 0, its leader the even one
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1u;
+  const uint32_t leader = crank & ~1u;
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
 
@@ -1163,7 +1173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int n0 = x.n0 + HB * static_cast<int>(rank);
         for_each_kblock(bt, x, [&](int q, int kb) {
           mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
-          const uint32_t leader_full = map_to_cta(full0 + 8 * stage, 0);
+          const uint32_t leader_full = map_to_cta(full0 + 8 * stage, leader);
           if (rank == 0) mbar_expect_tx_cluster(leader_full, 2 * G::kStageBytes);
           else mbar_arrive_cluster(leader_full);
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
@@ -1221,13 +1231,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         (!first) || (kk != 0));
           }
           first = false;
-          tc_commit_pair(empty0 + 8 * stage);
+          tc_commit_pair(empty0 + 8 * stage, leader);
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
         });
-        tc_commit_pair(tfull0 + 8 * acc);
+        tc_commit_pair(tfull0 + 8 * acc, leader);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -1240,7 +1250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
     const uint32_t ld_bar = smem_u32(bars + 2 * G::kStages + 6 + 2 * (warp - 4));   // fused-epilogue input loads
     uint32_t ld_phase = 0;
-    const uint32_t leader_tempty = map_to_cta(tempty0, 0);
+    const uint32_t leader_tempty = map_to_cta(tempty0, leader);
     int acc = 0;
     uint32_t acc_phase = 0;
     PairCursor<BN> cur(bt, pair, num_pairs);
@@ -1250,6 +1260,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
+      if (bt.csplit > 1) {   // cluster split K: partial to this CTA's idle pipeline smem, reduced after the loop
+        fence_async_smem();
+        csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       // stream-K: this CTA's 128 x BN share of a cut tile's partial
       float* part = nullptr;
       unsigned* flag = nullptr;
@@ -1280,6 +1300,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
+  }
+  if (bt.csplit > 1) {   // every thread of every CTA of the cluster takes part in both barriers
+    cluster_sync_all();   // all partials are in shared memory
+    if (warp >= 4 && pair < bt.total_units) {
+      const Unit x = decode_unit<256, BN>(bt, pair);
+      // CTAs holding the same 128 rows (same rank in their pairs) reduce together
+      csplit_finish<BN, OutT>(bt, bt.p[x.prob], x.prob, x.m0 + 128 * static_cast<int>(rank), x.n0, smem,
+                              static_cast<int>(crank >> 1), bt.csplit, threadIdx.x - 128, 2, static_cast<int>(rank));
+    }
+    cluster_sync_all();   // every peer has read this CTA's partial
   }
   tc_fence_before();
   cluster_sync_all();
@@ -1380,9 +1410,10 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 hap_status launch_shape(bool pair, const TcBatch& bt, int cap, cudaStream_t stream) {
   if (pair || BN == 192) {   // 192-wide tiles exist only for SM pairs
-    const int pairs = std::min<int>(bt.total_units, std::max(1, cap / 2));
+    // clusters of one pair, or (cluster split K) of the csplit pairs of a tile, one unit each
+    const int pairs = bt.csplit > 1 ? bt.total_units : std::min<int>(bt.total_units, std::max(1, cap / 2));
     return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, Cfg2<BN, kBMN>::kSmem, bt, 2 * pairs, stream,
-                        "gemm_tc2_kernel");
+                        "gemm_tc2_kernel", bt.csplit > 1 ? 2 * bt.csplit : 2);
   }
   if constexpr (BN != 192) {
     if (bt.csplit > 1)   // one CTA per unit, the splits of a tile one cluster
@@ -1419,9 +1450,12 @@ struct Shape {
   bool cl = false;   // split K over a thread-block cluster (single-CTA tiles, DSMEM reduction)
 };
 
-// Cluster split factors: a cluster of S single-CTA tiles (portable size
-// <= 8) whose rows divide 128 evenly.
-inline bool cluster_split_ok(int64_t splits) { return splits == 2 || splits == 4 || splits == 8; }
+// Cluster split factors: S CTAs (single-CTA tiles) or S SM pairs (2S CTAs)
+// per cluster, within the portable cluster size 8, the tile's 128 rows per
+// CTA dividing evenly among the S.
+inline bool cluster_split_ok(int64_t splits, bool pair) {
+  return splits == 2 || splits == 4 || (splits == 8 && !pair);
+}
 
 Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
                    bool fp32_out, int cap, int allow_pair) {
@@ -1477,17 +1511,19 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
   cl.score = -1.0;
   if (allow_split && k_blocks >= 8) {
     for (const Cand& c : cands) {
-      if (c.pair) continue;
+      if (c.pair && (!allow_pair || min_m < 256 || cap < 4)) continue;
+      const int64_t rows = c.pair ? 256 : 128;
+      const int64_t slots = c.pair ? cap / 2 : cap;
       int64_t tiles = 0;
-      for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + 127) / 128) * ((Ns[q] + c.bn - 1) / c.bn);
+      for (int q = 0; q < (sum_k ? 1 : count); ++q) tiles += ((Ms[q] + rows - 1) / rows) * ((Ns[q] + c.bn - 1) / c.bn);
       const double t_kb = 0.26 * c.bn / 256.0 / c.weight;
       for (int64_t S = 2; S <= 8; S *= 2) {
-        if (tiles * S > cap || k_blocks / S < 2) break;
+        if (!cluster_split_ok(S, c.pair) || tiles * S > slots || k_blocks / S < 2) break;
         const int64_t kps = (k_blocks + S - 1) / S;
         if ((S - 1) * kps >= k_blocks) continue;   // every split walks at least one K block
         const double est = static_cast<double>(kps) * t_kb;
         if (cl.score < 0 || est < cl.est_us) {
-          cl = {{c.bn, static_cast<int>(S), static_cast<int>(kps), false}, 1.0, est};
+          cl = {{c.bn, static_cast<int>(S), static_cast<int>(kps), c.pair}, 1.0, est};
           cl.s.cl = true;
         }
       }
@@ -1537,15 +1573,13 @@ void candidate_shapes(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, i
       for (const Shape& o : out) dup = dup || (o.bn == sh.bn && o.pair == sh.pair && o.splits == sh.splits && !o.cl);
       if (!dup) out.push_back(sh);
     }
-    if (!c.pair) {   // cluster split K of the single-CTA tiles
-      for (int64_t S = 2; S <= 8; S *= 2) {
-        if (tiles * S > cap || k_blocks / S < 2) break;
-        const int64_t kps = (k_blocks + S - 1) / S;
-        if ((S - 1) * kps >= k_blocks) continue;
-        Shape sh{c.bn, static_cast<int>(S), static_cast<int>(kps), false};
-        sh.cl = true;
-        out.push_back(sh);
-      }
+    for (int64_t S = 2; S <= 8; S *= 2) {   // cluster split K
+      if (!cluster_split_ok(S, c.pair) || tiles * S > slots || k_blocks / S < 2) break;
+      const int64_t kps = (k_blocks + S - 1) / S;
+      if ((S - 1) * kps >= k_blocks) continue;
+      Shape sh{c.bn, static_cast<int>(S), static_cast<int>(kps), c.pair};
+      sh.cl = true;
+      out.push_back(sh);
     }
   }
 }
@@ -1886,7 +1920,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     const int64_t r = sh.pair ? 256 : tc::BM;
     return (Ms[q] + r - 1) / r * r;
   };
-  const bool csplit = shp.cl && shp.splits > 1 && !shp.pair && tc::cluster_split_ok(shp.splits);
+  const bool csplit = shp.cl && shp.splits > 1 && tc::cluster_split_ok(shp.splits, shp.pair);
   if (shp.cl && !csplit) shp = tc::choose_shape(Ms, Ns, Ks, count, sum_k, false, fp32, cap, pair_mode());
   if (shp.splits > 1 && !csplit) {
     int64_t need = 0;
@@ -2363,7 +2397,7 @@ extern "C" hap_status hap_matmul_tune_import(const char* text) {
                                                            &splits, &kbps, &cl);
     HAP_CHECK_ARG(got == 4 || got == 5, "hap_matmul_tune_import: malformed line: " + line);
     HAP_CHECK_ARG((bn == 128 || bn == 256 || (bn == 192 && pair)) && splits >= 1 && kbps >= 1 &&
-                      (!cl || (!pair && tc::cluster_split_ok(splits))),
+                      (!cl || tc::cluster_split_ok(splits, pair != 0)),
                   "hap_matmul_tune_import: bad shape: " + line);
     tc::Shape shape{bn, splits, kbps, pair != 0};
     shape.cl = cl != 0;

@@ -92,7 +92,7 @@ def main():
                 if sp > 1 and (tiles * sp > slots or kb // sp < 2):
                     continue
                 kbps = -(-kb // sp)
-                for cl in ((0, 1) if (not pair and sp in (2, 4, 8)) else (0,)):
+                for cl in ((0, 1) if (sp in (2, 4) or (sp == 8 and not pair)) else (0,)):
                     L.hap_matmul_tune_import(f"{key}\t{pair} {bn} {sp} {kbps} {cl}\n".encode())
                     us = graph_us(lambda: L.hap_matmul_batch(d, 1, 0, BF16, odt, 0, s.cuda_stream), s)
                     res.append((us, f"{'pair' if pair else 'cta'}{bn}/s{sp}{'c' if cl else ''}"))
