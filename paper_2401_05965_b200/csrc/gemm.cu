@@ -707,68 +707,102 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t cluster_addr) {
 
 // `rank` = this CTA's index among the S that hold the same rows, whose
 // cluster ranks are q * stride + offset (single-CTA tiles: stride 1; SM-pair
-// tiles: stride 2, offset = rank within the pair).
+// tiles: stride 2, offset = rank within the pair).  16 DSMEM loads (16 / S
+// chunks x S partials) plus their C / R loads are in flight per iteration.
+template <int BN, typename OutT, int S>
+__device__ __forceinline__ void csplit_finish_t(const TcBatch& bt, const TcProblem& pr, int prob, int m0, int n0,
+                                                uint8_t* part, int rank, int tid, int stride, int offset) {
+  constexpr int kChunks = BN / 4;   // float4 chunks per row
+  constexpr int CPI = 16 / S;       // chunks per iteration per thread
+  constexpr int kThreadsE = kEpiWarps * 32;
+  const int rows = 128 / S;
+  const int r0 = rank * rows;
+  const int total = rows * kChunks;
+  const uint32_t base = smem_u32(part);
+  uint32_t peer[S];
+#pragma unroll
+  for (int q = 0; q < S; ++q) peer[q] = map_to_cta(base, static_cast<uint32_t>(q * stride + offset));
+  const int epi = bt.fin_epi[prob];
+  const bool acc_c = pr.accumulate != 0;
+  for (int k0 = tid; k0 < total; k0 += CPI * kThreadsE) {
+    float4 v[CPI][S];
+#pragma unroll
+    for (int c = 0; c < CPI; ++c) {
+      const int k = k0 + c * kThreadsE;
+      if (k < total) {
+        const uint32_t off = csplit_offset(r0 + k / kChunks, k % kChunks, BN);
+#pragma unroll
+        for (int q = 0; q < S; ++q) v[c][q] = ld_dsmem_f4(peer[q] + off);
+      }
+    }
+    float old[CPI][4], res[CPI][4];
+#pragma unroll
+    for (int c = 0; c < CPI; ++c) {
+      const int k = k0 + c * kThreadsE;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) old[c][j] = res[c][j] = 0.f;
+      if (k >= total) continue;
+      const int grow = m0 + r0 + k / kChunks, col = n0 + (k % kChunks) * 4;
+      if (grow >= pr.M || col >= pr.N) continue;
+      const int valid = pr.N - col < 4 ? pr.N - col : 4;
+      const OutT* dst = static_cast<const OutT*>(pr.C) + static_cast<int64_t>(grow) * pr.ldc + col;
+      if (acc_c) {
+        if constexpr (std::is_same<OutT, float>::value) {
+          if (valid == 4 && pr.vec_ok) {
+            const float4 o = *reinterpret_cast<const float4*>(dst);
+            old[c][0] = o.x; old[c][1] = o.y; old[c][2] = o.z; old[c][3] = o.w;
+          } else {
+            for (int j = 0; j < valid; ++j) old[c][j] = dst[j];
+          }
+        } else {
+          for (int j = 0; j < valid; ++j) old[c][j] = __bfloat162float(dst[j]);
+        }
+      }
+      if (epi != EPI_OP_NONE) {
+        const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(bt.fin_R[prob]) +
+                                 static_cast<int64_t>(grow) * bt.fin_ldr[prob] + col;
+        for (int j = 0; j < valid; ++j) res[c][j] = __bfloat162float(R[j]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPI; ++c) {
+      const int k = k0 + c * kThreadsE;
+      if (k >= total) continue;
+      const int grow = m0 + r0 + k / kChunks, col = n0 + (k % kChunks) * 4;
+      if (grow >= pr.M || col >= pr.N) continue;
+      float4 a = v[c][0];
+#pragma unroll
+      for (int q = 1; q < S; ++q) {   // rank order: the same sum whatever the timing
+        a.x += v[c][q].x; a.y += v[c][q].y; a.z += v[c][q].z; a.w += v[c][q].w;
+      }
+      float f[4] = {a.x + old[c][0], a.y + old[c][1], a.z + old[c][2], a.w + old[c][3]};
+      const int valid = pr.N - col < 4 ? pr.N - col : 4;
+      OutT* dst = static_cast<OutT*>(pr.C) + static_cast<int64_t>(grow) * pr.ldc + col;
+      if constexpr (std::is_same<OutT, float>::value) {
+        if (valid == 4 && pr.vec_ok) *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+        else for (int j = 0; j < valid; ++j) dst[j] = f[j];
+      } else {
+        if (epi == EPI_OP_ADD)
+          for (int j = 0; j < 4; ++j) f[j] += res[c][j];
+        for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(f[j]);
+        if (epi == EPI_OP_ADD2) {
+          __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(bt.fin_Y[prob]) +
+                             static_cast<int64_t>(grow) * bt.fin_ldy[prob] + col;
+          for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(f[j]) + res[c][j]);
+        }
+      }
+    }
+  }
+}
+
 template <int BN, typename OutT>
 __device__ __forceinline__ void csplit_finish(const TcBatch& bt, const TcProblem& pr, int prob, int m0, int n0,
                                               uint8_t* part, int rank, int S, int tid, int stride = 1,
                                               int offset = 0) {
-  constexpr int kChunks = BN / 4;   // float4 chunks per row
-  const int rows = 128 / S;
-  const int r0 = rank * rows;
-  const uint32_t base = smem_u32(part);
-  uint32_t peer[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q)
-    if (q < S) peer[q] = map_to_cta(base, static_cast<uint32_t>(q * stride + offset));
-  const int epi = bt.fin_epi[prob];
-  for (int k = tid; k < rows * kChunks; k += kEpiWarps * 32) {
-    const int row = r0 + k / kChunks, chunk = k % kChunks;
-    const uint32_t off = csplit_offset(row, chunk, BN);
-    float4 v[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-      if (q < S) v[q] = ld_dsmem_f4(peer[q] + off);
-    float4 a = v[0];
-#pragma unroll
-    for (int q = 1; q < 16; ++q)
-      if (q < S) {
-        a.x += v[q].x; a.y += v[q].y; a.z += v[q].z; a.w += v[q].w;
-      }
-    const int grow = m0 + row, col = n0 + chunk * 4;
-    if (grow >= pr.M || col >= pr.N) continue;
-    float f[4] = {a.x, a.y, a.z, a.w};
-    const int valid = pr.N - col < 4 ? pr.N - col : 4;
-    OutT* dst = static_cast<OutT*>(pr.C) + static_cast<int64_t>(grow) * pr.ldc + col;
-    const bool vec = valid == 4 && pr.vec_ok;
-    if constexpr (std::is_same<OutT, float>::value) {
-      if (pr.accumulate) {
-        if (vec) {
-          const float4 o = *reinterpret_cast<const float4*>(dst);
-          f[0] += o.x; f[1] += o.y; f[2] += o.z; f[3] += o.w;
-        } else {
-          for (int j = 0; j < valid; ++j) f[j] += dst[j];
-        }
-      }
-      if (vec) *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
-      else for (int j = 0; j < valid; ++j) dst[j] = f[j];
-    } else {
-      if (pr.accumulate)
-        for (int j = 0; j < valid; ++j) f[j] += __bfloat162float(dst[j]);
-      float x[4] = {0.f, 0.f, 0.f, 0.f};
-      if (epi != EPI_OP_NONE) {
-        const __nv_bfloat16* R = static_cast<const __nv_bfloat16*>(bt.fin_R[prob]) +
-                                 static_cast<int64_t>(grow) * bt.fin_ldr[prob] + col;
-        for (int j = 0; j < valid; ++j) x[j] = __bfloat162float(R[j]);
-      }
-      if (epi == EPI_OP_ADD)
-        for (int j = 0; j < 4; ++j) f[j] += x[j];
-      for (int j = 0; j < valid; ++j) dst[j] = __float2bfloat16_rn(f[j]);
-      if (epi == EPI_OP_ADD2) {
-        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(bt.fin_Y[prob]) + static_cast<int64_t>(grow) * bt.fin_ldy[prob]
-                           + col;
-        for (int j = 0; j < valid; ++j) Y[j] = __float2bfloat16_rn(bf16_round(f[j]) + x[j]);
-      }
-    }
+  switch (S) {
+    case 2: csplit_finish_t<BN, OutT, 2>(bt, pr, prob, m0, n0, part, rank, tid, stride, offset); break;
+    case 4: csplit_finish_t<BN, OutT, 4>(bt, pr, prob, m0, n0, part, rank, tid, stride, offset); break;
+    default: csplit_finish_t<BN, OutT, 8>(bt, pr, prob, m0, n0, part, rank, tid, stride, offset); break;
   }
 }
 
@@ -1983,12 +2017,14 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     int epi = pr.epi;
     const void* R = out.R;
     int64_t ldr = out.ldr;
-    if (epi == HAP_EPI_NONE && !fp32 && out.accumulate && pr.splits <= 1 && pr.vec_ok && tma_epilogue()) {
+    // K split (workspace slices or cluster): the reduction adds C itself when accumulating
+    const bool splitting = csplit || pr.splits > 1;
+    if (epi == HAP_EPI_NONE && !fp32 && out.accumulate && !splitting && pr.vec_ok && tma_epilogue()) {
       epi = HAP_EPI_ADD;
       R = out.C;
       ldr = out.ldc;
     }
-    if (epi == HAP_EPI_ADD && out.accumulate && pr.splits > 1) epi = HAP_EPI_NONE;   // += C: the accumulate
+    if (epi == HAP_EPI_ADD && out.accumulate && splitting) epi = HAP_EPI_NONE;   // += C: the accumulate
     pr.epi = epi;
     if (csplit && (!sum_k || q == 0)) {
       // cluster split K: the DSMEM finish applies accumulate and the residual

@@ -89,8 +89,19 @@ def main():
     args = ap.parse_args()
     if args.verbose:
         import faulthandler
+        import subprocess
+        import threading
 
         faulthandler.dump_traceback_later(60, repeat=True)
+
+        def smi():   # is the GPU busy (a kernel spinning) or idle (a host-side wait)?
+            while True:
+                threading.Event().wait(45)
+                out = subprocess.run(["nvidia-smi", "--query-gpu=utilization.gpu,memory.used,clocks.sm",
+                                      "--format=csv,noheader"], capture_output=True, text=True).stdout
+                print(f"[watchdog] nvidia-smi: {out.strip()}", flush=True)
+
+        threading.Thread(target=smi, daemon=True).start()
     torch.cuda.set_device(0)
     failures, count, bit_equal, bit_total = [], 0, 0, 0
     for world in [int(w) for w in args.world.split(",")]:
