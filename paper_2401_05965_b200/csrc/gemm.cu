@@ -238,6 +238,8 @@ __device__ __forceinline__ void bulk_wait_read1() {
 // Before a CTA exits: its staged boxes have been read by the TMA engine (the
 // global writes complete with the grid).
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// Every bulk store / reduce this thread committed has been performed in global memory.
+__device__ __forceinline__ void bulk_wait_complete() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t x, int32_t y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -672,6 +674,47 @@ __device__ __forceinline__ uint32_t csplit_offset(int row, int chunk, int bn) {
   return static_cast<uint32_t>(row * bn * 4 + ((chunk ^ (row & 7)) << 4));
 }
 
+// fp32 outputs (weight gradients): the splits of a tile add into C one after
+// another in rank order — split s waits on its warp's turn barrier until
+// split s-1 has finished, then drains its accumulator into C by TMA
+// reduce-add (split 0 without accumulate: TMA store), waits until those
+// writes are performed, and passes the turn to split s+1 (a release arrive
+// on the next CTA's barrier, through the cluster).  C = ((C + p0) + p1) + ...
+// on every run, at the price of the serialised adds (one tile slab each).
+__device__ __forceinline__ void chain_wait(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "CHAINW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], 0;\n\t"
+      "@!done bra CHAINW_%=;\n}" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void chain_pass(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+
+template <int BN>
+__device__ __forceinline__ void csplit_chain(const TcProblem& pr, const Unit& x, uint32_t tmem_acc, int quarter,
+                                             int half, int lane, int row0, uint8_t* buf, uint32_t& box_seq,
+                                             uint32_t turn, int next_rank) {
+  if (x.split > 0) {
+    if (lane == 0) chain_wait(turn);
+    __syncwarp();
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // the acquire orders this warp's TMA reduce
+  }
+  const bool tma = pr.epi_mode == EPI_TMA_ADD;
+  const int mode = tma ? ((x.split == 0 && !pr.accumulate) ? EPI_TMA_STORE : EPI_TMA_ADD) : EPI_DIRECT;
+  drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, row0, x.n0, pr.M, pr.N, static_cast<float*>(pr.C),
+                               pr.ldc, mode, pr.vec_ok, (x.split > 0 || pr.accumulate) ? 1 : 0, &pr.c, buf,
+                               box_seq);
+  if (lane == 0) bulk_wait_complete();
+  __syncwarp();
+  if (next_rank >= 0 && lane == 0) {
+    __threadfence();
+    chain_pass(map_to_cta(turn, static_cast<uint32_t>(next_rank)));
+  }
+}
+
 template <int BN>
 __device__ __forceinline__ void csplit_drain(uint32_t tmem_acc, int quarter, int half, int lane, uint8_t* part,
                                              bool empty) {
@@ -933,6 +976,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_init(tempty0 + 8 * a, kEpiWarps * 32);
     }
     for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 22 + w), 1);   // split-K turns
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -1040,11 +1084,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       if (bt.csplit > 1) {
-        // cluster split K: the partial goes to this CTA's shared memory (the
-        // pipeline stages are idle: this was the CTA's only unit); the
-        // cluster reduces it after the loop
-        fence_async_smem();
-        csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+        if constexpr (std::is_same<OutT, float>::value) {   // splits add into C in rank order
+          const int rnk = static_cast<int>(cluster_rank());
+          csplit_chain<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, buf, box_seq,
+                           smem_u32(bars + 2 * G::kStages + 22 + (warp - 4)), rnk + 1 < bt.csplit ? rnk + 1 : -1);
+        } else {
+          // the partial goes to this CTA's shared memory (the pipeline stages
+          // are idle: this was the CTA's only unit); the cluster reduces it
+          // after the loop
+          fence_async_smem();
+          csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+        }
       } else {
         epilogue_unit<BN, OutT>(pr, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, x.n0, x.split,
                                 buf, box_seq, ld_bar, ld_phase, nullptr);
@@ -1057,7 +1107,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
   }
-  if (bt.csplit > 1) {   // every thread of every CTA of the cluster takes part in both barriers
+  if (bt.csplit > 1 && !std::is_same<OutT, float>::value) {   // every thread of the cluster: both barriers
     cluster_sync_all();   // all partials are in shared memory
     if (warp >= 4 && static_cast<int>(blockIdx.x) < num_units) {
       const Unit x = decode_unit<BM, BN>(bt, blockIdx.x);
@@ -1182,6 +1232,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       mbar_init(tempty0 + 8 * a, 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
     }
     for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 22 + w), 1);   // split-K turns
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -1294,9 +1345,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
       mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      if (bt.csplit > 1) {   // cluster split K: partial to this CTA's idle pipeline smem, reduced after the loop
-        fence_async_smem();
-        csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+      if (bt.csplit > 1) {   // cluster split K
+        if constexpr (std::is_same<OutT, float>::value) {   // the pairs add into C in rank order
+          const int nxt = static_cast<int>(crank) + 2;
+          csplit_chain<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, buf, box_seq,
+                           smem_u32(bars + 2 * G::kStages + 22 + (warp - 4)), nxt < 2 * bt.csplit ? nxt : -1);
+        } else {   // partial to this CTA's idle pipeline smem, reduced after the loop
+          fence_async_smem();
+          csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(leader_tempty + 8 * acc);
@@ -1335,7 +1392,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
     hap::pdl_trigger();   // last tile drained: let the next kernel start launching
     if (lane == 0) bulk_wait_all();
   }
-  if (bt.csplit > 1) {   // every thread of every CTA of the cluster takes part in both barriers
+  if (bt.csplit > 1 && !std::is_same<OutT, float>::value) {   // every thread of the cluster: both barriers
     cluster_sync_all();   // all partials are in shared memory
     if (warp >= 4 && pair < bt.total_units) {
       const Unit x = decode_unit<256, BN>(bt, pair);
@@ -1493,7 +1550,6 @@ inline bool cluster_split_ok(int64_t splits, bool pair) {
 
 Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int count, int sum_k, bool allow_split,
                    bool fp32_out, int cap, int allow_pair) {
-  (void)fp32_out;
   // K blocks a unit walks: the concatenated K of a sum, else the largest
   // problem's (grouped problems with less K simply walk fewer blocks)
   int64_t k_blocks = 0;
@@ -1555,7 +1611,9 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
         if (!cluster_split_ok(S, c.pair) || tiles * S > slots || k_blocks / S < 2) break;
         const int64_t kps = (k_blocks + S - 1) / S;
         if ((S - 1) * kps >= k_blocks) continue;   // every split walks at least one K block
-        const double est = static_cast<double>(kps) * t_kb;
+        // fp32: the splits' adds into C run one after another (~0.7 us each);
+        // bf16: the DSMEM reduction measured ~4 us beyond the K walk
+        const double est = static_cast<double>(kps) * t_kb + (fp32_out ? 0.7 * static_cast<double>(S) : 4.0);
         if (cl.score < 0 || est < cl.est_us) {
           cl = {{c.bn, static_cast<int>(S), static_cast<int>(kps), c.pair}, 1.0, est};
           cl.s.cl = true;
@@ -1566,14 +1624,14 @@ Shape choose_shape(const int64_t* Ms, const int64_t* Ns, const int64_t* Ks, int 
   // Split K through the workspace stores fp32 partial slices and sums them in
   // order in a second launch (split_reduce_kernel): a serial tail (~5 us
   // measured on B200), so split only when the shortened K walk saves more.
-  constexpr double kSplitTailUs = 5.0, kClusterTailUs = 1.0;
+  constexpr double kSplitTailUs = 5.0;
   double best_us = plain.score > 0 ? plain.est_us : 1e30;
   Shape best = plain.score > 0 ? plain.s : split.s;
   if (split.score > 0 && split.est_us + kSplitTailUs < best_us) {
     best_us = split.est_us + kSplitTailUs;
     best = split.s;
   }
-  if (cl.score > 0 && cl.est_us + kClusterTailUs < best_us) best = cl.s;
+  if (cl.score > 0 && cl.est_us < best_us) best = cl.s;
   return best;
 }
 
@@ -2040,6 +2098,9 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
       bt.fin_ldy[q] = out.ldy;
       pr.epi = HAP_EPI_NONE;
       pr.epi_mode = tc::EPI_DIRECT;
+      // fp32: the split chain adds by TMA reduce-add when C is 16-byte pitched
+      if (fp32 && pr.vec_ok && tma_epilogue() && tc::make_map_c(&pr.c, out.C, out_dtype, out.N, out.M, out.ldc, shp.bn))
+        pr.epi_mode = tc::EPI_TMA_ADD;
     } else if (pr.splits > 1 && (!sum_k || q == 0)) {
       // split K: the ordered reduction applies the residual epilogue (split_fusable)
       HAP_CHECK_ARG(epi == HAP_EPI_NONE || epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2,
