@@ -2045,7 +2045,13 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
     const hap_gemm_desc& g = d[q];
     bool ok = g.transA ? tc::make_map(&pr.a, g.A, g.M, g.K, g.lda, tc::BK) : tc::make_map(&pr.a, g.A, g.K, g.M, g.lda, tc::BM);
     ok = ok && (g.transB ? tc::make_map(&pr.b, g.B, g.K, g.N, g.ldb, b_box) : tc::make_map(&pr.b, g.B, g.N, g.K, g.ldb, tc::BK));
-    HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout");
+    HAP_CHECK_ARG(ok, "hap_matmul: cuTensorMapEncodeTiled rejected the operand layout (problem " + std::to_string(q) +
+                          " of " + std::to_string(count) + ": M " + std::to_string(g.M) + " N " + std::to_string(g.N) +
+                          " K " + std::to_string(g.K) + " lda " + std::to_string(g.lda) + " ldb " +
+                          std::to_string(g.ldb) + " trans " + std::to_string(g.transA) + std::to_string(g.transB) +
+                          " A%16 " + std::to_string(reinterpret_cast<uintptr_t>(g.A) & 15) + " B%16 " +
+                          std::to_string(reinterpret_cast<uintptr_t>(g.B) & 15) + " box " + std::to_string(b_box) +
+                          (shp.pair ? " pair" : " cta") + ")");
     const hap_gemm_desc& out = sum_k ? d[0] : g;
     pr.C = out.C;
     pr.ldc = out.ldc;

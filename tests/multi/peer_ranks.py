@@ -120,9 +120,13 @@ def main():
                         print(f"run {count}: {label}{' (graph)' if capture else ''}", flush=True)
                     try:
                         exs, losses = run_peer(doc, shapes, inputs, dtype, sync, capture)
-                    except Exception as exc:  # noqa: BLE001 - reported as a failure
-                        failures.append(f"{label}: {type(exc).__name__}: {exc}")
-                        continue
+                    except Exception as exc:  # noqa: BLE001 - fatal: a peer kernel may be left spinning
+                        # one rank failed to enqueue its step: the other rank's peer kernel now waits for a
+                        # partner that never comes, so no later GPU call can return — report and stop
+                        print(f"  FAIL {label}: {type(exc).__name__}: {exc}", flush=True)
+                        for f in failures[:40]:
+                            print("  FAIL", f, flush=True)
+                        os._exit(2)
                     grads = grads_of(exs, program)
                     failures += check(label + (" graph" if capture else ""), doc, gname, inputs, dtype, losses, grads)
                     if dtype == "fp32":
