@@ -33,6 +33,14 @@ int carveout_pref() {
   return pref;
 }
 
+void ensure_context() {
+  static thread_local bool done = false;
+  if (done) return;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) done = true;
+  cudaGetLastError();
+}
+
 int sm_count() {
   static int cached[64] = {0};
   int dev = 0;

@@ -45,6 +45,12 @@ inline hap_status launch_status(const char* what) {
 // SM count of the current device (cached per device).
 int sm_count();
 
+// Make the current device's primary context current in the calling thread
+// (once per thread) before a driver-API call such as cuTensorMapEncodeTiled:
+// a thread whose first CUDA call is into this library (ranks stepped from
+// worker threads) would otherwise have no context and the call would fail.
+void ensure_context();
+
 // Per-stream device scratch for kernels that need a workspace (ordered
 // reduction partials, split-K partial tiles, arrival counters).  Launches on
 // one stream are ordered, so they share a slot.  A slot grows only outside

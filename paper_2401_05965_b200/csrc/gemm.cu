@@ -1429,6 +1429,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // pitch `ld` elements, box {64, box_outer}, 128B swizzle, zero OOB fill.
 bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld,
               int box_outer) {
+  ensure_context();
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -1444,6 +1445,7 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, i
 // Output tensor map for the TMA epilogue: boxes of 128 bytes x 32 rows.
 bool make_map_c(CUtensorMap* map, void* ptr, hap_dtype dt, int64_t inner, int64_t outer, int64_t ld, int bn,
                 int box_w = 0) {
+  ensure_context();
   auto fn = encode_fn();
   if (!fn) return false;
   const int es = dt == HAP_BF16 ? 2 : 4;

@@ -638,6 +638,7 @@ extern "C" hap_status hap_symm_destroy(void* ctx) {
 namespace {
 // Base of the allocation holding `ptr` (driver cuMemGetAddressRange).
 bool alloc_base(const void* ptr, char** base) {
+  ensure_context();
   using Fn = int (*)(uint64_t*, size_t*, uint64_t);
   static Fn fn = nullptr;
   static std::once_flag once;
