@@ -16,6 +16,7 @@ timeout:
 import argparse
 import os
 import sys
+import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
@@ -85,6 +86,9 @@ def main():
     ap.add_argument("--variants", default="all_reduce,sfb")
     ap.add_argument("--dtypes", default="fp32,bf16")
     ap.add_argument("--capture-every", type=int, default=5, help="every k-th run replays a captured graph (0: never)")
+    ap.add_argument("--stride", type=int, default=1, help="every k-th case only")
+    ap.add_argument("--rotate", action="store_true",
+                    help="one (dtype, gradient sync) combination per case, rotating through them")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.verbose:
@@ -104,44 +108,47 @@ def main():
         threading.Thread(target=smi, daemon=True).start()
     torch.cuda.set_device(0)
     failures, count, bit_equal, bit_total = [], 0, 0, 0
+    combos = [(d, v) for d in args.dtypes.split(",") for v in args.variants.split(",")]
+    t0 = time.time()
     for world in [int(w) for w in args.world.split(",")]:
-        for name, doc, gname, inputs in cases(world):
+        for ci, (name, doc, gname, inputs) in enumerate(cases(world)):
             if args.only and args.only not in name:
+                continue
+            if ci % args.stride:
                 continue
             g = goldens.graph(gname)
             shapes = {n.id: n.shape for n in g.sources()}
             program, _, _ = O.load_plan(doc)
-            for dtype in args.dtypes.split(","):
-                for sync in args.variants.split(","):
-                    count += 1
-                    label = f"{name} {dtype} {sync}"
-                    capture = args.capture_every > 0 and count % args.capture_every == 0
-                    if args.verbose:
-                        print(f"run {count}: {label}{' (graph)' if capture else ''}", flush=True)
-                    try:
-                        exs, losses = run_peer(doc, shapes, inputs, dtype, sync, capture)
-                    except Exception as exc:  # noqa: BLE001 - fatal: a peer kernel may be left spinning
-                        # one rank failed to enqueue its step: the other rank's peer kernel now waits for a
-                        # partner that never comes, so no later GPU call can return — report and stop
-                        print(f"  FAIL {label}: {type(exc).__name__}: {exc}", flush=True)
-                        for f in failures[:40]:
-                            print("  FAIL", f, flush=True)
-                        os._exit(2)
-                    grads = grads_of(exs, program)
-                    failures += check(label + (" graph" if capture else ""), doc, gname, inputs, dtype, losses, grads)
-                    if dtype == "fp32":
-                        lex, llosses = run_local(doc, shapes, inputs, dtype, sync)
-                        lgrads = grads_of([lex], program)
-                        same = list(losses) == list(llosses) and all(
-                            all(np.array_equal(a[1], b[1]) for a, b in zip(grads[ref][r], lgrads[ref][r]))
-                            for ref in grads for r in grads[ref])
-                        bit_total += 1
-                        bit_equal += int(same)
-                        lex.close()
-                    for ex in exs:
-                        ex.close()
+            for dtype, sync in ([combos[(ci // args.stride) % len(combos)]] if args.rotate else combos):
+                count += 1
+                label = f"{name} {dtype} {sync}"
+                capture = args.capture_every > 0 and count % args.capture_every == 0
+                if args.verbose:
+                    print(f"run {count} [{time.time() - t0:.1f}s]: {label}{' (graph)' if capture else ''}", flush=True)
+                try:
+                    exs, losses = run_peer(doc, shapes, inputs, dtype, sync, capture)
+                except Exception as exc:  # noqa: BLE001 - fatal: a peer kernel may be left spinning
+                    # one rank failed to enqueue its step: the other rank's peer kernel now waits for a
+                    # partner that never comes, so no later GPU call can return — report and stop
+                    print(f"  FAIL {label}: {type(exc).__name__}: {exc}", flush=True)
+                    for f in failures[:40]:
+                        print("  FAIL", f, flush=True)
+                    os._exit(2)
+                grads = grads_of(exs, program)
+                failures += check(label + (" graph" if capture else ""), doc, gname, inputs, dtype, losses, grads)
+                if dtype == "fp32":
+                    lex, llosses = run_local(doc, shapes, inputs, dtype, sync)
+                    lgrads = grads_of([lex], program)
+                    same = list(losses) == list(llosses) and all(
+                        all(np.array_equal(a[1], b[1]) for a, b in zip(grads[ref][r], lgrads[ref][r]))
+                        for ref in grads for r in grads[ref])
+                    bit_total += 1
+                    bit_equal += int(same)
+                    lex.close()
+                for ex in exs:
+                    ex.close()
     print(f"peer ranks parity: {count} runs, {len(failures)} failures; fp32 bit-identical to LocalGroup "
-          f"in {bit_equal}/{bit_total}")
+          f"in {bit_equal}/{bit_total}; {time.time() - t0:.0f} s")
     for f in failures[:40]:
         print("  FAIL", f)
     sys.exit(1 if failures else 0)
