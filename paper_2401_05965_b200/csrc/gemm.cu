@@ -1191,6 +1191,36 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar, uint32_t leader) {
 }
 
 
+// HAP_GEMM_TRACE builds (tools/gemm_trace.py): per-CTA %globaltimer stamps
+// of the pipeline's milestones, to see where a launch's fixed cost goes.
+#ifdef HAP_GEMM_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_ctas = 0;
+__device__ __forceinline__ void trace(int ev) {
+  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x * 16 + ev] = t;
+  }
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_put(int ev, unsigned long long v) {
+  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) g_trace[blockIdx.x * 16 + ev] = v;
+}
+// time spent in one wait, accumulated into `acc` (ns)
+#define HAP_TIMED(acc, stmt) do { const unsigned long long t_ = gtimer(); stmt; (acc) += gtimer() - t_; } while (0)
+#define HAP_TRACE(ev) trace(ev)
+#define HAP_TRACE_ONCE(ev, flag) do { if (!(flag)) { trace(ev); (flag) = true; } } while (0)
+#else
+#define HAP_TIMED(acc, stmt) stmt
+#define HAP_TRACE_ONCE(ev, flag) ((void)0)
+#define HAP_TRACE(ev) ((void)0)
+#endif
+
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {
   using G = Cfg2<BN, kBMN>;
@@ -1215,6 +1245,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
   const uint32_t leader = crank & ~1u;
   const int pair = blockIdx.x >> 1;
   const int num_pairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) HAP_TRACE(0);
 
   if (warp == 0 && lane == 0) {
     for (int q = 0; q < bt.count; ++q) {
@@ -1245,19 +1276,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   hap::pdl_wait();   // everything above touched no global memory
+  if (threadIdx.x == 0) HAP_TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
+      unsigned long long w_empty = 0;
+#ifdef HAP_GEMM_TRACE
+      bool traced = false;
+#endif
       PairCursor<BN> cur(bt, pair, num_pairs);
       Unit x;
       while (cur.next(bt, x)) {
         const int m0 = x.m0 + 128 * static_cast<int>(rank);
         const int n0 = x.n0 + HB * static_cast<int>(rank);
         for_each_kblock(bt, x, [&](int q, int kb) {
-          mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
+          HAP_TIMED(w_empty, mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1));
           const uint32_t leader_full = map_to_cta(full0 + 8 * stage, leader);
           if (rank == 0) mbar_expect_tx_cluster(leader_full, 2 * G::kStageBytes);
           else mbar_arrive_cluster(leader_full);
@@ -1279,12 +1315,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
           } else {
             tma_load_2d_pair(sb, mb, leader_full, k0, n0);
           }
+#ifdef HAP_GEMM_TRACE
+          HAP_TRACE_ONCE(2, traced);
+          HAP_TRACE(9);
+#endif
           if (++stage == G::kStages) {
             stage = 0;
             phase ^= 1;
           }
         });
       }
+#ifdef HAP_GEMM_TRACE
+      trace_put(14, w_empty);
+#endif
+      (void)w_empty;
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -1296,16 +1340,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      unsigned long long w_full = 0, w_tempty = 0;
+#ifdef HAP_GEMM_TRACE
+      bool traced = false;
+#endif
       PairCursor<BN> cur(bt, pair, num_pairs);
       Unit x;
       while (cur.next(bt, x)) {
-        mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1);
+        HAP_TIMED(w_tempty, mbar_wait_cluster(tempty0 + 8 * acc, acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         bool first = true;
         for_each_kblock(bt, x, [&](int, int) {
-          mbar_wait_cluster(full0 + 8 * stage, phase);
+          HAP_TIMED(w_full, mbar_wait_cluster(full0 + 8 * stage, phase));
           tc_fence_after();
+#ifdef HAP_GEMM_TRACE
+          if (first) { HAP_TRACE_ONCE(3, traced); HAP_TRACE(10); }
+#endif
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
 #pragma unroll
@@ -1323,9 +1374,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
           }
         });
         tc_commit_pair(tfull0 + 8 * acc, leader);
+        HAP_TRACE(4);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef HAP_GEMM_TRACE
+      trace_put(12, w_full);
+      trace_put(13, w_tempty);
+#endif
+      (void)w_full;
+      (void)w_tempty;
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): own 128 rows of the 256-row tile
@@ -1338,13 +1396,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
     const uint32_t leader_tempty = map_to_cta(tempty0, leader);
     int acc = 0;
     uint32_t acc_phase = 0;
+#ifdef HAP_GEMM_TRACE
+    bool traced = false;
+#endif
     PairCursor<BN> cur(bt, pair, num_pairs);
     Unit x;
+    unsigned long long w_tfull = 0;
     while (cur.next(bt, x)) {
       const TcProblem& pr = bt.p[x.prob];
       const int m0 = x.m0 + 128 * static_cast<int>(rank);
-      mbar_wait_cluster(tfull0 + 8 * acc, acc_phase);
+      HAP_TIMED(w_tfull, mbar_wait_cluster(tfull0 + 8 * acc, acc_phase));
       tc_fence_after();
+#ifdef HAP_GEMM_TRACE
+      if (warp == 4 && lane == 0) { HAP_TRACE_ONCE(5, traced); HAP_TRACE(11); }
+#endif
       if (bt.csplit > 1) {   // cluster split K
         if constexpr (std::is_same<OutT, float>::value) {   // the pairs add into C in rank order
           const int nxt = static_cast<int>(crank) + 2;
@@ -1389,8 +1454,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+#ifdef HAP_GEMM_TRACE
+    if (warp == 4 && lane == 0) trace_put(15, w_tfull);
+#endif
+    (void)w_tfull;
     hap::pdl_trigger();   // last tile drained: let the next kernel start launching
+    if (warp == 4 && lane == 0) HAP_TRACE(6);
     if (lane == 0) bulk_wait_all();
+    if (warp == 4 && lane == 0) HAP_TRACE(7);
   }
   if (bt.csplit > 1 && !std::is_same<OutT, float>::value) {   // every thread of the cluster: both barriers
     cluster_sync_all();   // all partials are in shared memory
@@ -1408,6 +1479,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(G::kTmemCols));
   }
+  if (threadIdx.x == 0) HAP_TRACE(8);
 }
 
 // ------------------------------------------------------------------ host side
@@ -2517,3 +2589,11 @@ extern "C" void hap_matmul_tune_clear(void) {
   std::lock_guard<std::mutex> lock(tune_mutex());
   tune_cache().clear();
 }
+
+#ifdef HAP_GEMM_TRACE
+extern "C" int hap_gemm_trace_set(void* buf, int ctas) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  if (cudaMemcpyToSymbol(hap::tc::g_trace, &p, sizeof(p)) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(hap::tc::g_trace_ctas, &ctas, sizeof(ctas)) != cudaSuccess;
+}
+#endif

@@ -57,6 +57,7 @@ def run_peer(doc, shapes, inputs, dtype, sync, capture):
                                           config=ExecConfig(dtype=dtype, sm_caps=caps, input_grads=True,
                                                             grad_sync=sync))
                      for r in range(m)])
+    LIVE[:] = exs
     run_ranks([lambda ex=ex: ex.load(inputs) for ex in exs])
     if capture:
         run_ranks([lambda ex=ex: ex.step() for ex in exs])   # warm up together, capture one by one
@@ -79,6 +80,59 @@ def run_local(doc, shapes, inputs, dtype, sync):
     return ex, ex.losses()
 
 
+LIVE: list = []   # executors of the current run (the watchdog's view)
+
+
+def _install_watchdog(args):
+    """--verbose: every eager op is followed by a CUDA event; when no rank
+    makes progress for 30 s, print each rank's first incomplete op, the GPU
+    utilisation (a spinning kernel or a host-side wait), and exit 3."""
+    import subprocess
+    import threading
+
+    from paper_2401_05965_b200 import _lib
+
+    args.capture_every = 0   # events cannot be recorded inside a graph capture
+
+    def run_traced(self, ops):
+        trace = self.__dict__.setdefault("op_trace", [])
+        for op in ops:
+            st = op.fn(*op.args)
+            if st:
+                _lib.check(st, op.what)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            trace.append((op.what, ev))
+
+    Executor._run = run_traced
+
+    def watch():
+        last, since = None, time.time()
+        while True:
+            threading.Event().wait(5)
+            state = []
+            for r, ex in enumerate(list(LIVE)):
+                trace = list(ex.__dict__.get("op_trace", []))
+                first = next((i for i, (_, ev) in enumerate(trace) if not ev.query()), None)
+                state.append((r, len(trace), first, trace[first][0] if first is not None else "-"))
+            if state != last:
+                last, since = state, time.time()
+                continue
+            if time.time() - since < 30 or not state or all(f is None for _, _, f, _ in state):
+                continue
+            util = subprocess.run(["nvidia-smi", "--query-gpu=utilization.gpu", "--format=csv,noheader"],
+                                  capture_output=True, text=True).stdout.strip()
+            for r, n, first, what in state:
+                print(f"[watchdog] rank {r}: {n} ops enqueued, first incomplete op #{first}: {what}", flush=True)
+                trace = LIVE[r].__dict__.get("op_trace", [])
+                lo = max(0, (first or 0) - 4)
+                print(f"[watchdog]   ops {lo}..: {[w for w, _ in trace[lo:(first or 0) + 3]]}", flush=True)
+            print(f"[watchdog] GPU utilisation {util}; exiting", flush=True)
+            os._exit(3)
+
+    threading.Thread(target=watch, daemon=True).start()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("only", nargs="?")
@@ -92,20 +146,7 @@ def main():
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.verbose:
-        import faulthandler
-        import subprocess
-        import threading
-
-        faulthandler.dump_traceback_later(60, repeat=True)
-
-        def smi():   # is the GPU busy (a kernel spinning) or idle (a host-side wait)?
-            while True:
-                threading.Event().wait(45)
-                out = subprocess.run(["nvidia-smi", "--query-gpu=utilization.gpu,memory.used,clocks.sm",
-                                      "--format=csv,noheader"], capture_output=True, text=True).stdout
-                print(f"[watchdog] nvidia-smi: {out.strip()}", flush=True)
-
-        threading.Thread(target=smi, daemon=True).start()
+        _install_watchdog(args)
     torch.cuda.set_device(0)
     failures, count, bit_equal, bit_total = [], 0, 0, 0
     combos = [(d, v) for d in args.dtypes.split(",") for v in args.variants.split(",")]

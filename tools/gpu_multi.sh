@@ -12,6 +12,8 @@ port=29500
 trun() { port=$((port + 1)); python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $port "$@"; }
 nvidia-smi topo -m > $OUT/topo.txt 2>&1
 timeout 900 trun tools/coll_fit.py --json $OUT/coll_fit.json > $OUT/coll_fit.log 2>&1; echo "coll_fit rc=$?" >> $OUT/status.txt
+# this box's fitted lines drive gather="auto" in the bench runs below (merged with the other world sizes locally)
+python tools/coll_fit.py --fit $OUT/coll_fit.json >> $OUT/coll_fit.log 2>&1; cp paper_2401_05965_b200/collectives_b200.json $OUT/ 2>/dev/null
 timeout 300 trun tools/nvlink_ncu.py --json $OUT/nvl_events.json > $OUT/nvl_events.log 2>&1; echo "nvl_events rc=$?" >> $OUT/status.txt
 port=$((port + 1))
 timeout 900 ncu --target-processes all -k regex:p2p_ --clock-control none --csv \
