@@ -28,6 +28,10 @@ import argparse
 import json
 import math
 import os
+
+# one hardware work queue per stream (see paper_2401_05965_b200/__init__.py);
+# must precede CUDA context creation
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -56,6 +56,43 @@ struct Cfg {
   static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + kBarrierBytes + 1024;
 };
 
+// HAP_GEMM_TRACE builds (tools/gemm_trace.py): per-CTA %globaltimer stamps
+// of the pipeline's milestones, to see where a launch's fixed cost goes.
+constexpr int kTraceSlots = 32;
+#ifdef HAP_GEMM_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_ctas = 0;
+__device__ __forceinline__ void trace(int ev) {
+  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x * kTraceSlots + ev] = t;
+  }
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_put(int ev, unsigned long long v) {
+  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) g_trace[blockIdx.x * kTraceSlots + ev] = v;
+}
+__device__ __forceinline__ void trace_add(int ev, unsigned long long v) {
+  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) g_trace[blockIdx.x * kTraceSlots + ev] += v;
+}
+// time spent in one wait, accumulated into `acc` (ns)
+#define HAP_TIMED(acc, stmt) do { const unsigned long long t_ = gtimer(); stmt; (acc) += gtimer() - t_; } while (0)
+#define HAP_TRACE(ev) trace(ev)
+#define HAP_TRACE_ONCE(ev, flag) do { if (!(flag)) { trace(ev); (flag) = true; } } while (0)
+// epilogue step timing of one warp (quarter 0, half 0, lane 0) into slot ev
+#define HAP_ETIMED(on, ev, stmt) do { const unsigned long long t_ = gtimer(); stmt; if (on) trace_add(ev, gtimer() - t_); } while (0)
+#else
+#define HAP_ETIMED(on, ev, stmt) stmt
+#define HAP_TIMED(acc, stmt) stmt
+#define HAP_TRACE_ONCE(ev, flag) ((void)0)
+#define HAP_TRACE(ev) ((void)0)
+#endif
+
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -307,18 +344,24 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
   constexpr int kRowBytes = W * static_cast<int>(sizeof(OutT));
   constexpr int kBoxes = (BN / 2) / W;
   const uint32_t buf0 = smem_u32(buf);
+  const bool tr = quarter == 0 && half == 0 && lane == 0;
+  (void)tr;
 #pragma unroll 1
   for (int b = 0; b < kBoxes; ++b) {
     // the two staging buffers alternate across boxes AND units (a unit with
     // an odd box count must not restart on the buffer its last box is still
     // being stored from)
     const uint32_t dst = buf0 + (box_seq++ & 1) * 4096;
-    if (lane == 0) bulk_wait_read1();   // the buffer's previous box has been read out
+    HAP_ETIMED(tr, 16, if (lane == 0) bulk_wait_read1());   // the buffer's previous box has been read out
     __syncwarp();
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(20, 1);
+    const unsigned long long t_st = gtimer();
+#endif
 #pragma unroll
     for (int k = 0; k < W / 32; ++k) {
       uint32_t r[32];
-      tmem_ld32(lane_base + half * (BN / 2) + b * W + k * 32, r);
+      HAP_ETIMED(tr, 17, tmem_ld32(lane_base + half * (BN / 2) + b * W + k * 32, r));
       if (prow) add_partial(r, prow + (b * W + k * 32) * 128);
       if constexpr (std::is_same<OutT, float>::value) {
         static_assert(W % 32 == 0 || W == 16, "fp32 box width");
@@ -346,11 +389,14 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
     }
     fence_async_smem();
     __syncwarp();
-    if (lane == 0) {
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(18, gtimer() - t_st);
+#endif
+    HAP_ETIMED(tr, 19, if (lane == 0) {
       if (mode == EPI_TMA_ADD) tma_reduce_add_2d(tmC, dst, first + b * W, row0);
       else tma_store_2d(tmC, dst, first + b * W, row0);
       bulk_commit();
-    }
+    });
   }
 }
 
@@ -547,9 +593,15 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
     if (n_in) issue_loads(0);
   }
   __syncwarp();
+  const bool tr = quarter == 0 && half == 0 && lane == 0;
+  (void)tr;
 #pragma unroll 1
   for (int ch = 0; ch < kChunks; ++ch) {
     const int set = dbl ? (ch & 1) : ch;
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(26, 1);
+    const unsigned long long t_w = gtimer();
+#endif
     if (lane == 0) {
       if (dbl) {
         // the other pair was last stored from by chunk ch-1: once read out,
@@ -562,14 +614,20 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
         bulk_wait_read1();   // ring: only the previous chunk's last box may still be read
       }
     }
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(22, gtimer() - t_w);
+#endif
     uint32_t r[32];
-    tmem_ld32(lane_base + ch * kFusedW, r);
+    HAP_ETIMED(tr, 23, tmem_ld32(lane_base + ch * kFusedW, r));
     if (prow) add_partial(r, prow + ch * kFusedW * 128);
     if (n_in) {
-      mbar_wait(ld_bar0 + 8 * set, (ld_phase >> set) & 1);
+      HAP_ETIMED(tr, 21, mbar_wait(ld_bar0 + 8 * set, (ld_phase >> set) & 1));
       ld_phase ^= 1u << set;
     }
     __syncwarp();
+#ifdef HAP_GEMM_TRACE
+    const unsigned long long t_c = gtimer();
+#endif
     const uint32_t s0 = slot(set, 0), s1 = slot(set, 1), s2 = slot(set, 2);
     // one dispatch per chunk: the 32 columns run a loop specialised on (op, f)
 #define HAP_FUSED_CASE(EPI, TAG) fused_chunk<EPI, TAG>(r, lane, s0, s1, s2)
@@ -595,6 +653,10 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
 #undef HAP_FUSED_CASE
     fence_async_smem();
     __syncwarp();
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(24, gtimer() - t_c);
+    const unsigned long long t_i = gtimer();
+#endif
     if (lane == 0) {
       const int x0 = first + ch * kFusedW;
       tma_store_2d(&pr.c, slot(set, 0), x0, row0);
@@ -607,6 +669,9 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
       }
       bulk_commit();
     }
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(25, gtimer() - t_i);
+#endif
   }
   // a following unit may be unfused: its staging boxes overlap these slots
   if (lane == 0) bulk_wait_read0();
@@ -1190,36 +1255,6 @@ __device__ __forceinline__ void tc_commit_pair(uint32_t bar, uint32_t leader) {
       : "memory");
 }
 
-
-// HAP_GEMM_TRACE builds (tools/gemm_trace.py): per-CTA %globaltimer stamps
-// of the pipeline's milestones, to see where a launch's fixed cost goes.
-#ifdef HAP_GEMM_TRACE
-__device__ unsigned long long* g_trace = nullptr;
-__device__ int g_trace_ctas = 0;
-__device__ __forceinline__ void trace(int ev) {
-  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_trace[blockIdx.x * 16 + ev] = t;
-  }
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void trace_put(int ev, unsigned long long v) {
-  if (g_trace && static_cast<int>(blockIdx.x) < g_trace_ctas) g_trace[blockIdx.x * 16 + ev] = v;
-}
-// time spent in one wait, accumulated into `acc` (ns)
-#define HAP_TIMED(acc, stmt) do { const unsigned long long t_ = gtimer(); stmt; (acc) += gtimer() - t_; } while (0)
-#define HAP_TRACE(ev) trace(ev)
-#define HAP_TRACE_ONCE(ev, flag) do { if (!(flag)) { trace(ev); (flag) = true; } } while (0)
-#else
-#define HAP_TIMED(acc, stmt) stmt
-#define HAP_TRACE_ONCE(ev, flag) ((void)0)
-#define HAP_TRACE(ev) ((void)0)
-#endif
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_constant__ TcBatch bt) {

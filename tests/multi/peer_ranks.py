@@ -18,6 +18,10 @@ import os
 import sys
 import time
 
+# every rank's streams on their own hardware work queues (see
+# paper_2401_05965_b200/__init__.py); before CUDA is initialised
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, os.path.dirname(HERE))

@@ -22,6 +22,10 @@ from paper_2401_05965_b200._lib import BF16, F32, check  # noqa: E402
 EVENTS = {0: "entry", 1: "prologue done", 2: "first TMA issued", 3: "first MMA (stage full)",
           10: "last unit's first MMA", 9: "last TMA issued", 4: "last MMA commit", 5: "first tile in epilogue",
           11: "last tile in epilogue", 6: "last stores issued", 7: "stores complete", 8: "exit"}
+EPI_STEPS = {20: "plain boxes", 16: "plain wait staging read", 17: "plain tcgen05.ld",
+             18: "plain convert+st.shared", 19: "plain TMA issue", 26: "fused chunks",
+             21: "fused input-load wait", 22: "fused wait staging read", 23: "fused tcgen05.ld",
+             24: "fused compute+st.shared", 25: "fused TMA issue"}
 WAITS = {12: "MMA waits for data", 13: "MMA waits for TMEM", 14: "TMA waits for a free stage",
          15: "epilogue waits for a tile"}
 
@@ -31,7 +35,7 @@ def main():
     L.hap_gemm_trace_set.argtypes = [ctypes.c_void_p, ctypes.c_int]
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream()
-    buf = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+    buf = torch.zeros(148 * 32, dtype=torch.int64, device=dev)
     shapes = [("one tile 256x192x64", 256, 192, 64, 0, 0, "none"),
               ("one tile 256x192x768", 256, 192, 768, 0, 0, "none"),
               ("8192x768x768 NN", 8192, 768, 768, 0, 0, "none"), ("8192x768x768 NN add2", 8192, 768, 768, 0, 0, "add2"),
@@ -90,10 +94,14 @@ def main():
                 run()
             torch.cuda.synchronize()
             L.hap_gemm_trace_set(None, 0)
-            t = buf.view(148, 16).cpu()
+            t = buf.view(148, 32).cpu()
             runs.append(t)
         t = runs[-1]
         ctas = int((t[:, 0] > 0).sum())
+        if ctas == 0:
+            print(f"\n{name}: not the SM-pair kernel (no trace), {ev_us:.2f} us per launch")
+            out.append({"name": name, "event_us": round(ev_us, 2), "ctas": 0})
+            continue
         t0 = int(t[:ctas, 0].min())
         row = {"name": name, "event_us": round(ev_us, 2), "ctas": ctas, "events": {}}
         print(f"\n{name}: {ctas} CTAs, back-to-back event time {ev_us:.2f} us per launch")
@@ -114,6 +122,15 @@ def main():
             q = (round(float(w.min()), 2), round(float(w.median()), 2), round(float(w.max()), 2))
             row["events"][label] = q
             print(f"  {label:26s} min {q[0]:8.2f}  med {q[1]:8.2f}  max {q[2]:8.2f} us total per CTA")
+        for ev, label in EPI_STEPS.items():
+            col = t[:ctas, ev].double()
+            if float(col.max()) <= 0:
+                continue
+            w = col if ev in (20, 26) else col / 1e3
+            q = (round(float(w.min()), 2), round(float(w.median()), 2), round(float(w.max()), 2))
+            row["events"][label] = q
+            print(f"  {label:26s} min {q[0]:8.2f}  med {q[1]:8.2f}  max {q[2]:8.2f} {'' if ev in (20, 26) else 'us'}"
+                  " (one epilogue warp)")
         out.append(row)
     if "--json" in sys.argv:
         with open(sys.argv[sys.argv.index("--json") + 1], "w") as fh:
