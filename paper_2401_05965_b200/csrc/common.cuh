@@ -127,6 +127,19 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
   return __float2bfloat16_rn(v);
 }
 
+// Round a pair of fp32 values to storage precision T and back (in place):
+// for bf16 one F2FP pack + two shifts on the ALU pipe — the same
+// round-to-nearest-even as from_f32 per value (F2F, a quarter-rate XU op that
+// MUFU shares) — so vectorised kernels round two values per instruction.
+template <typename T> __device__ __forceinline__ void round2(float& a, float& b);
+template <> __device__ __forceinline__ void round2<float>(float&, float&) {}
+template <> __device__ __forceinline__ void round2<__nv_bfloat16>(float& a, float& b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
+  a = __uint_as_float(u << 16);
+  b = __uint_as_float(u & 0xffff0000u);
+}
+
 // Elementwise unary functions (interpreter.py:141-143), shared by the
 // elementwise kernels and the GEMM's fused epilogues so both round alike.
 __device__ __forceinline__ float unary_fwd(int tag, float x) {
@@ -134,7 +147,12 @@ __device__ __forceinline__ float unary_fwd(int tag, float x) {
     case HAP_EXP: return __expf(x);
     case HAP_NEG: return -x;
     case HAP_RELU: return fmaxf(x, 0.f);
-    case HAP_SIGMOID: return __fdividef(1.f, 1.f + __expf(-x));   // MUFU rcp: ~2 ulp fp32, exact after bf16
+    case HAP_SIGMOID: {   // two MUFU ops: 2^(-x log2 e), then 1 / (1 + that) (~2 ulp fp32)
+      float e, y;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(1.f + e));
+      return y;
+    }
     default: return tanhf(x);
   }
 }

@@ -544,10 +544,11 @@ __global__ void __launch_bounds__(kBlock) swish_fwd_kernel(const T* __restrict__
     float v[8], fy[8], fz[8];
     Vec8<T>::load(x + 8 * i, v);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      fy[j] = to_f32(from_f32<T>(unary_fwd(tag, v[j])));   // z uses the stored (rounded) y
-      fz[j] = v[j] * fy[j];
-    }
+    for (int j = 0; j < 8; ++j) fy[j] = unary_fwd(tag, v[j]);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(fy[j], fy[j + 1]);   // z uses the stored (rounded) y
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fz[j] = v[j] * fy[j];
     Vec8<T>::store(y + 8 * i, fy);
     Vec8<T>::store(z + 8 * i, fz);
   }
@@ -574,11 +575,17 @@ __global__ void __launch_bounds__(kBlock) swish_bwd_kernel(const T* __restrict__
     Vec8<T>::load(y + 8 * i, vy);
     Vec8<T>::load(dz + 8 * i, g);
     if (accumulate) Vec8<T>::load(dx + 8 * i, o);
+    float dy[8], t[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float dy = to_f32(from_f32<T>(g[j] * vx[j]));   // as the unfused path stores dy
-      o[j] += g[j] * vy[j] + to_f32(from_f32<T>(dy * unary_deriv(tag, vx[j], vy[j])));
-    }
+    for (int j = 0; j < 8; ++j) dy[j] = g[j] * vx[j];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(dy[j], dy[j + 1]);   // as the unfused path stores dy
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = dy[j] * unary_deriv(tag, vx[j], vy[j]);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(t[j], t[j + 1]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] += g[j] * vy[j] + t[j];
     Vec8<T>::store(dx + 8 * i, o);
   }
   for (int64_t i = nv * 8 + tid; i < n; i += stride) {
@@ -604,11 +611,15 @@ __global__ void __launch_bounds__(kBlock) gate_fwd_kernel(const T* __restrict__ 
     Vec8<T>::load(b + 8 * i, vb);
     Vec8<T>::load(c + 8 * i, vc);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      vp[j] = to_f32(from_f32<T>(va[j] * vb[j]));
-      vq[j] = to_f32(from_f32<T>(unary_fwd(tag, vp[j])));
-      vo[j] = vq[j] * vc[j];
-    }
+    for (int j = 0; j < 8; ++j) vp[j] = va[j] * vb[j];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(vp[j], vp[j + 1]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) vq[j] = unary_fwd(tag, vp[j]);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(vq[j], vq[j + 1]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) vo[j] = vq[j] * vc[j];
     Vec8<T>::store(p + 8 * i, vp);
     Vec8<T>::store(q + 8 * i, vq);
     Vec8<T>::store(o + 8 * i, vo);
@@ -643,13 +654,20 @@ __global__ void __launch_bounds__(kBlock)
     if (da && acc_a) Vec8<T>::load(da + 8 * i, oa);
     if (db && acc_b) Vec8<T>::load(db + 8 * i, ob);
     if (dc && acc_c) Vec8<T>::load(dc + 8 * i, oc);
+    float dq[8], dp[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dq[j] = vg[j] * vc[j];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(dq[j], dq[j + 1]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dp[j] = dq[j] * unary_deriv(tag, vp[j], vq[j]);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) round2<T>(dp[j], dp[j + 1]);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const float dq = to_f32(from_f32<T>(vg[j] * vc[j]));
-      const float dp = to_f32(from_f32<T>(dq * unary_deriv(tag, vp[j], vq[j])));
       oc[j] += vg[j] * vq[j];
-      oa[j] += dp * vb[j];
-      ob[j] += dp * va[j];
+      oa[j] += dp[j] * vb[j];
+      ob[j] += dp[j] * va[j];
     }
     if (dc) Vec8<T>::store(dc + 8 * i, oc);
     if (da) Vec8<T>::store(da + 8 * i, oa);

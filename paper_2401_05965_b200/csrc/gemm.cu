@@ -514,51 +514,81 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 constexpr int kFusedW = 32;                  // columns per fused box
 constexpr int kFusedBox = 32 * kFusedW * 2;  // bytes per fused box
 
+// bf16 rounding of two fp32 values at once: one F2FP pack (ALU pipe) and two
+// shifts, the same round-to-nearest-even as __float2bfloat16_rn per value
+// (F2F, a quarter-rate XU-pipe op that MUFU shares — with two of them per
+// element and the sigmoid's two MUFU ops, the swish epilogue was XU-bound).
+// Returns the packed pair (low = a) and replaces a, b by their rounded values.
+__device__ __forceinline__ uint32_t round2_bf16(float& a, float& b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
+  a = __uint_as_float(u << 16);
+  b = __uint_as_float(u & 0xffff0000u);
+  return u;
+}
+
+__device__ __forceinline__ void sts_u32x4(uint32_t at, const uint32_t (&p)[4]) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]));
+}
+
 // The elementwise op of one 32-column chunk: r = accumulator columns of the
 // lane's row; s0..s2 = the chunk's staging slots (inputs in place, outputs).
+// Values are rounded to bf16 exactly where the unfused kernels store them,
+// two at a time (round2_bf16).
 template <int EPI, int TAG>
 __device__ __forceinline__ void fused_chunk(const uint32_t (&r)[32], int lane, uint32_t s0, uint32_t s1,
                                             uint32_t s2) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {   // 8 columns: 16-byte chunk j of the lane's 64-byte row
     const uint32_t off = swz_offset<64>(lane, j);
-    float c[8], x[8], o0[8], o1[8], o2[8];
+    float c[8], x[8], y[8];
+    uint32_t p0[4], p1[4], p2[4];
 #pragma unroll
     for (int e = 0; e < 8; ++e) c[e] = __uint_as_float(r[8 * j + e]);
-    if constexpr (EPI == EPI_OP_ADD) {
+    if constexpr (EPI == EPI_OP_ADD) {   // C = bf16(acc + R)
       lds_bf16x8(s0 + off, x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o0[e] = c[e] + x[e];
-    } else if constexpr (EPI == EPI_OP_ADD2) {
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e] + x[e], b = c[e + 1] + x[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
+      }
+    } else if constexpr (EPI == EPI_OP_ADD2) {   // C = bf16(acc); Y = bf16(C + R)
       lds_bf16x8(s1 + off, x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        o0[e] = c[e];
-        o1[e] = bf16_round(c[e]) + x[e];
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e], b = c[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
+        float u = a + x[e], v = b + x[e + 1];
+        p1[e / 2] = round2_bf16(u, v);
       }
-    } else if constexpr (EPI == EPI_OP_SWISH) {
+    } else if constexpr (EPI == EPI_OP_SWISH) {   // C = bf16(acc); Y = bf16(f(C)); Z = bf16(C * Y)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float cv = bf16_round(c[e]);
-        const float yv = bf16_round(unary_fwd_t<TAG>(cv));
-        o0[e] = cv;
-        o1[e] = yv;
-        o2[e] = cv * yv;
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e], b = c[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
+        float ya = unary_fwd_t<TAG>(a), yb = unary_fwd_t<TAG>(b);
+        p1[e / 2] = round2_bf16(ya, yb);
+        float za = a * ya, zb = b * yb;
+        p2[e / 2] = round2_bf16(za, zb);
       }
     } else {   // EPI_OP_SWISH_BWD: C = dz*y + (dz*x)*f'(x, y), dz = rounded accumulator
-      float y[8];
       lds_bf16x8(s0 + off, x);
       lds_bf16x8(s1 + off, y);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float gz = bf16_round(c[e]);
-        const float dy = bf16_round(gz * x[e]);
-        o0[e] = gz * y[e] + bf16_round(dy * unary_deriv(TAG, x[e], y[e]));
+      for (int e = 0; e < 8; e += 2) {
+        float ga = c[e], gb = c[e + 1];
+        round2_bf16(ga, gb);
+        float da = ga * x[e], db = gb * x[e + 1];
+        round2_bf16(da, db);
+        float ta = da * unary_deriv(TAG, x[e], y[e]), tb = db * unary_deriv(TAG, x[e + 1], y[e + 1]);
+        round2_bf16(ta, tb);
+        float oa = ga * y[e] + ta, ob = gb * y[e + 1] + tb;
+        p0[e / 2] = round2_bf16(oa, ob);
       }
     }
-    sts_bf16x8(s0 + off, o0);
-    if constexpr (EPI == EPI_OP_ADD2 || EPI == EPI_OP_SWISH) sts_bf16x8(s1 + off, o1);
-    if constexpr (EPI == EPI_OP_SWISH) sts_bf16x8(s2 + off, o2);
+    sts_u32x4(s0 + off, p0);
+    if constexpr (EPI == EPI_OP_ADD2 || EPI == EPI_OP_SWISH) sts_u32x4(s1 + off, p1);
+    if constexpr (EPI == EPI_OP_SWISH) sts_u32x4(s2 + off, p2);
   }
 }
 

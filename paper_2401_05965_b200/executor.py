@@ -908,12 +908,21 @@ class Executor:
         return "side" if self._emit_on is not None else "main"
 
     SIDE_P2P_CTAS = 32
+    IN_PROCESS_P2P_CTAS = 16
 
     def _p2p_cap(self, tag: str) -> int:
         """Grid cap of a peer kernel: the rank's SM cap; on the side stream at
         most SIDE_P2P_CTAS, so a spinning side-stream kernel leaves the
-        compute stream's persistent GEMM most of the GPU."""
+        compute stream's persistent GEMM most of the GPU.  Ranks sharing one
+        GPU (thread_peer_groups): at most IN_PROCESS_P2P_CTAS, because a
+        rank's peer kernel spins while its partner may still be running a
+        persistent SM-pair GEMM, whose CTAs (clusters of two on one TPC) must
+        all become resident: the hardware may place the spinner's CTAs one
+        per TPC, so with m ranks at most m x 16 TPCs are held, leaving the
+        largest capped GEMM (ceil(148 / m / 2) TPCs) room on the 74."""
         cap = self.caps[self.group.rank] or 148
+        if getattr(self.group, "in_process", False):
+            return min(cap, self.IN_PROCESS_P2P_CTAS)
         return min(cap, self.SIDE_P2P_CTAS) if tag == "side" else cap
 
     def _register(self, tag: str, buf: Buf) -> dict:

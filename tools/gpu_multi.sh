@@ -1,7 +1,7 @@
 #!/bin/bash
 # One multi-GPU session under `gpurun --gpus N`: collective latency/bandwidth
-# sweeps for the cost model, NVLink counters of the peer-memory kernels (ncu,
-# one pass), bench lines (BERT, BERT-MoE with each gradient sync, ViT-MoE with
+# sweeps for the cost model, NVLink hardware byte counters (NVML) around the
+# peer-memory kernels, bench lines (BERT, BERT-MoE with each gradient sync, ViT-MoE with
 # each collective implementation) and the NCCL-group parity run.  Outputs in
 # gpurun_out/m$N/.
 N=${1:-2}
@@ -14,12 +14,7 @@ nvidia-smi topo -m > $OUT/topo.txt 2>&1
 timeout 900 trun tools/coll_fit.py --json $OUT/coll_fit.json > $OUT/coll_fit.log 2>&1; echo "coll_fit rc=$?" >> $OUT/status.txt
 # this box's fitted lines drive gather="auto" in the bench runs below (merged with the other world sizes locally)
 python tools/coll_fit.py --fit $OUT/coll_fit.json >> $OUT/coll_fit.log 2>&1; cp paper_2401_05965_b200/collectives_b200.json $OUT/ 2>/dev/null
-timeout 300 trun tools/nvlink_ncu.py --json $OUT/nvl_events.json > $OUT/nvl_events.log 2>&1; echo "nvl_events rc=$?" >> $OUT/status.txt
-port=$((port + 1))
-timeout 900 ncu --target-processes all -k regex:p2p_ --clock-control none --csv \
-  --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum \
-  --log-file $OUT/nvl_ncu.csv python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-  --master-port $port tools/nvlink_ncu.py --calls 2 > $OUT/nvl_ncu.log 2>&1; echo "nvl_ncu rc=$?" >> $OUT/status.txt
+timeout 300 trun tools/nvlink_ncu.py --nvml --rows 16384,65536,262144 --json $OUT/nvl_counters.json > $OUT/nvl_counters.log 2>&1; echo "nvl_counters rc=$?" >> $OUT/status.txt
 for args in "--workload bert" "--workload moe" "--workload moe --grad-sync sfb" "--workload moe --grad-sync all_reduce" \
             "--workload vitmoe" "--workload vitmoe --collectives p2p" "--workload vitmoe --collectives nccl"; do
   tag=$(echo $args | tr -d '-' | tr ' ' '_')

@@ -8,6 +8,12 @@ nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum \\
         --log-file gpurun_out/nvl.csv \\
         torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/nvlink_ncu.py
 
+--nvml (no profiler): the GPU's NVLink data counters (NVML field values
+NVLINK_THROUGHPUT_DATA_TX / _RX, summed over the links, KiB) are read before
+and after `--reps` back-to-back calls of each collective; the line then holds
+the counted NVLink bytes per call beside the algorithmic ones and the
+achieved GB/s from CUDA events over the same calls (max over ranks).
+
 Each rank runs, eagerly with a barrier between calls, the push all-gather,
 the direct reduce-scatter, the two-shot all-reduce and the push all-to-all of
 a [rows, 768] bf16 tensor sharded by the bench's SM-cap ratios (the executor's
@@ -26,6 +32,26 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
+def _nvlink_kib(index: int) -> tuple[int, int]:
+    """(tx, rx) NVLink data KiB of GPU `index` since boot, summed over its links."""
+    import pynvml as nv
+
+    nv.nvmlInit()
+    h = nv.nvmlDeviceGetHandleByIndex(index)
+    tx = rx = 0
+    for link in range(18):
+        try:
+            vals = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                   (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+        except nv.NVMLError:
+            break
+        if vals[0].nvmlReturn or vals[1].nvmlReturn:
+            continue
+        tx += vals[0].value.ullVal
+        rx += vals[1].value.ullVal
+    return tx, rx
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -39,6 +65,8 @@ def main():
     ap.add_argument("--rows", default="16384,65536")
     ap.add_argument("--calls", type=int, default=3)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--nvml", action="store_true", help="NVML NVLink byte counters instead of an ncu capture")
+    ap.add_argument("--reps", type=int, default=100)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -100,6 +128,30 @@ def main():
                                                              max(send_counts), cap, stream),
                                 (sum(recv_counts) - recv_counts[rank]) * b, (sum(send_counts) - send_counts[rank]) * b),
         }
+        if args.nvml:
+            for name, (fn, rx, tx) in ops.items():
+                check(fn(), name)
+                torch.cuda.synchronize(dev)
+                dist.barrier()
+                c0 = _nvlink_kib(local)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(args.reps):
+                    check(fn(), name)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                c1 = _nvlink_kib(local)
+                ms = torch.tensor([e0.elapsed_time(e1) / args.reps], device=dev)
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+                t = float(ms) * 1e-3
+                ctx_b = (c1[0] - c0[0]) * 1024 / args.reps, (c1[1] - c0[1]) * 1024 / args.reps
+                report.append({"rank": rank, "op": name, "rows": rows, "rx_bytes": rx, "tx_bytes": tx,
+                               "us_per_call_max_over_ranks": round(t * 1e6, 2),
+                               "nvlink_tx_bytes_counted": ctx_b[0], "nvlink_rx_bytes_counted": ctx_b[1],
+                               "alg_GBps": round(max(rx, tx) / t / 1e9, 1),
+                               "counted_GBps": round(max(ctx_b) / t / 1e9, 1),
+                               "frac_of_770": round(max(rx, tx) / t / 770e9, 3)})
+            continue
         for name, (fn, rx, tx) in ops.items():
             times = []
             for _ in range(args.calls):
