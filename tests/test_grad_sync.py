@@ -49,3 +49,45 @@ def test_moe_plans_are_comm_free_forward(cname):
     assert not [i for i in prog.instrs if i.is_comm]
     params = [i for i in prog.instrs if i.kind == "parameter"]
     assert len(params) == 8
+
+
+def test_collective_implementation_flips_at_the_fitted_crossover(monkeypatch):
+    """Executor._use_p2p prices both implementations of a call site with the
+    reference cost model (cost_model.comm_time) on each implementation's
+    fitted line and takes the cheaper: with a low-latency / lower-bandwidth
+    kernel line and a high-latency / higher-bandwidth NCCL line the choice
+    flips from the kernel to NCCL where the lines cross."""
+    from paper_2401_05965_b200.executor import Executor
+
+    lat_p, bw_p, lat_n, bw_n = 8e-6, 400e9, 30e-6, 700e9
+    fits = {kind: {"p2p": {"latency_s": lat_p, "bw_Bps": bw_p}, "nccl": {"latency_s": lat_n, "bw_Bps": bw_n}}
+            for kind in ("all_gather", "reduce_scatter", "all_reduce", "all_to_all")}
+    monkeypatch.setattr(workloads, "_FITS", {2: fits})
+
+    class _Group:
+        comm = object()
+        distributed = True
+        rank = 0
+
+    class _Cfg:
+        gather = "auto"
+        ratios = (0.5, 0.5)
+
+    ex = Executor.__new__(Executor)
+    ex.__dict__.update(group=_Group(), cfg=_Cfg(), caps=[148, 148], impl_choice=[], _peer_ok=True)
+    from paper_2401_05965_b200.cost_model import ClusterSpec, comm_time
+    from paper_2401_05965_b200.program import Instruction
+
+    specs = ex._impl_specs(2)
+    assert specs is not None
+    for kind in ("all_gather", "reduce_scatter", "all_reduce", "all_to_all"):
+        choices = []
+        for elements in [2 ** k for k in range(8, 26)]:
+            choices.append(ex._use_p2p(kind, elements, 2))
+            ins = Instruction(kind, "t", elements=elements)
+            t_p, t_n = comm_time(ins, (0.5, 0.5), specs["p2p"]), comm_time(ins, (0.5, 0.5), specs["nccl"])
+            assert choices[-1] == (t_p <= t_n)
+        assert choices[0] and not choices[-1], (kind, choices)   # kernel for small calls, NCCL for large
+        flips = sum(a != b for a, b in zip(choices, choices[1:]))
+        assert flips == 1, (kind, choices)
+    assert isinstance(specs["p2p"], ClusterSpec)
