@@ -253,6 +253,10 @@ hap_status hap_symm_destroy(void* ctx);
 hap_status hap_symm_open_local(void* ctx, const int64_t* peer_bases);
 void* hap_symm_local_base(void* ctx);
 int64_t hap_symm_capacity(void* ctx);
+/* Debugging: copy this rank's 512-byte signal page (per-peer ready / done /
+ * armed flags, call epoch, grid-barrier counters) to host memory through a
+ * private non-blocking stream — usable while peer kernels spin. */
+hap_status hap_symm_peek(void* ctx, void* host512);
 /* all_gather along a blocked axis with uneven shards — interpreter.py:69-71:
  * rank j's shard is [outer, sizes[j], inner]; the output is
  * [outer, extent, inner] with shard j at offsets[j].  Peers' shards are read

@@ -83,6 +83,7 @@ SIGNATURES = {
     "hap_symm_capacity": (c_int64, [_P]),
     "hap_symm_open_local": (c_int, [_P, _I64P]),
     "hap_symm_local_base": (c_void_p, [_P]),
+    "hap_symm_peek": (c_int, [_P, _P]),
     "hap_p2p_all_reduce": (c_int, [_P, _P, _P, c_int, c_int64, c_int, _P]),
     "hap_p2p_all_to_all": (c_int, [_P, _P, _P, c_int, _P, _P, _P, c_int64, c_int, _P]),
     "hap_p2p_probe": (c_int, [_P, c_int, c_int64, c_int, _P]),

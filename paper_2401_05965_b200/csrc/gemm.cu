@@ -41,19 +41,30 @@ constexpr int UMMA_K = 16;
 constexpr int kThreads = 384;   // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
 
-// Epilogue staging: 8 warps x 2 buffers x (32 rows x 128 B), 128B-swizzled
-// boxes for TMA bulk stores.
-constexpr int kStageOutBytes = kEpiWarps * 2 * 32 * 128;
+// Epilogue staging: one 4 KB box (32 rows x 128 B, or two 32 x 64 B boxes)
+// per epilogue warp, where the warp transposes its row-per-lane accumulator
+// values into full-line coalesced global stores (box_out).  The other 190 KB
+// or so go to the operand pipeline.
+constexpr int kEpiBoxBytes = 4096;        // plain epilogues
+constexpr int kEpiBoxBytesFused = 8192;   // fused epilogues (drain_fused's slots)
+constexpr int kSmemLimit = 232448;        // 227 KB per CTA
+constexpr int kMaxStages = 8;             // barrier slots reserved
+// operand stages that fit beside the epilogue boxes, the barriers and the
+// 1 KB alignment slack
+constexpr int stages_for(int stage_bytes, int box_bytes) {
+  return (kSmemLimit - 1024 - 512 - kEpiWarps * box_bytes) / stage_bytes < kMaxStages
+             ? (kSmemLimit - 1024 - 512 - kEpiWarps * box_bytes) / stage_bytes
+             : kMaxStages;
+}
 
 template <int BN>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 3 : 5;
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kBarrierBytes = 512;
-  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + kBarrierBytes + 1024;
+  static int smem(int nst, int box) { return nst * kStageBytes + kEpiWarps * box + kBarrierBytes + 1024; }
 };
 
 // HAP_GEMM_TRACE builds (tools/gemm_trace.py): per-CTA %globaltimer stamps
@@ -310,6 +321,47 @@ __device__ __forceinline__ uint32_t swz_offset(int r, int c) {
   else return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
 }
 
+__device__ __forceinline__ void red_add_v4(float* p, const uint32_t (&q)[4]) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(q[0])),
+               "f"(__uint_as_float(q[1])), "f"(__uint_as_float(q[2])), "f"(__uint_as_float(q[3]))
+               : "memory");
+}
+
+// Copy one staged 32-row box (rows of kRowBytes, swizzled 16-byte chunks) to
+// global memory with full-line coalesced accesses: per pass, CPR consecutive
+// lanes cover one row, the warp 32 / CPR rows.  kAdd (fp32 accumulate):
+// vector reduce-add — one writer per element, so the result is the same
+// whatever the order.  Rows >= M and columns >= N are not written.
+template <typename OutT, int kRowBytes, bool kAdd>
+__device__ __forceinline__ void box_out(uint32_t box, int lane, OutT* C, int64_t ldc, int row0, int col0, int M,
+                                        int N, int vec_ok) {
+  constexpr int CPR = kRowBytes / 16;
+  constexpr int EPC = 16 / static_cast<int>(sizeof(OutT));
+  constexpr int RPP = 32 / CPR;
+#pragma unroll
+  for (int it = 0; it < CPR; ++it) {
+    const int r = it * RPP + lane / CPR, c = lane % CPR;
+    uint32_t q[4];
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
+                 : "r"(box + swz_offset<kRowBytes>(r, c)));
+    const int row = row0 + r, col = col0 + c * EPC;
+    if (row >= M || col >= N) continue;
+    OutT* dst = C + static_cast<int64_t>(row) * ldc + col;
+    if (vec_ok && col + EPC <= N) {
+      if constexpr (kAdd) red_add_v4(reinterpret_cast<float*>(dst), q);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(q[0], q[1], q[2], q[3]);
+    } else {
+      const OutT* v = reinterpret_cast<const OutT*>(q);
+      const int valid = N - col < EPC ? N - col : EPC;
+      for (int e = 0; e < valid; ++e) {
+        if constexpr (kAdd) dst[e] = static_cast<float>(dst[e]) + static_cast<float>(v[e]);
+        else dst[e] = v[e];
+      }
+    }
+  }
+}
+
 // Drain one warp's 32 rows x BN/2 columns of a finished accumulator.
 // TMA modes stage 32 x 128 B boxes (64 bf16 or 32 fp32 columns) in a
 // 128B-swizzled double buffer — 16-byte chunk c of row r at c ^ (r & 7), the
@@ -337,23 +389,21 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
     }
     return;
   }
-  // Box rows of 128 B (SWIZZLE_128B) when the warp's BN/2 columns split into
-  // them evenly, else 64 B rows (SWIZZLE_64B: chunk c of row r at c ^ (r>>1 & 3)).
+  // Box rows of 128 B when the warp's BN/2 columns split into them evenly,
+  // else 64 B rows; 16-byte chunk c of row r is stored at the swizzled
+  // position (swz_offset) so the row-per-lane writes and the row-major reads
+  // of box_out both hit every bank.
   constexpr int kWide = 128 / static_cast<int>(sizeof(OutT));
   constexpr int W = ((BN / 2) % kWide == 0) ? kWide : kWide / 2;   // columns per box
   constexpr int kRowBytes = W * static_cast<int>(sizeof(OutT));
   constexpr int kBoxes = (BN / 2) / W;
-  const uint32_t buf0 = smem_u32(buf);
+  const uint32_t box = smem_u32(buf);
   const bool tr = quarter == 0 && half == 0 && lane == 0;
   (void)tr;
+  (void)box_seq;
+  (void)tmC;
 #pragma unroll 1
   for (int b = 0; b < kBoxes; ++b) {
-    // the two staging buffers alternate across boxes AND units (a unit with
-    // an odd box count must not restart on the buffer its last box is still
-    // being stored from)
-    const uint32_t dst = buf0 + (box_seq++ & 1) * 4096;
-    HAP_ETIMED(tr, 16, if (lane == 0) bulk_wait_read1());   // the buffer's previous box has been read out
-    __syncwarp();
 #ifdef HAP_GEMM_TRACE
     if (tr) trace_add(20, 1);
     const unsigned long long t_st = gtimer();
@@ -367,7 +417,7 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
         static_assert(W % 32 == 0 || W == 16, "fp32 box width");
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t at = dst + swz_offset<kRowBytes>(lane, j);
+          const uint32_t at = box + swz_offset<kRowBytes>(lane, j);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(r[4 * j]), "r"(r[4 * j + 1]),
                        "r"(r[4 * j + 2]), "r"(r[4 * j + 3]));
         }
@@ -381,22 +431,27 @@ __device__ __forceinline__ void drain_accumulator(uint32_t tmem_acc, int quarter
                                                      __uint_as_float(r[8 * j + 2 * e + 1]));
             p[e] = *reinterpret_cast<uint32_t*>(&h);
           }
-          const uint32_t at = dst + swz_offset<kRowBytes>(lane, k * 4 + j);
+          const uint32_t at = box + swz_offset<kRowBytes>(lane, k * 4 + j);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]),
                        "r"(p[3]));
         }
       }
     }
-    fence_async_smem();
     __syncwarp();
 #ifdef HAP_GEMM_TRACE
     if (tr) trace_add(18, gtimer() - t_st);
+    const unsigned long long t_o = gtimer();
 #endif
-    HAP_ETIMED(tr, 19, if (lane == 0) {
-      if (mode == EPI_TMA_ADD) tma_reduce_add_2d(tmC, dst, first + b * W, row0);
-      else tma_store_2d(tmC, dst, first + b * W, row0);
-      bulk_commit();
-    });
+    if (mode == EPI_TMA_ADD) {
+      if constexpr (std::is_same<OutT, float>::value)
+        box_out<float, kRowBytes, true>(box, lane, C, ldc, row0, first + b * W, M, N, vec_ok);
+    } else {
+      box_out<OutT, kRowBytes, false>(box, lane, C, ldc, row0, first + b * W, M, N, vec_ok);
+    }
+    __syncwarp();   // every lane has read the box before the next one is written
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(19, gtimer() - t_o);
+#endif
   }
 }
 
@@ -435,6 +490,11 @@ struct alignas(64) TcProblem {
 
 struct alignas(64) TcBatch {
   TcProblem p[kMaxProblems];
+  // shared-memory layout of this launch: nst operand stages, then one
+  // epilogue box of box_bytes per epilogue warp (4 KB; 8 KB when a fused
+  // epilogue stages its TMA-loaded inputs and three-output chunks), then the
+  // barriers — a plain launch turns the spare 32 KB into pipeline depth
+  int nst, box_bytes;
   int count;
   int sum_k;
   int sum_kb;              // sum_k: K blocks of all problems (the concatenated K range)
@@ -618,6 +678,8 @@ __device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_a
     tma_load_2d(in_slot(set, 0), &pr.e1, bar, x0, row0);
     if (n_in == 2) tma_load_2d(in_slot(set, 1), &pr.e2, bar, x0, row0);
   };
+  fence_async_smem();   // a preceding plain unit's generic accesses to this box come first
+  __syncwarp();
   if (lane == 0) {
     bulk_wait_read0();   // the previous unit's stores have read the staging slots
     if (n_in) issue_loads(0);
@@ -724,9 +786,10 @@ __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem
       return;
     }
   }
-  if (pr.epi_mode == EPI_SPLIT_WS) {
-    drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0, pr.M, pr.N, pr.ws,
-                                 pr.ws_ld, EPI_TMA_STORE, 1, 0, &pr.c, buf, box_seq);
+  if (pr.epi_mode == EPI_SPLIT_WS) {   // split s's slice: rows [s * ws_rows, s * ws_rows + M)
+    drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, split * pr.ws_rows + row0, col0,
+                                 split * pr.ws_rows + pr.M, pr.N, pr.ws, pr.ws_ld, EPI_TMA_STORE, 1, 0, &pr.c, buf,
+                                 box_seq);
     return;
   }
   drain_accumulator<BN, OutT>(tmem_acc, quarter, half, lane, row0, col0, pr.M, pr.N, static_cast<OutT*>(pr.C),
@@ -802,12 +865,9 @@ __device__ __forceinline__ void csplit_chain(const TcProblem& pr, const Unit& x,
   drain_accumulator<BN, float>(tmem_acc, quarter, half, lane, row0, x.n0, pr.M, pr.N, static_cast<float*>(pr.C),
                                pr.ldc, mode, pr.vec_ok, (x.split > 0 || pr.accumulate) ? 1 : 0, &pr.c, buf,
                                box_seq);
-  if (lane == 0) bulk_wait_complete();
+  __threadfence();   // this lane's adds into C are performed before the turn passes
   __syncwarp();
-  if (next_rank >= 0 && lane == 0) {
-    __threadfence();
-    chain_pass(map_to_cta(turn, static_cast<uint32_t>(next_rank)));
-  }
+  if (next_rank >= 0 && lane == 0) chain_pass(map_to_cta(turn, static_cast<uint32_t>(next_rank)));
 }
 
 template <int BN>
@@ -1044,13 +1104,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* staging = smem + G::kStages * G::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStageOutBytes);
+  const int nst = bt.nst;
+  uint8_t* staging = smem + nst * G::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kEpiWarps * bt.box_bytes);
   const uint32_t full0 = smem_u32(bars);
-  const uint32_t empty0 = smem_u32(bars + G::kStages);
-  const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
-  const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
+  const uint32_t empty0 = smem_u32(bars + nst);
+  const uint32_t tfull0 = smem_u32(bars + 2 * nst);
+  const uint32_t tempty0 = smem_u32(bars + 2 * nst + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * nst + 4);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_units = bt.total_units;
@@ -1062,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < G::kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
     }
@@ -1070,8 +1131,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, kEpiWarps * 32);
     }
-    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
-    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 22 + w), 1);   // split-K turns
+    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * nst + 6 + w), 1);
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * nst + 22 + w), 1);   // split-K turns
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -1113,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           } else {
             tma_load_2d(sb, mb, fb, k0, x.n0);
           }
-          if (++stage == G::kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -1153,7 +1214,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
           }
           first = false;
           tc_commit(empty0 + 8 * stage);
-          if (++stage == G::kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -1167,9 +1228,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // ---------------- epilogue: TMEM -> registers -> (smem -> TMA | global)
     const int quarter = warp & 3;              // TMEM lanes 32*quarter .. +31
     const int half = (warp - 4) >> 2;          // which half of the tile's columns
-    uint8_t* buf = staging + (warp - 4) * 8192;
+    uint8_t* buf = staging + (warp - 4) * bt.box_bytes;
     uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
-    const uint32_t ld_bar = smem_u32(bars + 2 * G::kStages + 6 + 2 * (warp - 4));   // fused-epilogue input loads
+    const uint32_t ld_bar = smem_u32(bars + 2 * nst + 6 + 2 * (warp - 4));   // fused-epilogue input loads
     uint32_t ld_phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1182,7 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         if constexpr (std::is_same<OutT, float>::value) {   // splits add into C in rank order
           const int rnk = static_cast<int>(cluster_rank());
           csplit_chain<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, x.m0 + quarter * 32, buf, box_seq,
-                           smem_u32(bars + 2 * G::kStages + 22 + (warp - 4)), rnk + 1 < bt.csplit ? rnk + 1 : -1);
+                           smem_u32(bars + 2 * nst + 22 + (warp - 4)), rnk + 1 < bt.csplit ? rnk + 1 : -1);
         } else {
           // the partial goes to this CTA's shared memory (the pipeline stages
           // are idle: this was the CTA's only unit); the cluster reduces it
@@ -1234,12 +1295,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 template <int BN, bool kBMN = false>
 struct Cfg2 {
   static constexpr int kHalfLoaded = kBMN ? ((BN / 2 + 63) / 64) * 64 : BN / 2;
-  static constexpr int kStages = BN == 128 ? 6 : 5;
   static constexpr int kABytes = 128 * BK * 2;
   static constexpr int kBBytes = kHalfLoaded * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kSmem = kStages * kStageBytes + kStageOutBytes + 512 + 1024;
+  static int smem(int nst, int box) { return nst * kStageBytes + kEpiWarps * box + 512 + 1024; }
 };
 
 
@@ -1293,13 +1353,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* staging = smem + G::kStages * G::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kStageOutBytes);
+  const int nst = bt.nst;
+  uint8_t* staging = smem + nst * G::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + kEpiWarps * bt.box_bytes);
   const uint32_t full0 = smem_u32(bars);
-  const uint32_t empty0 = smem_u32(bars + G::kStages);
-  const uint32_t tfull0 = smem_u32(bars + 2 * G::kStages);
-  const uint32_t tempty0 = smem_u32(bars + 2 * G::kStages + 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * G::kStages + 4);
+  const uint32_t empty0 = smem_u32(bars + nst);
+  const uint32_t tfull0 = smem_u32(bars + 2 * nst);
+  const uint32_t tempty0 = smem_u32(bars + 2 * nst + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * nst + 4);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // launched in clusters of 2 (one SM pair) or, under cluster split K, of
@@ -1319,7 +1380,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < G::kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full0 + 8 * s, 2);   // one producer arrival per CTA (+ both CTAs' bytes)
       mbar_init(empty0 + 8 * s, 1);  // the leader's multicast commit
     }
@@ -1327,8 +1388,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
     }
-    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 6 + w), 1);
-    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * G::kStages + 22 + w), 1);   // split-K turns
+    for (int w = 0; w < 2 * kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * nst + 6 + w), 1);
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(smem_u32(bars + 2 * nst + 22 + w), 1);   // split-K turns
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -1384,7 +1445,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
           HAP_TRACE_ONCE(2, traced);
           HAP_TRACE(9);
 #endif
-          if (++stage == G::kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -1433,7 +1494,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
           }
           first = false;
           tc_commit_pair(empty0 + 8 * stage, leader);
-          if (++stage == G::kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -1454,9 +1515,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
     // ---------------- epilogue (both CTAs): own 128 rows of the 256-row tile
     const int quarter = warp & 3;
     const int half = (warp - 4) >> 2;
-    uint8_t* buf = staging + (warp - 4) * 8192;
+    uint8_t* buf = staging + (warp - 4) * bt.box_bytes;
     uint32_t box_seq = 0;   // staging-buffer alternation, continued across units
-    const uint32_t ld_bar = smem_u32(bars + 2 * G::kStages + 6 + 2 * (warp - 4));   // fused-epilogue input loads
+    const uint32_t ld_bar = smem_u32(bars + 2 * nst + 6 + 2 * (warp - 4));   // fused-epilogue input loads
     uint32_t ld_phase = 0;
     const uint32_t leader_tempty = map_to_cta(tempty0, leader);
     int acc = 0;
@@ -1479,7 +1540,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
         if constexpr (std::is_same<OutT, float>::value) {   // the pairs add into C in rank order
           const int nxt = static_cast<int>(crank) + 2;
           csplit_chain<BN>(pr, x, tmem_base + acc * BN, quarter, half, lane, m0 + quarter * 32, buf, box_seq,
-                           smem_u32(bars + 2 * G::kStages + 22 + (warp - 4)), nxt < 2 * bt.csplit ? nxt : -1);
+                           smem_u32(bars + 2 * nst + 22 + (warp - 4)), nxt < 2 * bt.csplit ? nxt : -1);
         } else {   // partial to this CTA's idle pipeline smem, reduced after the loop
           fence_async_smem();
           csplit_drain<BN>(tmem_base + acc * BN, quarter, half, lane, smem, x.kb0 >= x.kb1);
@@ -1610,7 +1671,7 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
   {
     std::lock_guard<std::mutex> lock(mu);
     if (std::find(configured.begin(), configured.end(), reinterpret_cast<const void*>(kern)) == configured.end()) {
-      HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+      HAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
       configured.push_back(reinterpret_cast<const void*>(kern));
     }
   }
@@ -1638,18 +1699,27 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
 }
 
 template <int BN, bool kAMN, bool kBMN, typename OutT>
-hap_status launch_shape(bool pair, const TcBatch& bt, int cap, cudaStream_t stream) {
+hap_status launch_shape(bool pair, const TcBatch& bt_in, int cap, cudaStream_t stream) {
+  TcBatch bt = bt_in;
+  bool fused = false;
+  for (int q = 0; q < bt.count; ++q) fused = fused || bt.p[q].epi != EPI_OP_NONE;
+  bt.box_bytes = fused ? kEpiBoxBytesFused : kEpiBoxBytes;
   if (pair || BN == 192) {   // 192-wide tiles exist only for SM pairs
+    using G = Cfg2<BN, kBMN>;
+    bt.nst = stages_for(G::kStageBytes, bt.box_bytes);
     // clusters of one pair, or (cluster split K) of the csplit pairs of a tile, one unit each
     const int pairs = bt.csplit > 1 ? bt.total_units : std::min<int>(bt.total_units, std::max(1, cap / 2));
-    return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, Cfg2<BN, kBMN>::kSmem, bt, 2 * pairs, stream,
+    return launch_batch(gemm_tc2_kernel<BN, kAMN, kBMN, OutT>, G::smem(bt.nst, bt.box_bytes), bt, 2 * pairs, stream,
                         "gemm_tc2_kernel", bt.csplit > 1 ? 2 * bt.csplit : 2);
   }
   if constexpr (BN != 192) {
+    using G = Cfg<BN>;
+    bt.nst = stages_for(G::kStageBytes, bt.box_bytes);
+    const int smem = G::smem(bt.nst, bt.box_bytes);
     if (bt.csplit > 1)   // one CTA per unit, the splits of a tile one cluster
-      return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, bt.total_units, stream,
+      return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, smem, bt, bt.total_units, stream,
                           "gemm_tc_kernel (cluster split K)", bt.csplit);
-    return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, Cfg<BN>::kSmem, bt, std::min(bt.total_units, cap),
+    return launch_batch(gemm_tc_kernel<BN, kAMN, kBMN, OutT>, smem, bt, std::min(bt.total_units, cap),
                         stream, "gemm_tc_kernel");
   }
   return HAP_ERR_UNSUPPORTED;

@@ -843,6 +843,21 @@ extern "C" hap_status hap_symm_open_local(void* ctx, const int64_t* peer_bases) 
   return HAP_OK;
 }
 
+extern "C" hap_status hap_symm_peek(void* ctx, void* host512) {
+  auto* s = static_cast<Symm*>(ctx);
+  HAP_CHECK_ARG(s && host512, "hap_symm_peek: bad arguments");
+  cudaStream_t st = nullptr;
+  HAP_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(host512, s->local, kSignalBytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) {
+    set_error(std::string("hap_symm_peek: ") + cudaGetErrorString(e));
+    return HAP_ERR_CUDA;
+  }
+  return HAP_OK;
+}
+
 extern "C" void* hap_symm_local_base(void* ctx) {
   auto* s = static_cast<Symm*>(ctx);
   return s ? s->local : nullptr;

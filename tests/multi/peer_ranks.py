@@ -87,6 +87,28 @@ def run_local(doc, shapes, inputs, dtype, sync):
 LIVE: list = []   # executors of the current run (the watchdog's view)
 
 
+def _dump_signal_pages():
+    """Each rank's peer-memory signal pages (p2p.cu SignalPage: ready, done,
+    armed per peer, epoch, grid-barrier counters), read through a private
+    non-blocking stream while the kernels spin (hap_symm_peek)."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2401_05965_b200 import _lib
+
+    L = _lib.lib()
+    m = len(LIVE)
+    for r, ex in enumerate(LIVE):
+        for tag, ctx in ex.__dict__.get("_symm", {}).items():
+            buf = (ctypes.c_uint64 * 64)()
+            st = L.hap_symm_peek(ctx, buf)
+            a = np.frombuffer(buf, dtype=np.uint64)
+            gen = (int(a[49]) >> 32, int(a[49]) & 0xffffffff)
+            print(f"[watchdog] rank {r} {tag} page (status {st}): ready {a[0:m].tolist()} done {a[16:16 + m].tolist()} "
+                  f"armed {a[32:32 + m].tolist()} epoch {int(a[48])} barrier (generation, arrive) {gen}", flush=True)
+
+
 def _install_watchdog(args):
     """--verbose: every eager op is followed by a CUDA event; when no rank
     makes progress for 30 s, print each rank's first incomplete op, the GPU
@@ -131,6 +153,7 @@ def _install_watchdog(args):
                 trace = LIVE[r].__dict__.get("op_trace", [])
                 lo = max(0, (first or 0) - 4)
                 print(f"[watchdog]   ops {lo}..: {[w for w, _ in trace[lo:(first or 0) + 3]]}", flush=True)
+            _dump_signal_pages()
             print(f"[watchdog] GPU utilisation {util}; exiting", flush=True)
             os._exit(3)
 
