@@ -229,6 +229,29 @@ def run_ranks(fns: list) -> list:
     return out
 
 
+_CUDART = None
+
+
+def _cudart():
+    """The CUDA runtime library the process already uses (PyTorch's)."""
+    global _CUDART
+    if _CUDART is None:
+        import glob
+
+        base = os.path.dirname(torch.__file__)
+        cands = sorted(glob.glob(os.path.join(base, "..", "nvidia", "cuda_runtime", "lib", "libcudart.so*")) +
+                       glob.glob(os.path.join(base, "lib", "libcudart*.so*")))
+        if not cands:
+            raise ExecutionError("libcudart not found next to torch")
+        _CUDART = ctypes.CDLL(cands[0])
+    return _CUDART
+
+
+def _destroy_streams(ptrs: list) -> None:
+    while ptrs:
+        _cudart().cudaStreamDestroy(ctypes.c_void_p(ptrs.pop()))
+
+
 class _HostStream:
     """Stand-in for a CUDA stream when the executor only COMPILES on the host
     (device "cpu": the dry-run form used by the CPU tests to check the
@@ -403,7 +426,27 @@ class Executor:
         self._create_symm()
 
     def _stream(self):
-        return _HostStream() if self.dry else torch.cuda.Stream(self.device)
+        """A CUDA stream of this executor alone (non-blocking, destroyed by
+        close): torch.cuda.Stream() hands out streams round-robin from a pool
+        of 32 per device, so two executors of one process — the in-process
+        ranks of thread_peer_groups, or an executor and a later one — could
+        be given the same cudaStream_t, and a rank's peer kernel spinning for
+        its partner would then sit in front of that partner's work."""
+        if self.dry:
+            return _HostStream()
+        ptr = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = _cudart().cudaStreamCreateWithFlags(ctypes.byref(ptr), 1)   # cudaStreamNonBlocking
+        if rc:
+            raise ExecutionError(f"cudaStreamCreateWithFlags failed ({rc})")
+        if "_own_streams" not in self.__dict__:
+            import weakref
+
+            self._own_streams = []
+            # released with the executor (cudaStreamDestroy lets queued work finish first)
+            weakref.finalize(self, _destroy_streams, self._own_streams)
+        self._own_streams.append(ptr.value)
+        return torch.cuda.ExternalStream(ptr.value, device=self.device)
 
     def _event(self):
         return _HostEvent() if self.dry else torch.cuda.Event()
@@ -2247,5 +2290,9 @@ class Executor:
             for ctx in self._symm.values():
                 check(self.lib.hap_symm_destroy(ctx), "hap_symm_destroy")
             self._symm = {}
+        if self.__dict__.get("_own_streams"):
+            self.graph = None
+            torch.cuda.synchronize(self.device)
+            _destroy_streams(self._own_streams)
         if self.group is not None:
             self.group.close()
