@@ -1413,16 +1413,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
 #ifdef HAP_GEMM_TRACE
       bool traced = false;
 #endif
+#ifdef HAP_GEMM_TRACE
+      HAP_TRACE(29);
+      bool traced_a = false, traced_b = false;
+#endif
       PairCursor<BN> cur(bt, pair, num_pairs);
       Unit x;
       while (cur.next(bt, x)) {
         const int m0 = x.m0 + 128 * static_cast<int>(rank);
         const int n0 = x.n0 + HB * static_cast<int>(rank);
         for_each_kblock(bt, x, [&](int q, int kb) {
+#ifdef HAP_GEMM_TRACE
+          HAP_TRACE_ONCE(27, traced_a);
+#endif
           HAP_TIMED(w_empty, mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1));
           const uint32_t leader_full = map_to_cta(full0 + 8 * stage, leader);
           if (rank == 0) mbar_expect_tx_cluster(leader_full, 2 * G::kStageBytes);
           else mbar_arrive_cluster(leader_full);
+#ifdef HAP_GEMM_TRACE
+          HAP_TRACE_ONCE(28, traced_b);
+#endif
           const uint32_t sa = smem_u32(smem + stage * G::kStageBytes);
           const uint32_t sb = sa + G::kABytes;
           const int k0 = kb * BK;

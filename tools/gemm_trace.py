@@ -19,7 +19,8 @@ import torch  # noqa: E402
 from paper_2401_05965_b200 import _lib  # noqa: E402
 from paper_2401_05965_b200._lib import BF16, F32, check  # noqa: E402
 
-EVENTS = {0: "entry", 1: "prologue done", 2: "first TMA issued", 3: "first MMA (stage full)",
+EVENTS = {0: "entry", 1: "prologue done", 29: "producer starts", 27: "first K block (cursor done)",
+          28: "first stage armed", 2: "first TMA issued", 3: "first MMA (stage full)",
           10: "last unit's first MMA", 9: "last TMA issued", 4: "last MMA commit", 5: "first tile in epilogue",
           11: "last tile in epilogue", 6: "last stores issued", 7: "stores complete", 8: "exit"}
 EPI_STEPS = {20: "plain boxes", 16: "plain wait staging read", 17: "plain tcgen05.ld",
