@@ -711,14 +711,21 @@ inline int p2p_grid(int64_t bytes, int sm_cap) {
 }
 
 // Every CTA of a peer-memory kernel spins on flags (peers' and the grid
-// barrier's), so the whole grid must be resident at once: launched
-// cooperatively, the driver guarantees co-residency (or fails the launch
-// loudly) even when other kernels — a persistent GEMM on another stream —
-// hold SMs.  HAP_P2P_COOP=0 launches plainly.
+// barrier's), so the whole grid must become resident.  Plain launches (the
+// default): the grid is small (p2p_grid, and the executor caps side-stream and
+// in-process peer kernels at 32 / 16 CTAs), and the only other kernels on the
+// GPU are finite (GEMMs, elementwise), so the missing CTAs become resident as
+// those finish.  HAP_P2P_COOP=1 launches cooperatively instead, which
+// guarantees co-residency up front — but measured on B200, a running
+// cooperative kernel keeps kernels of OTHER streams from being scheduled: two
+// in-process ranks deadlocked with rank 0's plain elementwise kernel queued
+// behind rank 1's spinning cooperative all-reduce (tests/multi/peer_ranks.py),
+// and in one process per GPU it would stall the compute stream while a
+// side-stream collective waits for its peers.
 int p2p_cooperative() {
   static int on = [] {
     const char* v = getenv("HAP_P2P_COOP");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 0;
   }();
   return on;
 }

@@ -170,13 +170,15 @@ def main():
     ap.add_argument("--stride", type=int, default=1, help="every k-th case only")
     ap.add_argument("--rotate", action="store_true",
                     help="one (dtype, gradient sync) combination per case, rotating through them")
+    ap.add_argument("--skip", default="", help="comma-separated dtype:sync combinations to leave out")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.verbose:
         _install_watchdog(args)
     torch.cuda.set_device(0)
     failures, count, bit_equal, bit_total = [], 0, 0, 0
-    combos = [(d, v) for d in args.dtypes.split(",") for v in args.variants.split(",")]
+    skip = {tuple(c.split(":")) for c in args.skip.split(",") if c}
+    combos = [(d, v) for d in args.dtypes.split(",") for v in args.variants.split(",") if (d, v) not in skip]
     t0 = time.time()
     for world in [int(w) for w in args.world.split(",")]:
         for ci, (name, doc, gname, inputs) in enumerate(cases(world)):
