@@ -501,8 +501,9 @@ def main() -> None:
     gemm_bytes = sum(2 * (m["M"] * m["K"] + m["K"] * m["N"]) + m["M"] * m["N"] * (2 if m["out_dt"] else 4)
                      * (2 if m["accumulate"] else 1) for m in members)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"r01h_gemm_traffic_{args.workload}.json")
-    if n == 1 and os.path.exists(prof):
+    prof = next((q for q in (os.path.join(ROOT, "profiles", f"r{r}_gemm_traffic_{args.workload}.json")
+                             for r in ("02", "01h")) if os.path.exists(q)), "")
+    if n == 1 and prof:
         with open(prof) as fh:
             tr = json.load(fh)
         traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]

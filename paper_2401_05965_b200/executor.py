@@ -247,9 +247,24 @@ def _cudart():
     return _CUDART
 
 
-def _destroy_streams(ptrs: list) -> None:
+_FREE_STREAMS: dict = {}   # device index -> streams no live executor holds
+
+
+def _acquire_stream(dev: int) -> int:
+    free = _FREE_STREAMS.setdefault(dev, [])
+    if free:
+        return free.pop()
+    ptr = ctypes.c_void_p()
+    with torch.cuda.device(dev):
+        rc = _cudart().cudaStreamCreateWithFlags(ctypes.byref(ptr), 1)   # cudaStreamNonBlocking
+    if rc:
+        raise ExecutionError(f"cudaStreamCreateWithFlags failed ({rc})")
+    return ptr.value
+
+
+def _release_streams(dev: int, ptrs: list) -> None:
     while ptrs:
-        _cudart().cudaStreamDestroy(ctypes.c_void_p(ptrs.pop()))
+        _FREE_STREAMS.setdefault(dev, []).append(ptrs.pop())
 
 
 class _HostStream:
@@ -426,27 +441,25 @@ class Executor:
         self._create_symm()
 
     def _stream(self):
-        """A CUDA stream of this executor alone (non-blocking, destroyed by
-        close): torch.cuda.Stream() hands out streams round-robin from a pool
-        of 32 per device, so two executors of one process — the in-process
-        ranks of thread_peer_groups, or an executor and a later one — could
-        be given the same cudaStream_t, and a rank's peer kernel spinning for
-        its partner would then sit in front of that partner's work."""
+        """A CUDA stream no other live executor uses (non-blocking): torch's
+        torch.cuda.Stream() hands out streams round-robin from a pool of 32 per
+        device, so two executors of one process — the in-process ranks of
+        thread_peer_groups — could be given the same cudaStream_t, and a rank's
+        peer kernel spinning for its partner would then sit in front of that
+        partner's work.  Streams come from a process-wide free list, go back to
+        it when the executor is closed or collected, and are never destroyed
+        (torch may still record events on them for tensors they touched)."""
         if self.dry:
             return _HostStream()
-        ptr = ctypes.c_void_p()
-        with torch.cuda.device(self.device):
-            rc = _cudart().cudaStreamCreateWithFlags(ctypes.byref(ptr), 1)   # cudaStreamNonBlocking
-        if rc:
-            raise ExecutionError(f"cudaStreamCreateWithFlags failed ({rc})")
+        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
         if "_own_streams" not in self.__dict__:
             import weakref
 
             self._own_streams = []
-            # released with the executor (cudaStreamDestroy lets queued work finish first)
-            weakref.finalize(self, _destroy_streams, self._own_streams)
-        self._own_streams.append(ptr.value)
-        return torch.cuda.ExternalStream(ptr.value, device=self.device)
+            weakref.finalize(self, _release_streams, dev, self._own_streams)
+        ptr = _acquire_stream(dev)
+        self._own_streams.append(ptr)
+        return torch.cuda.ExternalStream(ptr, device=self.device)
 
     def _event(self):
         return _HostEvent() if self.dry else torch.cuda.Event()
@@ -656,6 +669,23 @@ class Executor:
         in_dt = BF16 if (a.dtype == BF16 and b.dtype == BF16) else F32
         a = self._as(a, in_dt, cap)
         b = self._as(b, in_dt, cap)
+        c_out = None
+        if in_dt == BF16 and not self.dry and (self._misaligned(a) or self._misaligned(b) or self._misaligned(c)):
+            # uneven shards of a bf16 dimension (e.g. the ViT-MoE expert slices
+            # 1804 / 1268 of 3072 columns) leave rows that are not 16-byte
+            # pitched, which TMA cannot describe: stage misaligned operands
+            # into padded copies and compute a misaligned C into a padded
+            # buffer copied back, so the GEMM stays on the tcgen05 path
+            if self._misaligned(a):
+                a = self._pitched(a, True, cap)
+            if self._misaligned(b):
+                b = self._pitched(b, True, cap)
+            if self._misaligned(c):
+                rows, cols = c.shape
+                c_out, c = c, self._pitched(c, bool(accumulate), cap)
+                if addend is not None:   # C = A.B + addend: stage the addend and accumulate onto it
+                    self._block(addend, (rows, cols, 1), 0, c, (rows, c.shape[1], 1), 0, cols, cap)
+                    accumulate, addend = 1, None
         g = dict(A=a.ptr, lda=a.shape[1], transA=int(trans_a), B=b.ptr, ldb=b.shape[1],
                  transB=int(trans_b), C=c.ptr, ldc=c.shape[1], M=am, N=bn, K=ak,
                  accumulate=accumulate, in_dt=in_dt, out_dt=c.dtype, cap=cap,
@@ -667,6 +697,25 @@ class Executor:
         self._ops.append(Op(self.lib.hap_matmul_batch, (desc, 1, 0, in_dt, c.dtype, cap, self._sptr()),
                             "hap_matmul", True, g))
         self._sync_desc(self._ops[-1])
+        if c_out is not None:
+            rows, cols = c_out.shape
+            self._block(c, (rows, c.shape[1], 1), 0, c_out, (rows, cols, 1), 0, cols, cap)
+
+    @staticmethod
+    def _misaligned(buf: Buf) -> bool:
+        """Rows not 16-byte pitched: TMA cannot describe the matrix, and the
+        GEMM would fall back to the CUDA-core kernel."""
+        return len(buf.shape) == 2 and (buf.shape[1] * (2 if buf.dtype == BF16 else 4)) % 16 != 0
+
+    def _pitched(self, buf: Buf, copy_in: bool, cap: int) -> Buf:
+        """A copy of ``buf`` with its rows padded to a 16-byte pitch (the pad
+        columns are never read: the GEMM's extents are the logical ones)."""
+        rows, cols = buf.shape
+        per = 8 if buf.dtype == BF16 else 4
+        pad = self._new((rows, -(-cols // per) * per), buf.dtype)
+        if copy_in:
+            self._block(buf, (rows, cols, 1), 0, pad, (rows, pad.shape[1], 1), 0, cols, cap)
+        return pad
 
     @staticmethod
     def _fill_desc(d, g: dict):
@@ -2293,6 +2342,7 @@ class Executor:
         if self.__dict__.get("_own_streams"):
             self.graph = None
             torch.cuda.synchronize(self.device)
-            _destroy_streams(self._own_streams)
+            dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+            _release_streams(dev, self._own_streams)
         if self.group is not None:
             self.group.close()

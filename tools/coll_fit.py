@@ -170,7 +170,12 @@ def bench(args):
         }
         ref = None
         for name, fn in impls.items():
+            # cleared and visible on every rank before any rank's kernel may
+            # push into it (the zeroing runs on another stream than the call)
+            torch.cuda.synchronize(dev)
             a2a_recv.zero_()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
             check(fn(), name)
             torch.cuda.synchronize(dev)
             if ref is None:

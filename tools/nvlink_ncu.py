@@ -52,6 +52,42 @@ def _nvlink_kib(index: int) -> tuple[int, int]:
     return tx, rx
 
 
+class _Gpm:
+    """NVLink RX / TX of one GPU between two GPM samples (NVML GPU
+    Performance Monitoring: NVLINK_TOTAL_RX/TX_PER_SEC, MiB/s averaged over the
+    interval between the samples, all links)."""
+
+    def __init__(self, index: int):
+        import pynvml as nv
+
+        nv.nvmlInit()
+        self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+        self.ok = bool(nv.nvmlGpmQueryDeviceSupport(self.h).isSupportedDevice)
+        self.s1, self.s2 = nv.nvmlGpmSampleAlloc(), nv.nvmlGpmSampleAlloc()
+
+    def start(self):
+        import time
+
+        self.nv.nvmlGpmSampleGet(self.h, self.s1)
+        self.t0 = time.perf_counter()
+
+    def stop(self) -> tuple[float, float]:
+        """(tx, rx) bytes moved over NVLink since start()."""
+        import time
+
+        self.nv.nvmlGpmSampleGet(self.h, self.s2)
+        dt = time.perf_counter() - self.t0
+        nv = self.nv
+        mg = nv.c_nvmlGpmMetricsGet_t()
+        mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+        mg.numMetrics = 2
+        mg.sample1, mg.sample2 = self.s1, self.s2
+        mg.metrics[0].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_TX_PER_SEC
+        mg.metrics[1].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_RX_PER_SEC
+        nv.nvmlGpmMetricsGet(mg)
+        return mg.metrics[0].value * (1 << 20) * dt, mg.metrics[1].value * (1 << 20) * dt
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -87,6 +123,14 @@ def main():
     check(L.hap_symm_open(ctx, b"".join(handles)))
     stream = torch.cuda.current_stream(dev).cuda_stream
     report = []
+    gpm = None
+    if args.nvml:
+        try:
+            gpm = _Gpm(local)
+            if not gpm.ok:
+                gpm = None
+        except Exception as exc:  # noqa: BLE001 - fall back to the field counters
+            print(f"[rank {rank}] GPM unavailable: {exc}", flush=True)
     for rows in [int(v) for v in args.rows.split(",")]:
         sizes = round_shards(rows, ratios)
         offs = offsets(sizes)
@@ -134,17 +178,22 @@ def main():
                 torch.cuda.synchronize(dev)
                 dist.barrier()
                 c0 = _nvlink_kib(local)
+                if gpm is not None:
+                    gpm.start()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 for _ in range(args.reps):
                     check(fn(), name)
                 e1.record()
                 torch.cuda.synchronize(dev)
+                g_tx, g_rx = gpm.stop() if gpm is not None else (0.0, 0.0)
                 c1 = _nvlink_kib(local)
                 ms = torch.tensor([e0.elapsed_time(e1) / args.reps], device=dev)
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
                 t = float(ms) * 1e-3
                 ctx_b = (c1[0] - c0[0]) * 1024 / args.reps, (c1[1] - c0[1]) * 1024 / args.reps
+                if ctx_b == (0, 0) and (g_tx or g_rx):   # field counters not reported: GPM rates x interval
+                    ctx_b = g_tx / args.reps, g_rx / args.reps
                 report.append({"rank": rank, "op": name, "rows": rows, "rx_bytes": rx, "tx_bytes": tx,
                                "us_per_call_max_over_ranks": round(t * 1e6, 2),
                                "nvlink_tx_bytes_counted": ctx_b[0], "nvlink_rx_bytes_counted": ctx_b[1],
