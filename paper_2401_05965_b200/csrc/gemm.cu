@@ -524,6 +524,20 @@ struct alignas(64) TcBatch {
   int64_t fin_ldr[kMaxProblems], fin_ldy[kMaxProblems];
 };
 
+// Touch every 64-byte line of the launch parameters from one idle warp while
+// the prologue runs: the unit decode of the producer, MMA and epilogue
+// cursors reads TcBatch fields with dynamic indices (constant-cache loads),
+// and their first, serialised misses otherwise sit between the prologue and
+// the first TMA load (~0.6-1 us per launch, tools/gemm_trace.py).
+__device__ __forceinline__ void warm_params(const TcBatch& bt, int lane) {
+  const int* w = reinterpret_cast<const int*>(&bt);
+  constexpr int kLines = (static_cast<int>(sizeof(TcBatch)) + 63) / 64;
+  int acc = 0;
+#pragma unroll
+  for (int i = lane; i < kLines; i += 32) acc += w[i * 16];
+  asm volatile("" ::"r"(acc));
+}
+
 __device__ __forceinline__ float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
 // 8 consecutive fp32 accumulator columns of this warp's 32 TMEM lanes.
@@ -1122,6 +1136,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       tma_prefetch(&bt.p[q].b);
     }
   }
+  if (warp == 3) warm_params(bt, lane);
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -1379,6 +1394,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2_kernel(const __grid_cons
       tma_prefetch(&bt.p[q].b);
     }
   }
+  if (warp == 3) warm_params(bt, lane);
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(full0 + 8 * s, 2);   // one producer arrival per CTA (+ both CTAs' bytes)

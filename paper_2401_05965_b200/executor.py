@@ -670,7 +670,7 @@ class Executor:
         a = self._as(a, in_dt, cap)
         b = self._as(b, in_dt, cap)
         c_out = None
-        if in_dt == BF16 and not self.dry and (self._misaligned(a) or self._misaligned(b) or self._misaligned(c)):
+        if in_dt == BF16 and (self._misaligned(a) or self._misaligned(b) or self._misaligned(c)):
             # uneven shards of a bf16 dimension (e.g. the ViT-MoE expert slices
             # 1804 / 1268 of 3072 columns) leave rows that are not 16-byte
             # pitched, which TMA cannot describe: stage misaligned operands

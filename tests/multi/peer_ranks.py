@@ -200,7 +200,9 @@ def main():
                 except Exception as exc:  # noqa: BLE001 - fatal: a peer kernel may be left spinning
                     # one rank failed to enqueue its step: the other rank's peer kernel now waits for a
                     # partner that never comes, so no later GPU call can return — report and stop
-                    print(f"  FAIL {label}: {type(exc).__name__}: {exc}", flush=True)
+                    import traceback
+
+                    print(f"  FAIL {label}: {type(exc).__name__}: {exc}\n{traceback.format_exc()}", flush=True)
                     for f in failures[:40]:
                         print("  FAIL", f, flush=True)
                     os._exit(2)
