@@ -60,7 +60,20 @@ struct Symm {
 
 struct Peers {
   char* base[kMaxRanks];
+  // HAP_P2P_NOSYNC=1 (measurement only, results undefined): skip the waits
+  // on peers' flags, so each kernel moves its NVLink bytes alone — what an
+  // ncu capture of the NVLink counters needs, since ncu serialises kernels
+  // and a kernel waiting for its partner would never finish under it
+  int nosync;
 };
+
+int p2p_nosync() {
+  static int on = [] {
+    const char* v = getenv("HAP_P2P_NOSYNC");
+    return v ? atoi(v) : 0;
+  }();
+  return on;
+}
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
@@ -163,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_gather_kernel(Peers peers, i
   const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
   // 1. peers have finished reading my staging buffer from the previous call
   if (threadIdx.x < nranks && threadIdx.x != rank)
-    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
   __syncthreads();
   // 2. publish my shard
   const int64_t mine = outer * sizes[rank] * inner;
@@ -178,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_gather_kernel(Peers peers, i
   }
   // 3. pull every chunk into place
   if (threadIdx.x < nranks && threadIdx.x != rank)
-    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   for (int q = 0; q < nranks; ++q) {
     const int p = (rank + q) % nranks;  // stagger sources across ranks
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_gather_push_kernel(Peers pee
   if (blockIdx.x == 0 && peer_thread)
     st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
   if (peer_thread)
-    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   for (int q = 1; q <= nranks; ++q) {
     const int p = (rank + q) % nranks;   // peers staggered across ranks, own output last (local HBM)
@@ -244,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_gather_push_kernel(Peers pee
     sig->epoch = epoch + 1;
   }
   if (peer_thread)
-    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
 }
 
 // Reduce-scatter: rank r stages its whole partial tensor [outer, extent,
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_kernel(Peers peer
   T* staging = reinterpret_cast<T*>(peers.base[rank] + kSignalBytes);
   const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(&sig->epoch);
   if (threadIdx.x < nranks && threadIdx.x != rank)
-    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch) __nanosleep(128);
   __syncthreads();
   copy_elems(staging, send, outer * extent * inner);
   if (grid_barrier(sig) && threadIdx.x == 0) {
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_kernel(Peers peer
     }
   }
   if (threadIdx.x < nranks && threadIdx.x != rank)
-    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   const int64_t rows = sizes[rank], off = offs[rank];
   const int64_t per = rows * inner, total = outer * per;
@@ -386,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
   if (blockIdx.x == 0 && peer_thread)
     st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->ready[rank], epoch + 1);
   if (peer_thread)
-    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   const int64_t rows = sizes[rank], off = offs[rank];
   const int64_t per = rows * inner, total = outer * per;
@@ -438,7 +451,7 @@ __global__ void __launch_bounds__(kThreads) p2p_reduce_scatter_direct_kernel(
     sig->epoch = epoch + 1;
   }
   if (peer_thread)
-    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
 }
 
 
@@ -464,7 +477,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_reduce_kernel(Peers peers, i
   if (blockIdx.x == 0 && peer_thread)
     st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
   if (peer_thread)
-    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   constexpr int kv = 16 / sizeof(T);
   const int64_t groups = count / 8;                     // whole 8-element groups, split into chunks
@@ -520,7 +533,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_reduce_kernel(Peers peers, i
     sig->epoch = epoch + 1;
   }
   if (peer_thread)
-    while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->done[threadIdx.x]) < epoch + 1) __nanosleep(64);
 }
 
 // All-to-all by pushing contiguous chunks: rank r stores chunk k of its send
@@ -542,7 +555,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_to_all_kernel(Peers peers, i
   if (blockIdx.x == 0 && peer_thread)
     st_release_sys(&reinterpret_cast<SignalPage*>(peers.base[threadIdx.x])->armed[rank], epoch + 1);
   if (peer_thread)
-    while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->armed[threadIdx.x]) < epoch + 1) __nanosleep(64);
   __syncthreads();
   for (int q = 1; q <= nranks; ++q) {
     const int k = (rank + q) % nranks;   // peers staggered across ranks, own chunk last
@@ -559,7 +572,7 @@ __global__ void __launch_bounds__(kThreads) p2p_all_to_all_kernel(Peers peers, i
     sig->epoch = epoch + 1;
   }
   if (peer_thread)
-    while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
+    if (!peers.nosync) while (ld_acquire_sys(&sig->ready[threadIdx.x]) < epoch + 1) __nanosleep(64);
 }
 
 }  // namespace
@@ -573,6 +586,7 @@ extern "C" hap_status hap_p2p_probe(void* ctx, int mode, int64_t chunk_bytes, in
                     chunk_bytes * s->nranks <= hap_symm_capacity(ctx),
                 "hap_p2p_probe: bad arguments");
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   const int grid = capped_grid(static_cast<int64_t>(sm_count()), sm_cap);
   launch_k(p2p_probe_kernel, dim3(grid), dim3(kThreads), 0, static_cast<cudaStream_t>(stream), peers, s->rank,
@@ -754,6 +768,7 @@ hap_status p2p_launch(void (*kern)(Peers, int, int, const T*, T*, int64_t, int64
                       const int64_t* dev_sizes, const int64_t* dev_offs, int64_t bytes, int sm_cap,
                       cudaStream_t stream) {
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   const int grid = p2p_grid(bytes, sm_cap);   // every CTA resident (they spin on peer flags)
   launch_p2p(kern, grid, stream, peers, s->rank, s->nranks, static_cast<const T*>(send), static_cast<T*>(out), outer,
@@ -787,6 +802,7 @@ extern "C" hap_status hap_p2p_all_gather_push(void* ctx, const void* send, void*
   auto* s = static_cast<Symm*>(ctx);
   HAP_CHECK_ARG(s && dev_outs && dev_sizes && dev_offsets, "hap_p2p_all_gather_push: bad arguments");
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   // every CTA spins on peer flags: all resident, one per (capped) SM at most
   const int grid = p2p_grid(total_elems * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
@@ -808,6 +824,7 @@ extern "C" hap_status hap_p2p_reduce_scatter_direct(void* ctx, const void* const
   auto* s = static_cast<Symm*>(ctx);
   HAP_CHECK_ARG(s && dev_sends && recv && dev_sizes && dev_offsets, "hap_p2p_reduce_scatter_direct: bad arguments");
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   const int grid = p2p_grid(recv_elems * s->nranks * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
   auto st = static_cast<cudaStream_t>(stream);
@@ -875,6 +892,7 @@ extern "C" hap_status hap_p2p_all_reduce(void* ctx, const void* const* dev_ins, 
   auto* s = static_cast<Symm*>(ctx);
   HAP_CHECK_ARG(s && dev_ins && dev_outs && count >= 0, "hap_p2p_all_reduce: bad arguments");
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   // bytes this rank moves: its chunk from every peer and to every peer
   const int grid = p2p_grid(2 * count * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
@@ -895,6 +913,7 @@ extern "C" hap_status hap_p2p_all_to_all(void* ctx, const void* send, void* cons
   auto* s = static_cast<Symm*>(ctx);
   HAP_CHECK_ARG(s && dev_recvs && dev_send_off && dev_counts && dev_dst_off, "hap_p2p_all_to_all: bad arguments");
   Peers peers{};
+  peers.nosync = p2p_nosync();
   for (int p = 0; p < s->nranks; ++p) peers.base[p] = s->peers[p];
   const int grid = p2p_grid(max_elems * static_cast<int64_t>(dtype_size(dtype)), sm_cap);
   auto st = static_cast<cudaStream_t>(stream);

@@ -18,6 +18,14 @@ python tools/coll_fit.py --fit $OUT/coll_fit.json >> $OUT/coll_fit.log 2>&1; cp 
 trun 300 tools/nvlink_ncu.py --nvml --rows 16384,65536,262144 --json $OUT/nvl_counters.json > $OUT/nvl_counters.log 2>&1; echo "nvl_counters rc=$?" >> $OUT/status.txt
 HAP_P2P_COOP=1 trun 900 bench.py --gpus $N --steps $STEPS --warmup 5 --workload moe --grad-sync sfb > $OUT/bench_workload_moe_gradsync_sfb_coop.json 2> $OUT/bench_coop.err
 echo "bench moe sfb (cooperative peer launches) rc=$?" >> $OUT/status.txt
+# NVLink counters under ncu: the peer kernels with their cross-rank flag waits
+# disabled (HAP_P2P_NOSYNC=1, results undefined), so ncu's kernel serialisation
+# cannot deadlock them; only p2p_* kernels are profiled
+port=$((port + 1))
+HAP_P2P_NOSYNC=1 timeout 900 ncu --target-processes all -k regex:p2p_ --clock-control none --csv \
+  --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvltx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum \
+  --log-file $OUT/nvl_ncu.csv python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+  --master-port $port tools/nvlink_ncu.py --calls 2 --rows 65536,262144 > $OUT/nvl_ncu.log 2>&1; echo "nvl_ncu rc=$?" >> $OUT/status.txt
 for args in "--workload bert" "--workload moe" "--workload moe --grad-sync sfb" "--workload moe --grad-sync all_reduce" \
             "--workload vitmoe" "--workload vitmoe --collectives p2p" "--workload vitmoe --collectives nccl"; do
   tag=$(echo $args | tr -d '-' | tr ' ' '_')

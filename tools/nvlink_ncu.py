@@ -179,7 +179,11 @@ def main():
                 dist.barrier()
                 c0 = _nvlink_kib(local)
                 if gpm is not None:
-                    gpm.start()
+                    try:
+                        gpm.start()
+                    except Exception as exc:  # noqa: BLE001 - GPM sampling refused on this box
+                        print(f"[rank {rank}] GPM sampling failed ({exc}); NVML field counters only", flush=True)
+                        gpm = None
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 for _ in range(args.reps):
