@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--rotate", action="store_true",
                     help="one (dtype, gradient sync) combination per case, rotating through them")
     ap.add_argument("--skip", default="", help="comma-separated dtype:sync combinations to leave out")
+    ap.add_argument("--start-run", type=int, default=1, help="skip the runs before this one (resume)")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.verbose:
@@ -191,6 +192,8 @@ def main():
             program, _, _ = O.load_plan(doc)
             for dtype, sync in ([combos[(ci // args.stride) % len(combos)]] if args.rotate else combos):
                 count += 1
+                if count < args.start_run:
+                    continue
                 label = f"{name} {dtype} {sync}"
                 capture = args.capture_every > 0 and count % args.capture_every == 0
                 if args.verbose:
@@ -219,6 +222,7 @@ def main():
                     lex.close()
                 for ex in exs:
                     ex.close()
+                print(f"DONE {count}", flush=True)
     print(f"peer ranks parity: {count} runs, {len(failures)} failures; fp32 bit-identical to LocalGroup "
           f"in {bit_equal}/{bit_total}; {time.time() - t0:.0f} s")
     for f in failures[:40]:
