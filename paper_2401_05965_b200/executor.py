@@ -960,7 +960,8 @@ class Executor:
             return use
         from .cost_model import comm_time
 
-        row = tuple(self.cfg.ratios) if self.cfg.ratios else tuple(c / sum(self.caps) for c in self.caps)
+        caps = [c or 148 for c in self.caps]   # no cap: the whole GPU
+        row = tuple(self.cfg.ratios) if self.cfg.ratios else tuple(c / sum(caps) for c in caps)
         ins = Instruction("all_gather" if kind == "grouped_broadcast" else kind, "t", elements=int(elements))
         t_p2p, t_nccl = comm_time(ins, row, specs["p2p"]), comm_time(ins, row, specs["nccl"])
         use = t_p2p <= t_nccl

@@ -372,19 +372,20 @@ _FITS: dict | None = None
 
 
 def collective_fits(world: int) -> dict | None:
-    """{kind: {impl: (latency_s, bw_Bps)}} measured at ``world`` GPUs — or at
-    the nearest measured world size below it (the lines barely move with
-    the rank count on NVSwitch) — or None when nothing was measured."""
+    """{kind: {impl: (latency_s, bw_Bps)}} measured at exactly ``world``
+    GPUs, or None (the hand-set round-1 lines are used then): a line fitted
+    at one rank count does not transfer — with the 4-GPU lines applied to 2
+    GPUs the model picked all-reduce for BERT-MoE, which measured 29 % slower
+    than SFB there (profiles/r02_multi_n2.md)."""
     global _FITS
     if _FITS is None:
         _FITS = {}
         if os.path.exists(FITS_PATH):
             with open(FITS_PATH) as fh:
                 _FITS = {int(k): v for k, v in json.load(fh).items()}
-    worlds = sorted(w for w in _FITS if w <= world) or sorted(_FITS)
-    if not worlds or world < 2:
+    if world < 2 or world not in _FITS:
         return None
-    doc = _FITS[worlds[-1]]
+    doc = _FITS[world]
     return {kind: {impl: (v["latency_s"], v["bw_Bps"]) for impl, v in impls.items()} for kind, impls in doc.items()}
 
 
