@@ -210,10 +210,14 @@ def fit(paths, out):
     from paper_2401_05965_b200.cost_model import fit_linear
 
     model = {}
+    if os.path.exists(out):   # keep the other world sizes' lines
+        with open(out) as fh:
+            model = json.load(fh)
     for path in paths:
         with open(path) as fh:
             doc = json.load(fh)
         world = str(doc["world"])
+        model[world] = {}
         for op in OPS:
             for impl in ("p2p", "nccl"):
                 samples = [(r["bytes"], r["s"]) for r in doc["results"]
