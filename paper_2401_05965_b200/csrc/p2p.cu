@@ -27,6 +27,7 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -54,7 +55,12 @@ struct Symm {
   size_t bytes = 0;
   char* local = nullptr;                 // arena base (signal page + staging)
   char* peers[kMaxRanks] = {};           // peer arena bases (IPC-mapped), peers[rank] = local
-  std::map<std::pair<int, uint64_t>, char*> opened;   // (peer, its allocation base) -> mapped here
+  // (peer, IPC handle of its allocation) -> mapped here.  Keyed by the handle,
+  // not the allocation's base address: a peer may free an allocation and get
+  // a new one at the same address, and a mapping cached by address would
+  // then point at the old memory (pushes silently lost — seen in
+  // tools/coll_fit.py's all-to-all check at 2 GPUs)
+  std::map<std::pair<int, std::string>, char*> opened;
   bool local_open = false;               // peers are arenas of this process (hap_symm_open_local)
 };
 
@@ -694,7 +700,8 @@ extern "C" hap_status hap_p2p_buffer_open(void* ctx, const void* own, const uint
       out_ptrs[p] = const_cast<void*>(own);
       continue;
     }
-    const auto key = std::make_pair(p, static_cast<uint64_t>(base_addrs[p]));
+    (void)base_addrs;
+    const auto key = std::make_pair(p, std::string(reinterpret_cast<const char*>(handles64xn + 64 * p), 64));
     auto it = s->opened.find(key);
     if (it == s->opened.end()) {
       cudaIpcMemHandle_t h;

@@ -195,7 +195,7 @@ def bench(args):
             results.append({"op": "all_to_all", "impl": name, "rows": rows, "bytes": total_b16,
                             "s": timed(fn, f"all_to_all {name}")})
         if rank == 0:
-            line = "  ".join(f"{r['op']}/{r['impl']} {r['s'] * 1e6:8.1f}us" for r in results[-8:])
+            line = "  ".join(f"{r['op']}/{r['impl']} {r['s'] * 1e6:8.1f}us" for r in results[-8:] if "s" in r)
             print(f"rows {rows:7d} ({total_b16 / 1e6:8.3f} MB): {line}", flush=True)
     if rank == 0 and args.json:
         with open(args.json, "w") as fh:
