@@ -45,7 +45,8 @@ constexpr int kEpiWarps = 8;
 // per epilogue warp, where the warp transposes its row-per-lane accumulator
 // values into full-line coalesced global stores (box_out).  The other 190 KB
 // or so go to the operand pipeline.
-constexpr int kEpiBoxBytes = 4096;
+constexpr int kEpiBoxBytes = 4096;        // plain epilogues
+constexpr int kEpiBoxBytesFused = 8192;   // fused epilogues (drain_fused's slots)
 constexpr int kSmemLimit = 232448;        // 227 KB per CTA
 constexpr int kMaxStages = 8;             // barrier slots reserved
 // operand stages that fit beside the epilogue boxes, the barriers and the
@@ -485,20 +486,14 @@ struct alignas(64) TcProblem {
   //   SWISH: e1 = Y, e2 = Z (out)   SWISH_BWD: e1 = R = x, e2 = R2 = f(x) (in)
   int epi, epi_tag;
   CUtensorMap e1, e2;
-  // the fused epilogue's tensors as pointers / row pitches (elements):
-  // in1 = R (ADD, ADD2) or x (SWISH_BWD), in2 = f(x) (SWISH_BWD);
-  // out2 = Y (ADD2, SWISH), out3 = Z (SWISH)
-  const void* in1;
-  const void* in2;
-  void* out2;
-  void* out3;
-  int64_t ld_in1, ld_in2, ld_out2, ld_out3;
 };
 
 struct alignas(64) TcBatch {
   TcProblem p[kMaxProblems];
   // shared-memory layout of this launch: nst operand stages, then one
-  // epilogue box of box_bytes (4 KB) per epilogue warp, then the barriers
+  // epilogue box of box_bytes per epilogue warp (4 KB; 8 KB when a fused
+  // epilogue stages its TMA-loaded inputs and three-output chunks), then the
+  // barriers — a plain launch turns the spare 32 KB into pipeline depth
   int nst, box_bytes;
   int count;
   int sum_k;
@@ -579,187 +574,214 @@ __device__ __forceinline__ void sts_bf16x8(uint32_t at, const float (&v)[8]) {
 
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
-// ---- fused epilogues through the warp's box (hap_gemm_desc.epi, bf16 C)
-// The accumulator chunk is staged like a plain epilogue (row per lane,
-// swizzled) — as fp32 for ADD (C = bf16(acc + R) needs the unrounded sum),
-// as bf16(acc) otherwise (every other op starts from the rounded C) — and
-// the elementwise op runs in the coalesced copy-out: a lane takes one
-// 16-byte chunk of one row, loads the matching chunk of each input with the
-// same full-line pattern, and stores every output chunk the same way.
-// Rounding follows the unfused kernels (elementwise.cu binary / swish_fwd /
-// swish_bwd), two values per F2FP pack.
-__device__ __forceinline__ uint32_t round2_pack(float& a, float& b) {
+// Fused epilogues (hap_gemm_desc.epi, bf16 outputs).  The warp drains its
+// 32 rows x BN/2 columns in chunks of 32 columns (one tcgen05.ld each); every
+// tensor a chunk touches — outputs (C, Y, Z) and inputs (R, x, f(x)) — is a
+// 32 x 32 bf16 box (64-byte rows, SWIZZLE_64B) in the warp's 8 KB staging area
+// (4 slots of 2 KB).  Inputs are TMA-loaded into the slot their output will
+// occupy and overwritten in place; outputs leave by TMA store, one bulk group
+// per chunk.  Ops with <= 2 slots per chunk double-buffer: the next chunk's
+// inputs are loaded into the other slot pair while this chunk computes.
+// Rounding follows the unfused kernels: C is rounded to bf16 first and the
+// elementwise results are computed from the rounded value (elementwise.cu
+// swish_fwd / binary / swish_bwd).
+constexpr int kFusedW = 32;                  // columns per fused box
+constexpr int kFusedBox = 32 * kFusedW * 2;  // bytes per fused box
+
+// bf16 rounding of two fp32 values at once: one F2FP pack (ALU pipe) and two
+// shifts, the same round-to-nearest-even as __float2bfloat16_rn per value
+// (F2F, a quarter-rate XU-pipe op that MUFU shares — with two of them per
+// element and the sigmoid's two MUFU ops, the swish epilogue was XU-bound).
+// Returns the packed pair (low = a) and replaces a, b by their rounded values.
+__device__ __forceinline__ uint32_t round2_bf16(float& a, float& b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
   a = __uint_as_float(u << 16);
   b = __uint_as_float(u & 0xffff0000u);
   return u;
 }
-__device__ __forceinline__ float lo_bf16(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float hi_bf16(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
-// 8 bf16 at p (16 bytes when whole and aligned, else element by element, zeros past `valid`)
-__device__ __forceinline__ uint4 ld_bf16x8(const __nv_bfloat16* p, int valid, bool vec) {
-  if (vec && valid == 8) return *reinterpret_cast<const uint4*>(p);
-  uint32_t q[4] = {0u, 0u, 0u, 0u};
-  for (int e = 0; e < valid; ++e) {
-    const uint32_t h = *reinterpret_cast<const unsigned short*>(p + e);
-    q[e / 2] |= (e & 1) ? (h << 16) : h;
-  }
-  return make_uint4(q[0], q[1], q[2], q[3]);
-}
-__device__ __forceinline__ void st_bf16x8(__nv_bfloat16* p, uint4 v, int valid, bool vec) {
-  if (vec && valid == 8) {
-    *reinterpret_cast<uint4*>(p) = v;
-    return;
-  }
-  const uint32_t q[4] = {v.x, v.y, v.z, v.w};
-  for (int e = 0; e < valid; ++e)
-    *reinterpret_cast<unsigned short*>(p + e) = static_cast<unsigned short>((e & 1) ? (q[e / 2] >> 16) : q[e / 2]);
+__device__ __forceinline__ void sts_u32x4(uint32_t at, const uint32_t (&p)[4]) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(at), "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]));
 }
 
-// ADD: fp32 staged box (32 columns, 128-byte rows); C = bf16(acc + R).
-__device__ __forceinline__ void box_out_add(uint32_t box, int lane, const TcProblem& pr, int row0, int col0) {
-  constexpr int CPR = 8, RPP = 4;   // 16-byte chunks per row, rows per pass
+// The elementwise op of one 32-column chunk: r = accumulator columns of the
+// lane's row; s0..s2 = the chunk's staging slots (inputs in place, outputs).
+// Values are rounded to bf16 exactly where the unfused kernels store them,
+// two at a time (round2_bf16).
+template <int EPI, int TAG>
+__device__ __forceinline__ void fused_chunk(const uint32_t (&r)[32], int lane, uint32_t s0, uint32_t s1,
+                                            uint32_t s2) {
 #pragma unroll
-  for (int it = 0; it < CPR; ++it) {
-    const int r = it * RPP + lane / CPR, c = lane % CPR;
-    float v[4];
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-                 : "r"(box + swz_offset<128>(r, c)));
-    const int row = row0 + r, col = col0 + c * 4;
-    if (row >= pr.M || col >= pr.N) continue;
-    const int valid = pr.N - col < 4 ? pr.N - col : 4;
-    const __nv_bfloat16* rp = static_cast<const __nv_bfloat16*>(pr.in1) + static_cast<int64_t>(row) * pr.ld_in1 + col;
-    __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(pr.C) + static_cast<int64_t>(row) * pr.ldc + col;
-    if (valid == 4) {
-      const uint2 q = *reinterpret_cast<const uint2*>(rp);
-      float a = v[0] + lo_bf16(q.x), b = v[1] + hi_bf16(q.x), c2 = v[2] + lo_bf16(q.y), d = v[3] + hi_bf16(q.y);
-      *reinterpret_cast<uint2*>(cp) = make_uint2(round2_pack(a, b), round2_pack(c2, d));
-    } else {
-      for (int e = 0; e < valid; ++e) cp[e] = __float2bfloat16_rn(v[e] + __bfloat162float(rp[e]));
-    }
-  }
-}
-
-// ADD2 / SWISH / SWISH_BWD: bf16(acc) staged box of kRowBytes rows.
-template <int EPI, int kRowBytes>
-__device__ __forceinline__ void box_out_fused(uint32_t box, int lane, const TcProblem& pr, int row0, int col0) {
-  const int tag = pr.epi_tag;   // uniform across the launch: a well-predicted branch per element
-  constexpr int CPR = kRowBytes / 16, RPP = 32 / CPR;
+  for (int j = 0; j < 4; ++j) {   // 8 columns: 16-byte chunk j of the lane's 64-byte row
+    const uint32_t off = swz_offset<64>(lane, j);
+    float c[8], x[8], y[8];
+    uint32_t p0[4], p1[4], p2[4];
 #pragma unroll
-  for (int it = 0; it < CPR; ++it) {
-    const int r = it * RPP + lane / CPR, c = lane % CPR;
-    uint32_t q[4];
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3])
-                 : "r"(box + swz_offset<kRowBytes>(r, c)));
-    const int row = row0 + r, col = col0 + c * 8;
-    if (row >= pr.M || col >= pr.N) continue;
-    const int valid = pr.N - col < 8 ? pr.N - col : 8;
-    const int64_t rr = static_cast<int64_t>(row);
-    __nv_bfloat16* cp = static_cast<__nv_bfloat16*>(pr.C) + rr * pr.ldc + col;
-    if constexpr (EPI == EPI_OP_ADD2) {   // C = bf16(acc); Y = bf16(C + R)
-      const uint4 x = ld_bf16x8(static_cast<const __nv_bfloat16*>(pr.in1) + rr * pr.ld_in1 + col, valid, true);
-      const uint32_t xr[4] = {x.x, x.y, x.z, x.w};
-      uint32_t y[4];
+    for (int e = 0; e < 8; ++e) c[e] = __uint_as_float(r[8 * j + e]);
+    if constexpr (EPI == EPI_OP_ADD) {   // C = bf16(acc + R)
+      lds_bf16x8(s0 + off, x);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float a = lo_bf16(q[k]) + lo_bf16(xr[k]), b = hi_bf16(q[k]) + hi_bf16(xr[k]);
-        y[k] = round2_pack(a, b);
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e] + x[e], b = c[e + 1] + x[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
       }
-      st_bf16x8(cp, make_uint4(q[0], q[1], q[2], q[3]), valid, true);
-      st_bf16x8(static_cast<__nv_bfloat16*>(pr.out2) + rr * pr.ld_out2 + col, make_uint4(y[0], y[1], y[2], y[3]),
-                valid, true);
+    } else if constexpr (EPI == EPI_OP_ADD2) {   // C = bf16(acc); Y = bf16(C + R)
+      lds_bf16x8(s1 + off, x);
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e], b = c[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
+        float u = a + x[e], v = b + x[e + 1];
+        p1[e / 2] = round2_bf16(u, v);
+      }
     } else if constexpr (EPI == EPI_OP_SWISH) {   // C = bf16(acc); Y = bf16(f(C)); Z = bf16(C * Y)
-      uint32_t y[4], z[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float c0 = lo_bf16(q[k]), c1 = hi_bf16(q[k]);
-        float y0 = unary_fwd(tag, c0), y1 = unary_fwd(tag, c1);
-        y[k] = round2_pack(y0, y1);
-        float z0 = c0 * y0, z1 = c1 * y1;
-        z[k] = round2_pack(z0, z1);
+      for (int e = 0; e < 8; e += 2) {
+        float a = c[e], b = c[e + 1];
+        p0[e / 2] = round2_bf16(a, b);
+        float ya = unary_fwd_t<TAG>(a), yb = unary_fwd_t<TAG>(b);
+        p1[e / 2] = round2_bf16(ya, yb);
+        float za = a * ya, zb = b * yb;
+        p2[e / 2] = round2_bf16(za, zb);
       }
-      st_bf16x8(cp, make_uint4(q[0], q[1], q[2], q[3]), valid, true);
-      st_bf16x8(static_cast<__nv_bfloat16*>(pr.out2) + rr * pr.ld_out2 + col, make_uint4(y[0], y[1], y[2], y[3]),
-                valid, true);
-      st_bf16x8(static_cast<__nv_bfloat16*>(pr.out3) + rr * pr.ld_out3 + col, make_uint4(z[0], z[1], z[2], z[3]),
-                valid, true);
-    } else {   // SWISH_BWD: C = dz*y + (dz*x)*f'(x, y), dz = bf16(acc) (never stored)
-      const uint4 xv = ld_bf16x8(static_cast<const __nv_bfloat16*>(pr.in1) + rr * pr.ld_in1 + col, valid, true);
-      const uint4 yv = ld_bf16x8(static_cast<const __nv_bfloat16*>(pr.in2) + rr * pr.ld_in2 + col, valid, true);
-      const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
-      uint32_t o[4];
+    } else {   // EPI_OP_SWISH_BWD: C = dz*y + (dz*x)*f'(x, y), dz = rounded accumulator
+      lds_bf16x8(s0 + off, x);
+      lds_bf16x8(s1 + off, y);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float g0 = lo_bf16(q[k]), g1 = hi_bf16(q[k]);
-        const float x0 = lo_bf16(xs[k]), x1 = hi_bf16(xs[k]), y0 = lo_bf16(ys[k]), y1 = hi_bf16(ys[k]);
-        float d0 = g0 * x0, d1 = g1 * x1;
-        round2_pack(d0, d1);
-        float t0 = d0 * unary_deriv(tag, x0, y0), t1 = d1 * unary_deriv(tag, x1, y1);
-        round2_pack(t0, t1);
-        float u = g0 * y0 + t0, w = g1 * y1 + t1;
-        o[k] = round2_pack(u, w);
+      for (int e = 0; e < 8; e += 2) {
+        float ga = c[e], gb = c[e + 1];
+        round2_bf16(ga, gb);
+        float da = ga * x[e], db = gb * x[e + 1];
+        round2_bf16(da, db);
+        float ta = da * unary_deriv(TAG, x[e], y[e]), tb = db * unary_deriv(TAG, x[e + 1], y[e + 1]);
+        round2_bf16(ta, tb);
+        float oa = ga * y[e] + ta, ob = gb * y[e + 1] + tb;
+        p0[e / 2] = round2_bf16(oa, ob);
       }
-      st_bf16x8(cp, make_uint4(o[0], o[1], o[2], o[3]), valid, true);
     }
+    sts_u32x4(s0 + off, p0);
+    if constexpr (EPI == EPI_OP_ADD2 || EPI == EPI_OP_SWISH) sts_u32x4(s1 + off, p1);
+    if constexpr (EPI == EPI_OP_SWISH) sts_u32x4(s2 + off, p2);
   }
 }
 
 template <int BN>
-__device__ __forceinline__ void drain_fused_box(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half,
-                                                int lane, int row0, int col0, uint8_t* buf, const float* prow) {
+__device__ __forceinline__ void drain_fused(const TcProblem& pr, uint32_t tmem_acc, int quarter, int half, int lane,
+                                            int row0, int col0, uint8_t* buf, uint32_t ld_bar0, uint32_t& ld_phase,
+                                            const float* prow) {
+  constexpr int kChunks = (BN / 2) / kFusedW;
   const uint32_t lane_base = tmem_acc + (static_cast<uint32_t>(quarter * 32) << 16) + half * (BN / 2);
   const int first = col0 + half * (BN / 2);
-  const uint32_t box = smem_u32(buf);
   const int epi = pr.epi;
-  if (epi == EPI_OP_ADD) {
-    constexpr int W = 32;   // fp32 columns per 128-byte box row
-#pragma unroll 1
-    for (int b = 0; b < (BN / 2) / W; ++b) {
-      uint32_t r[32];
-      tmem_ld32(lane_base + b * W, r);
-      if (prow) add_partial(r, prow + b * W * 128);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + swz_offset<128>(lane, j)), "r"(r[4 * j]),
-                     "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3]));
-      __syncwarp();
-      box_out_add(box, lane, pr, row0, first + b * W);
-      __syncwarp();
-    }
-    return;
+  const int n_in = epi == EPI_OP_SWISH_BWD ? 2 : ((epi == EPI_OP_ADD || epi == EPI_OP_ADD2) ? 1 : 0);
+  const bool dbl = epi != EPI_OP_SWISH;   // <= 2 slots per chunk: two slot pairs alternate
+  const uint32_t buf0 = smem_u32(buf);
+  // slot of input i / output o in slot set `set`
+  // dbl: slot pair `set`; otherwise (three outputs per chunk) `set` is the
+  // chunk index and its boxes take the next three slots of a 4-slot ring
+  auto slot = [&](int set, int k) -> uint32_t {
+    return buf0 + (dbl ? set * 2 + k : ((3 * set + k) & 3)) * kFusedBox;
+  };
+  auto in_slot = [&](int set, int i) -> uint32_t { return slot(set, epi == EPI_OP_ADD2 ? 1 : i); };
+  auto issue_loads = [&](int chunk) {   // lane 0
+    const int set = dbl ? (chunk & 1) : 0;
+    const uint32_t bar = ld_bar0 + 8 * set;
+    mbar_expect_tx(bar, n_in * kFusedBox);
+    const int x0 = first + chunk * kFusedW;
+    tma_load_2d(in_slot(set, 0), &pr.e1, bar, x0, row0);
+    if (n_in == 2) tma_load_2d(in_slot(set, 1), &pr.e2, bar, x0, row0);
+  };
+  fence_async_smem();   // a preceding plain unit's generic accesses to this box come first
+  __syncwarp();
+  if (lane == 0) {
+    bulk_wait_read0();   // the previous unit's stores have read the staging slots
+    if (n_in) issue_loads(0);
   }
-  constexpr int W = ((BN / 2) % 64 == 0) ? 64 : 32;   // bf16 columns per box row (128 or 64 bytes)
-  constexpr int kRowBytes = W * 2;
+  __syncwarp();
+  const bool tr = quarter == 0 && half == 0 && lane == 0;
+  (void)tr;
 #pragma unroll 1
-  for (int b = 0; b < (BN / 2) / W; ++b) {
-#pragma unroll
-    for (int k = 0; k < W / 32; ++k) {
-      uint32_t r[32];
-      tmem_ld32(lane_base + b * W + k * 32, r);
-      if (prow) add_partial(r, prow + (b * W + k * 32) * 128);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t p[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float a = __uint_as_float(r[8 * j + 2 * e]), c = __uint_as_float(r[8 * j + 2 * e + 1]);
-          p[e] = round2_pack(a, c);
+  for (int ch = 0; ch < kChunks; ++ch) {
+    const int set = dbl ? (ch & 1) : ch;
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(26, 1);
+    const unsigned long long t_w = gtimer();
+#endif
+    if (lane == 0) {
+      if (dbl) {
+        // the other pair was last stored from by chunk ch-1: once read out,
+        // prefetch chunk ch+1's inputs into it
+        if (ch + 1 < kChunks) {
+          bulk_wait_read0();
+          if (n_in) issue_loads(ch + 1);
         }
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(box + swz_offset<kRowBytes>(lane, k * 4 + j)),
-                     "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]));
+      } else {
+        bulk_wait_read1();   // ring: only the previous chunk's last box may still be read
       }
     }
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(22, gtimer() - t_w);
+#endif
+    uint32_t r[32];
+    HAP_ETIMED(tr, 23, tmem_ld32(lane_base + ch * kFusedW, r));
+    if (prow) add_partial(r, prow + ch * kFusedW * 128);
+    if (n_in) {
+      HAP_ETIMED(tr, 21, mbar_wait(ld_bar0 + 8 * set, (ld_phase >> set) & 1));
+      ld_phase ^= 1u << set;
+    }
     __syncwarp();
-    const int c0 = first + b * W;
-if (epi == EPI_OP_ADD2) box_out_fused<EPI_OP_ADD2, kRowBytes>(box, lane, pr, row0, c0);
-    else if (epi == EPI_OP_SWISH) box_out_fused<EPI_OP_SWISH, kRowBytes>(box, lane, pr, row0, c0);
-    else box_out_fused<EPI_OP_SWISH_BWD, kRowBytes>(box, lane, pr, row0, c0);
+#ifdef HAP_GEMM_TRACE
+    const unsigned long long t_c = gtimer();
+#endif
+    const uint32_t s0 = slot(set, 0), s1 = slot(set, 1), s2 = slot(set, 2);
+    // one dispatch per chunk: the 32 columns run a loop specialised on (op, f)
+#define HAP_FUSED_CASE(EPI, TAG) fused_chunk<EPI, TAG>(r, lane, s0, s1, s2)
+    if (epi == EPI_OP_ADD) HAP_FUSED_CASE(EPI_OP_ADD, 0);
+    else if (epi == EPI_OP_ADD2) HAP_FUSED_CASE(EPI_OP_ADD2, 0);
+    else if (epi == EPI_OP_SWISH) {
+      switch (pr.epi_tag) {
+        case HAP_SIGMOID: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_SIGMOID); break;
+        case HAP_EXP: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_EXP); break;
+        case HAP_NEG: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_NEG); break;
+        case HAP_RELU: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_RELU); break;
+        default: HAP_FUSED_CASE(EPI_OP_SWISH, HAP_TANH); break;
+      }
+    } else {
+      switch (pr.epi_tag) {
+        case HAP_SIGMOID: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_SIGMOID); break;
+        case HAP_EXP: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_EXP); break;
+        case HAP_NEG: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_NEG); break;
+        case HAP_RELU: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_RELU); break;
+        default: HAP_FUSED_CASE(EPI_OP_SWISH_BWD, HAP_TANH); break;
+      }
+    }
+#undef HAP_FUSED_CASE
+    fence_async_smem();
     __syncwarp();
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(24, gtimer() - t_c);
+    const unsigned long long t_i = gtimer();
+#endif
+    if (lane == 0) {
+      const int x0 = first + ch * kFusedW;
+      tma_store_2d(&pr.c, slot(set, 0), x0, row0);
+      if (epi == EPI_OP_ADD2) tma_store_2d(&pr.e2, slot(set, 1), x0, row0);
+      if (epi == EPI_OP_SWISH) {   // one bulk group per box (ring slots free up one by one)
+        bulk_commit();
+        tma_store_2d(&pr.e1, slot(set, 1), x0, row0);
+        bulk_commit();
+        tma_store_2d(&pr.e2, slot(set, 2), x0, row0);
+      }
+      bulk_commit();
+    }
+#ifdef HAP_GEMM_TRACE
+    if (tr) trace_add(25, gtimer() - t_i);
+#endif
   }
+  // a following unit may be unfused: its staging boxes overlap these slots
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
 }
 
 // Epilogue of one unit for one warp: drain the accumulator into C, or (split
@@ -772,11 +794,9 @@ __device__ __forceinline__ void epilogue_unit(const TcProblem& pr, uint32_t tmem
   // part: stream-K partial of this CTA's 128 x BN share (column-major), added to
   // the accumulator before anything is rounded
   const float* prow = part ? part + (half * (BN / 2)) * 128 + quarter * 32 + lane : nullptr;
-  (void)ld_bar;
-  (void)ld_phase;
   if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
     if (pr.epi != EPI_OP_NONE) {
-      drain_fused_box<BN>(pr, tmem_acc, quarter, half, lane, row0, col0, buf, prow);
+      drain_fused<BN>(pr, tmem_acc, quarter, half, lane, row0, col0, buf, ld_bar, ld_phase, prow);
       return;
     }
   }
@@ -1707,7 +1727,9 @@ hap_status launch_batch(K kern, int smem_bytes, const TcBatch& bt, int grid, cud
 template <int BN, bool kAMN, bool kBMN, typename OutT>
 hap_status launch_shape(bool pair, const TcBatch& bt_in, int cap, cudaStream_t stream) {
   TcBatch bt = bt_in;
-  bt.box_bytes = kEpiBoxBytes;
+  bool fused = false;
+  for (int q = 0; q < bt.count; ++q) fused = fused || bt.p[q].epi != EPI_OP_NONE;
+  bt.box_bytes = fused ? kEpiBoxBytesFused : kEpiBoxBytes;
   if (pair || BN == 192) {   // 192-wide tiles exist only for SM pairs
     using G = Cfg2<BN, kBMN>;
     bt.nst = stages_for(G::kStageBytes, bt.box_bytes);
@@ -2351,7 +2373,7 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
                     "hap_matmul: the fused swish adjoint writes C (no accumulate)");
       auto map = [&](CUtensorMap* m, const void* ptr, int64_t ld, const char* what) -> bool {
         if (ptr == nullptr ||
-            !tc::make_map_c(m, const_cast<void*>(ptr), HAP_BF16, out.N, out.M, ld, shp.bn, 32)) {
+            !tc::make_map_c(m, const_cast<void*>(ptr), HAP_BF16, out.N, out.M, ld, shp.bn, tc::kFusedW)) {
           set_error(std::string("hap_matmul: fused epilogue tensor ") + what +
                     " is null or not 16-byte aligned / pitched");
           return false;
@@ -2364,22 +2386,6 @@ hap_status tc_batch(const hap_gemm_desc* d, int count, int sum_k, hap_dtype out_
       if (epi == HAP_EPI_SWISH) ok = ok && map(&pr.e1, out.Y, out.ldy, "Y") && map(&pr.e2, out.Z, out.ldz, "Z");
       if (epi == HAP_EPI_SWISH_BWD) ok = ok && map(&pr.e1, R, ldr, "R") && map(&pr.e2, out.R2, out.ldr2, "R2");
       if (!ok) return HAP_ERR_ARG;
-      if (epi == HAP_EPI_ADD || epi == HAP_EPI_ADD2 || epi == HAP_EPI_SWISH_BWD) {
-        pr.in1 = R;
-        pr.ld_in1 = ldr;
-      }
-      if (epi == HAP_EPI_SWISH_BWD) {
-        pr.in2 = out.R2;
-        pr.ld_in2 = out.ldr2;
-      }
-      if (epi == HAP_EPI_ADD2 || epi == HAP_EPI_SWISH) {
-        pr.out2 = out.Y;
-        pr.ld_out2 = out.ldy;
-      }
-      if (epi == HAP_EPI_SWISH) {
-        pr.out3 = out.Z;
-        pr.ld_out3 = out.ldz;
-      }
       pr.accumulate = 0;
       pr.epi_mode = tc::EPI_TMA_STORE;
     } else if (pr.vec_ok && tma_epilogue() && (!pr.accumulate || fp32) &&
