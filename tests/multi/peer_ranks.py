@@ -153,7 +153,11 @@ def _install_watchdog(args):
                 trace = LIVE[r].__dict__.get("op_trace", [])
                 lo = max(0, (first or 0) - 4)
                 print(f"[watchdog]   ops {lo}..: {[w for w, _ in trace[lo:(first or 0) + 3]]}", flush=True)
-            _dump_signal_pages()
+            # the page dump goes through the CUDA runtime, which a stalled
+            # GPU can block: bounded, then exit regardless
+            dumper = threading.Thread(target=_dump_signal_pages, daemon=True)
+            dumper.start()
+            dumper.join(10)
             print(f"[watchdog] GPU utilisation {util}; exiting", flush=True)
             os._exit(3)
 
