@@ -26,7 +26,7 @@ def test_peer_ranks_in_one_process_match_oracle():
     can stall ("Ranks as threads on one GPU": a rank's plain kernel
     sometimes never starts while its partner's peer kernel waits for it); the
     script's watchdog then exits, the stalled run is reported, and the sweep
-    resumes in a fresh process after it.  At most one run in ten may stall —
+    resumes in a fresh process after it.  At most one run in five may stall —
     the same programs run one process per GPU in tests/multi/nccl_parity.py."""
     script = os.path.join(HERE, "multi", "peer_ranks.py")
     start, stalled, done = 1, [], 0
