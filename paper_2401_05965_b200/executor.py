@@ -343,13 +343,16 @@ class Op:
 
 # ---------------------------------------------------------------------------- executor
 
-def price_grad_sync(spec, ratios, weight: str, kdim: int, ndim: int, uses) -> str:
+def price_grad_sync(spec, ratios, weight: str, kdim: int, ndim: int, uses, shared: dict | None = None) -> str:
     """HAP's SFB rule for one replicated [kdim, ndim] weight whose uses are
     row-sharded matmuls ``(x_ref, y_ref, rows)``: all-reduce the partial dW
     (plus the ratio-sharded dW GEMMs) against all-gathering x and dy and
     rebuilding dW at full batch on every device — each priced with the
     reference cost model's collective times (cost_model.comm_time) and the
-    slowest device's GEMM time.  Returns "sfb" or "all_reduce"."""
+    slowest device's GEMM time.  ``shared`` maps a factor to the number of
+    weights whose SFB reuses its one gather (the executor gathers a factor
+    once per source buffer: both experts of a layer read the same input), so
+    each weight is charged its share.  Returns "sfb" or "all_reduce"."""
     from .cost_model import ClusterSpec, comm_time
 
     if not isinstance(spec, ClusterSpec):
@@ -360,7 +363,8 @@ def price_grad_sync(spec, ratios, weight: str, kdim: int, ndim: int, uses) -> st
     t_sfb = 0.0
     for x_ref, y_ref, rows in uses:
         flops = 2 * rows * kdim * ndim
-        t_sfb += comm_time(Instruction("all_gather", x_ref, elements=rows * kdim), row, spec)
+        t_sfb += comm_time(Instruction("all_gather", x_ref, elements=rows * kdim), row, spec) / \
+            max(1, (shared or {}).get(x_ref, 1))
         t_sfb += comm_time(Instruction("all_gather", y_ref, elements=rows * ndim), row, spec)
         # SFB replicates the weight-gradient GEMM at full batch on every device;
         # all-reduce keeps it sharded.
@@ -935,7 +939,7 @@ class Executor:
                 self._block(chunk, _view(recv_shapes[k], d1), 0, dst[r], _view(dst[r].shape, d1), off1[k],
                             sizes1[k], self.caps[r], accumulate)
 
-    def _use_p2p(self, kind: str, elements: int, esize: int) -> bool:
+    def _use_p2p(self, kind: str, elements: int, esize: int, side: bool = False) -> bool:
         """Hand-written NVLink kernel (True) or NCCL (False) for one call site.
 
         A PeerGroup has only the kernels; ``gather`` forces one side.
@@ -964,6 +968,14 @@ class Executor:
         row = tuple(self.cfg.ratios) if self.cfg.ratios else tuple(c / sum(caps) for c in caps)
         ins = Instruction("all_gather" if kind == "grouped_broadcast" else kind, "t", elements=int(elements))
         t_p2p, t_nccl = comm_time(ins, row, specs["p2p"]), comm_time(ins, row, specs["nccl"])
+        if side or getattr(self, "_emit_on", None) is not None:
+            # the kernel's line was fitted at the rank's full SM cap; on the side
+            # stream it runs with at most SIDE_P2P_CTAS CTAs, and its bandwidth
+            # scales with the CTAs moving data (each keeps a fixed number of
+            # NVLink requests in flight)
+            cap = self.caps[self.group.rank] or 148
+            t0 = comm_time(Instruction(ins.kind, "t", elements=0), row, specs["p2p"])
+            t_p2p = t0 + (t_p2p - t0) * max(1.0, cap / self.SIDE_P2P_CTAS)
         use = t_p2p <= t_nccl
         self.impl_choice.append((kind, elements * esize, "p2p" if use else "nccl", t_p2p, t_nccl))
         return use
@@ -1846,6 +1858,7 @@ class Executor:
         for ins in self.program.instrs:
             for d in ins.operands:
                 uses.setdefault(d, []).append(ins)
+        eligible = []
         for ins in self.program.instrs:
             if ins.kind != "parameter" or not self.req.get(ins.output):
                 continue
@@ -1854,8 +1867,14 @@ class Executor:
                                   and form_of_dist_id(u.operands[0]).kind == ALL_GATHER
                                   and form_of_dist_id(u.operands[0]).axis == 0
                                   and form_of_dist_id(u.output).kind == ALL_GATHER for u in us)
-            if not ok:
-                continue
+            if ok:
+                eligible.append((ins, us))
+        # weights per activation factor: one gather serves all of them (_sfb_factor)
+        self._sfb_shared: dict[str, int] = {}
+        for _, us in eligible:
+            for x in {u.operands[0].split("@")[0] for u in us}:
+                self._sfb_shared[x] = self._sfb_shared.get(x, 0) + 1
+        for ins, us in eligible:
             choice = self.cfg.grad_sync if self.cfg.grad_sync != "auto" else self._price_sync(ins, us)
             self.sync_choice[ins.ref] = choice
             if choice == "sfb":
@@ -1868,7 +1887,8 @@ class Executor:
         kdim, ndim = self.source_shapes[pins.ref]
         use_rows = [(u.operands[0].split("@")[0], u.ref, sum(s[0] for s in self.shapes[u.operands[0]]))
                     for u in uses]
-        return price_grad_sync(spec, self.cfg.ratios, pins.ref, kdim, ndim, use_rows)
+        return price_grad_sync(spec, self.cfg.ratios, pins.ref, kdim, ndim, use_rows,
+                               shared=getattr(self, "_sfb_shared", None))
 
     def _sfb_overlap(self) -> bool:
         g = self.group
@@ -2024,7 +2044,7 @@ class Executor:
             ptr = flat.data_ptr() + lo * 4
             inserted = [Op(ev.record, (self.stream,), "event.record", False),
                         Op(self.comm_stream.wait_event, (ev,), "stream.wait_event", False)]
-            if g.comm_grad is not None and not self._use_p2p("all_reduce", hi - lo, 4):
+            if g.comm_grad is not None and not self._use_p2p("all_reduce", hi - lo, 4, side=True):
                 inserted.append(Op(self.lib.hap_all_reduce, (g.comm_grad, ptr, ptr, hi - lo, F32,
                                                              self.comm_stream.cuda_stream), "hap_all_reduce", False))
             else:   # in place on the registered bucket, P2P kernel on the side stream

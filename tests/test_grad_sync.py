@@ -11,22 +11,31 @@ from paper_2401_05965_b200.executor import price_grad_sync
 from paper_2401_05965_b200.program import DistributedProgram
 
 
-def _choice(n, tokens_per_gpu, kdim=768, ndim=3072):
+def _choice(n, tokens_per_gpu, kdim=768, ndim=3072, shared=1):
     spec = ClusterSpec.from_dict(workloads.cluster_doc(workloads.sm_caps(n)))
-    return price_grad_sync(spec, None, "W", kdim, ndim, [("x", "y", tokens_per_gpu * n)])
+    return price_grad_sync(spec, None, "W", kdim, ndim, [("x", "y", tokens_per_gpu * n)], shared={"x": shared})
 
 
 @pytest.mark.parametrize("n,tokens,want", [(2, 256, "sfb"), (4, 256, "all_reduce"), (8, 256, "all_reduce"),
                                            (2, 1024, "all_reduce"), (2, 8192, "all_reduce")])
 def test_sfb_rule_on_b200_clusters(n, tokens, want):
-    # The MoE bench (2 sequences x 128 tokens per GPU) and the BERT bench
-    # (64 x 128) sit on either side of the crossover.  At 4 GPUs the fitted
-    # collective lines (collectives_b200.json) price the all-reduce below the
-    # two factor gathers — as measured: BERT-MoE N=4 all-reduce 2,580 vs SFB
-    # 2,415 samples/s; at 2 GPUs SFB 2,148 vs all-reduce 1,665
-    # (profiles/r02_multi_n2.md, r02_multi_n4.md).
-    assert _choice(n, tokens) == want
-    assert _choice(n, tokens, 3072, 768) == want
+    # A BERT-MoE expert up-projection W1 [768, 3072] whose input x is shared
+    # with the other expert of its layer (one gather serves both).  The MoE
+    # bench (2 sequences x 128 tokens per GPU) and the BERT bench (64 x 128)
+    # sit on either side of the crossover.  With the collective lines fitted
+    # at 2 and 4 GPUs (collectives_b200.json): SFB at 2, all-reduce at 4 —
+    # as measured: BERT-MoE N=2 SFB 2,148 vs all-reduce 1,665 samples/s, N=4
+    # all-reduce 2,580 vs SFB 2,415 (profiles/r02_multi_n2.md, r02_multi_n4.md).
+    assert _choice(n, tokens, shared=2) == want
+
+
+def test_sfb_charges_a_shared_gather_once():
+    # Without the sharing, the same weight's two factor gathers price above
+    # the all-reduce at 2 GPUs; the down-projection W2 [3072, 768] (its input
+    # is the expert's own activation) stays on the all-reduce.
+    assert _choice(2, 256, shared=1) == "all_reduce"
+    assert _choice(2, 256, shared=2) == "sfb"
+    assert _choice(2, 256, 3072, 768) == "all_reduce"
 
 
 def test_sfb_wins_for_the_small_batch_mlp():
@@ -38,8 +47,8 @@ def test_sfb_wins_for_the_small_batch_mlp():
 def test_sfb_price_grows_with_uses():
     # A weight used by several row-sharded matmuls gathers factors for each use.
     spec = ClusterSpec.from_dict(workloads.cluster_doc(workloads.sm_caps(2)))
-    one = price_grad_sync(spec, None, "W", 768, 3072, [("x", "y", 512)])
-    many = price_grad_sync(spec, None, "W", 768, 3072, [("x", "y", 512)] * 4)
+    one = price_grad_sync(spec, None, "W", 768, 3072, [("x", "y", 512)], shared={"x": 2})
+    many = price_grad_sync(spec, None, "W", 768, 3072, [("x", "y", 512)] * 4, shared={"x": 2})
     assert one == "sfb" and many == "all_reduce"
 
 
