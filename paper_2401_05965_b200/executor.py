@@ -973,7 +973,8 @@ class Executor:
             # stream it runs with at most SIDE_P2P_CTAS CTAs, and its bandwidth
             # scales with the CTAs moving data (each keeps a fixed number of
             # NVLink requests in flight)
-            cap = self.caps[self.group.rank] or 148
+            # (the same factor on every rank: the choice must agree across ranks)
+            cap = max(c or 148 for c in self.caps)
             t0 = comm_time(Instruction(ins.kind, "t", elements=0), row, specs["p2p"])
             t_p2p = t0 + (t_p2p - t0) * max(1.0, cap / self.SIDE_P2P_CTAS)
         use = t_p2p <= t_nccl
@@ -1143,6 +1144,9 @@ class Executor:
                   "hap_p2p_buffer_handle")
             mine.append((bytes(h.raw), base.value, off.value))
         everyone = g.exchange(mine)
+        if len({len(x) for x in everyone}) != 1:
+            raise ExecutionError(f"ranks registered {[len(x) for x in everyone]} peer-memory buffers: their "
+                                 "collective implementation choices disagree")
         for i, (tag, buf, reg) in enumerate(self._p2p_regs):
             handles = b"".join(everyone[p][i][0] for p in range(g.m))
             bases = _lib.i64_array([everyone[p][i][1] for p in range(g.m)])
