@@ -26,7 +26,7 @@ import torch.multiprocessing as mp
 HERE = os.path.dirname(os.path.abspath(__file__))
 WORLD = 2
 VARIANTS_ALL = [("sendrecv", "all_reduce"), ("kernel", "sfb")]
-VARIANTS_SOME = [("padded", "all_reduce"), ("kernel", "all_reduce"), ("sendrecv", "sfb")]
+VARIANTS_SOME = [("padded", "all_reduce"), ("kernel", "all_reduce"), ("sendrecv", "sfb"), ("auto", "auto")]
 
 
 def _free_port() -> int:
@@ -58,6 +58,8 @@ def _work(rank, port, out_dir):
     from paper_2401_05965_b200.executor import ExecConfig, Executor, NcclGroup
     from paper_2401_05965_b200.program import DistributedProgram
     from paper_2401_05965_b200.sharding import table_from_plan
+    from paper_2401_05965_b200 import workloads
+    from paper_2401_05965_b200.cost_model import ClusterSpec
 
     class HostNcclGroup(NcclGroup):
         """Placeholder communicators: the compile path only passes them on."""
@@ -75,8 +77,13 @@ def _work(rank, port, out_dir):
         refs = {n.id for n in g.sources()}
         for gather, sync in VARIANTS_ALL + (VARIANTS_SOME if i % 4 == 0 else []):
             label = f"{name} {gather} {sync}"
+            # "auto": per-call-site NCCL-vs-kernel and SFB-vs-all-reduce choices from the fitted lines on
+            # heterogeneous SM caps — every rank must make the same choices
+            extra = dict(sm_caps=[148, 104], cluster=ClusterSpec.from_dict(workloads.cluster_doc([148, 104]))) \
+                if gather == "auto" else {}
             ex = Executor(DistributedProgram.from_json(doc["program"]), WORLD, table_from_plan(doc), shapes,
-                          group=group, config=ExecConfig(dtype="fp32", input_grads=True, gather=gather, grad_sync=sync),
+                          group=group, config=ExecConfig(dtype="fp32", input_grads=True, gather=gather, grad_sync=sync,
+                                                         **extra),
                           device=torch.device("cpu"))
             ex.load(inputs)
             runner = cpu_exec.step(ex)
