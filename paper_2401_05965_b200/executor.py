@@ -957,6 +957,16 @@ class Executor:
             return True
         if self.cfg.gather in ("padded", "sendrecv", "nccl") or not self._peer_access():
             return False
+        if side or getattr(self, "_emit_on", None) is not None:
+            # side-stream call sites (SFB factor gathers, gradient buckets): the
+            # fitted lines were measured with the compute stream idle and do not
+            # predict these — measured at 2 GPUs, SFB with the push kernel 2,148
+            # samples/s vs NCCL gathers 1,581; bucketed all-reduce over NCCL
+            # 1,662 vs the two-shot kernel (32 CTAs) 1,003 — so gathers take the
+            # kernel and all-reduces NCCL
+            use = kind in ("all_gather", "grouped_broadcast")
+            self.impl_choice.append((kind, elements * esize, "p2p" if use else "nccl", None, None))
+            return use
         specs = self._impl_specs(esize)
         if specs is None:
             use = kind in ("all_gather", "grouped_broadcast", "reduce_scatter")
@@ -968,15 +978,6 @@ class Executor:
         row = tuple(self.cfg.ratios) if self.cfg.ratios else tuple(c / sum(caps) for c in caps)
         ins = Instruction("all_gather" if kind == "grouped_broadcast" else kind, "t", elements=int(elements))
         t_p2p, t_nccl = comm_time(ins, row, specs["p2p"]), comm_time(ins, row, specs["nccl"])
-        if side or getattr(self, "_emit_on", None) is not None:
-            # the kernel's line was fitted at the rank's full SM cap; on the side
-            # stream it runs with at most SIDE_P2P_CTAS CTAs, and its bandwidth
-            # scales with the CTAs moving data (each keeps a fixed number of
-            # NVLink requests in flight)
-            # (the same factor on every rank: the choice must agree across ranks)
-            cap = max(c or 148 for c in self.caps)
-            t0 = comm_time(Instruction(ins.kind, "t", elements=0), row, specs["p2p"])
-            t_p2p = t0 + (t_p2p - t0) * max(1.0, cap / self.SIDE_P2P_CTAS)
         use = t_p2p <= t_nccl
         self.impl_choice.append((kind, elements * esize, "p2p" if use else "nccl", t_p2p, t_nccl))
         return use
