@@ -613,7 +613,24 @@ extern "C" hap_status hap_symm_create(void** out, int64_t bytes, int rank, int n
     set_error(std::string("hap_symm_create: cudaMalloc: ") + cudaGetErrorString(e));
     return HAP_ERR_CUDA;
   }
-  HAP_CUDA_TRY(cudaMemset(s->local, 0, kSignalBytes));
+  // The signal page must be zero before any peer can see this arena and
+  // before this rank's first peer kernel: a plain cudaMemset runs on the
+  // legacy stream, which does not order against the executor's non-blocking
+  // streams, so a fresh process's first collective could read a stale epoch
+  // or have its peers' first flags wiped — both ranks then wait inside the
+  // same collective forever (tests/multi/peer_ranks.py, first run of a
+  // process).  Zero it on a private stream and wait for it here.
+  cudaStream_t st = nullptr;
+  HAP_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  e = cudaMemsetAsync(s->local, 0, kSignalBytes, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) {
+    cudaFree(s->local);
+    delete s;
+    set_error(std::string("hap_symm_create: zeroing the signal page: ") + cudaGetErrorString(e));
+    return HAP_ERR_CUDA;
+  }
   s->peers[rank] = s->local;
   *out = s;
   return HAP_OK;

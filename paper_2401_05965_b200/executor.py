@@ -443,6 +443,11 @@ class Executor:
         if self.wdt == BF16 and not self.dry:
             self._autotune()
         self._create_symm()
+        if not self.dry:
+            # compile-time initialisation (zeroed gradient buckets, tuning
+            # launches) ran on torch's streams, which the executor's own
+            # non-blocking stream does not wait for
+            torch.cuda.synchronize(self.device)
 
     def _stream(self):
         """A CUDA stream no other live executor uses (non-blocking): torch's
@@ -2263,6 +2268,10 @@ class Executor:
                 buf.tensor[:part.numel()].copy_(part.reshape(-1).to(self.device), non_blocking=False)
                 if (ins.output, r) in self.masters:
                     self.masters[(ins.output, r)].tensor[:part.numel()].copy_(part.reshape(-1).to(self.device))
+        # the copies ran on torch's current stream, which the executor's own
+        # (non-blocking) stream does not wait for: done before the next step
+        if not self.dry:
+            torch.cuda.current_stream(self.device).synchronize()
 
     def source_buffers(self, ref: str) -> dict[int, tuple[Instruction, Buf]]:
         out = {}
