@@ -1,4 +1,6 @@
-O=gpurun_out/v15
+# One 1-GPU verification session: the GPU test suite, smoke(), the bench lines of
+# every workload and the reference arm.  Outputs in gpurun_out/verify/.
+O=gpurun_out/verify
 mkdir -p $O
 timeout 2700 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=10 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt
